@@ -1,0 +1,240 @@
+/*
+ * tlru.h -- C ABI of libtlru, the B200-native (sm_100a) hot path of
+ * arXiv 2510.15152 "Tail-Optimized LRU": batched trace-driven simulation of
+ * prompt-cache (KV prefix) eviction under LRU and T-LRU over multi-turn
+ * conversation traces.
+ *
+ * Citations: P:NNN = PAPER.md line NNN with its section / equation / algorithm.
+ * "Reading #k" = DESIGN.md "Readings of the paper" item k.
+ *
+ * Conventions for every call
+ *   * Pointers are caller-owned DEVICE memory unless marked "host".  The library
+ *     never allocates device memory; scratch comes from the caller's workspace
+ *     `ws` (size it with the matching *_workspace_size call; ws must be
+ *     256-byte aligned).  `ws == NULL` with a non-zero requirement is TLRU_ERANGE.
+ *   * Calls are asynchronous on `stream` unless marked "synchronizes".  Outputs
+ *     are valid once the stream is synchronized.  Distinct streams are
+ *     thread-safe; one stream must not be used from two threads at once.
+ *   * No C++ exception crosses the ABI.  On a non-OK status, tlru_last_error()
+ *     returns a thread-local message naming the offending argument / index;
+ *     outputs are then unspecified.
+ *   * Integers are the contract: uncached-block counts, evictions, TEL in
+ *     blocks, SLO counts and percentiles (in blocks) are exact.  Floating point
+ *     appears only in tlru_tail's millisecond fields, derived from integers.
+ *   * Determinism: identical inputs give identical output bytes for any launch
+ *     configuration and any number of GPUs.
+ */
+#ifndef TLRU_H_
+#define TLRU_H_
+
+#include <stddef.h>
+#include <stdint.h>
+#include <cuda_runtime.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TLRU_NONE 0xFFFFFFFFu /* "no previous / next turn" in prev/next links */
+
+typedef enum {
+  TLRU_OK = 0,
+  TLRU_EINVAL = 1,       /* bad argument or configuration (block_tokens == 0, rate <= 0, q == 0, ...) */
+  TLRU_ERANGE = 2,       /* buffer / workspace too small, or a value exceeds its field width (J > 65535) */
+  TLRU_ECUDA = 3,        /* CUDA runtime error; tlru_last_error() carries cudaGetErrorString */
+  TLRU_EUNSUPPORTED = 4, /* policy family not built (THRESHOLD, END_AWARE, LENGTH_AWARE, TAIL_BELADY) */
+  TLRU_ESTATE = 5        /* internal per-chain state pool exhausted with no fallback left */
+} tlru_status;
+
+/* Thread-local message for the last non-OK status of this thread ("" if none). */
+const char* tlru_last_error(void);
+
+/* Library version string, e.g. "tlru 0.1 sm_100a". */
+const char* tlru_version(void);
+
+/* ------------------------------------------------------------------------
+ * Synthetic traces: the paper's stochastic conversation model (Sec. 5)
+ *   - conversations are born by a Poisson(birth_rate) process;
+ *   - each conversation lives an Exp(death_rate) time;
+ *   - while alive it issues turns by a Poisson(turn_rate) process;
+ *     the first turn is at birth (Reading #18);
+ *   - each turn draws a prompt length Q and a response length A,
+ *     here lognormal in tokens, quantized to blocks of `block_tokens`
+ *     (q = max(1, ceil(tokens/B)), a = ceil(tokens/B); Reading #16);
+ *   - a turn whose history would exceed max_history_blocks ends the
+ *     conversation (context window), as does max_turns.
+ * App. E's recipe is the ShareGPT preset.  Random numbers come from
+ * Philox4x64-10 keyed by (seed, tag) with counter (conv, turn, field|attempt<<8, 0),
+ * so a trace is a pure function of its parameters (Reading #16).  Time is kept
+ * in integer microsecond ticks; events are ordered by (tick, conv, turn).
+ * ------------------------------------------------------------------------ */
+typedef struct {
+  uint64_t seed;
+  uint32_t num_conversations;    /* N >= 1 */
+  uint32_t block_tokens;         /* tokens per KV block (128 in the BASELINE configs); 0 -> EINVAL */
+  double birth_rate;             /* lambda_conv > 0, per second */
+  double turn_rate;              /* lambda_turn > 0, per second, homogeneous */
+  double death_rate;             /* mu > 0, per second; mean turns = 1 + turn_rate / death_rate */
+  double prompt_mean_tokens;     /* lognormal mean > 0 (WildChat: 200) */
+  double prompt_sigma_ln;        /* lognormal sigma of ln(tokens) >= 0 */
+  double response_mean_tokens;   /* lognormal mean > 0 (paper silent; A is arbitrary) */
+  double response_sigma_ln;      /* >= 0 */
+  uint32_t prompt_min_tokens;    /* clip range for prompt tokens */
+  uint32_t prompt_max_tokens;
+  uint32_t response_min_tokens;  /* clip range for response tokens */
+  uint32_t response_max_tokens;
+  uint32_t max_history_blocks;   /* context cap L_max in blocks, 1..65535 */
+  uint32_t max_turns;            /* hard cap on turns per conversation, 1..65535 */
+} tlru_gen_params;
+
+/* One event-ordered trace (conversation i issues requests at
+ * disjoint times T_i; q_{i,t}, a_{i,t} in blocks).  Event index = tau. */
+typedef struct {
+  uint64_t capacity;    /* in:  allocated length of every non-NULL array below */
+  uint64_t num_events;  /* out: E */
+  uint32_t max_history; /* out: max over events of L_after (bounds every J and every b) */
+  uint32_t num_conversations; /* out: number of distinct conversation ids */
+  uint64_t* sim;        /* [E] required.  Simulation view, 8 B per request:
+                             bits  0..31 prev = event index of the same conversation's previous
+                                         turn, or TLRU_NONE for a first turn
+                             bits 32..47 J = L_before + q   (job size)
+                             bits 48..63 L_after = J + a    (history after the turn, Reading #6) */
+  uint32_t* next;       /* [E] required: event index of the next turn of the same conversation,
+                             TLRU_NONE if none (used to rebuild cache state at segment starts) */
+  uint32_t* conv;       /* [E] nullable export: conversation id (dense, birth order for generated traces) */
+  uint16_t* prompt;     /* [E] nullable export: q blocks >= 1 */
+  uint16_t* response;   /* [E] nullable export: a blocks >= 0 */
+  uint64_t* time_ticks; /* [E] nullable export: arrival time in microseconds (generated traces) */
+  uint8_t* is_last;     /* [E] nullable export: 1 on a conversation's last turn */
+} tlru_trace;
+
+/* Host: upper bound N * max_turns on the events of a generated trace. */
+tlru_status tlru_trace_max_events(const tlru_gen_params* p /*host*/, uint64_t* out /*host*/);
+
+/* Host: workspace bytes for tlru_count_events / tlru_generate_traces of one trace
+ * with N conversations whose trace arrays have `capacity` entries. */
+tlru_status tlru_gen_workspace_size(const tlru_gen_params* p /*host*/, uint64_t capacity,
+                                    size_t* bytes /*host*/);
+
+/* Exact event count of the trace `p` describes.  Synchronizes `stream`. */
+tlru_status tlru_count_events(const tlru_gen_params* p /*host*/, uint64_t* out /*host*/, void* ws,
+                              size_t ws_bytes, cudaStream_t stream);
+
+/* Generate n traces (one per params entry) into traces[i] (host structs holding
+ * device arrays).  capacity < E -> TLRU_ERANGE.  Fills num_events, max_history
+ * and num_conversations.  Synchronizes `stream` once per trace (to read E). */
+tlru_status tlru_generate_traces(const tlru_gen_params* p /*host[n]*/, uint32_t n,
+                                 tlru_trace* traces /*host[n]*/, void* ws, size_t ws_bytes,
+                                 cudaStream_t stream);
+
+/* Host: workspace bytes for tlru_trace_from_turns with E requests. */
+tlru_status tlru_upload_workspace_size(uint64_t E, size_t* bytes /*host*/);
+
+/* Build the simulation view of an uploaded trace.  conv/q/a are DEVICE arrays
+ * in event (time) order; conversation ids are arbitrary u32 except TLRU_NONE.
+ * The library derives prev, next, J = L_before + q and L_after = J + a
+ * and fills out->sim / out->next, copying the non-NULL export arrays.
+ * q == 0 -> TLRU_EINVAL; J or L_after > 65535 -> TLRU_ERANGE (offending event index
+ * in tlru_last_error()).  E == 0 is valid.  Synchronizes `stream`. */
+tlru_status tlru_trace_from_turns(const uint32_t* conv, const uint16_t* q, const uint16_t* a, uint64_t E,
+                                  tlru_trace* out /*host struct, device arrays*/, void* ws,
+                                  size_t ws_bytes, cudaStream_t stream);
+
+/* ------------------------------------------------------------------------
+ * Batched simulation: Alg. 1 per instance.
+ * Per request of conversation theta: b = J - X_theta (uncached blocks,
+ * P:154-156); then X_theta <- L_after (optional caching caches the whole
+ * history, Reading #7), tau_theta <- now; if sum X > C:
+ *   Phase 1 (T-LRU only): evict TEL-safe ("infinitely old", P:62,
+ *     P:225) blocks, i.e. each conversation's blocks above its budget
+ *     (L + Q_hat - xi)^+ (P:56), oldest tau first, theta last, as many
+ *     as needed (Readings #1-#5);
+ *   Phase 2: evict from the least recently used conversation,
+ *     partially, tail blocks first (Reading #10).
+ * LRU = Phase 2 only.  xi and Q_hat are in blocks (xi = xi_s / alpha).
+ * ------------------------------------------------------------------------ */
+enum {
+  TLRU_POLICY_LRU = 0,
+  TLRU_POLICY_TLRU = 1
+  /* 2..5 reserved: THRESHOLD_LRU, END_AWARE, LENGTH_AWARE, TAIL_BELADY -> TLRU_EUNSUPPORTED */
+};
+
+typedef struct {
+  uint32_t trace;    /* index into traces[] */
+  uint32_t policy;   /* TLRU_POLICY_* */
+  uint32_t capacity; /* C in blocks, >= 0 */
+  uint32_t xi;       /* xi in blocks: T-LRU threshold and TEL threshold (Eq. 3) */
+  uint32_t q_hat;    /* Q_hat in blocks, next-prompt estimate */
+  uint32_t slo;      /* SLO violation iff b > slo (strict); 16 = 200 ms at 12.5 ms/block */
+} tlru_instance;
+
+typedef struct { /* 64 B, all exact integers */
+  uint64_t requests;       /* E of the instance's trace */
+  uint64_t sum_uncached;   /* sum b */
+  uint64_t tel_blocks;     /* sum max(b - xi, 0)  (Eq. 3) */
+  uint64_t slo_violations; /* #{b > slo} */
+  uint64_t evicted_trim;   /* blocks evicted by Phase 1 */
+  uint64_t evicted_lru;    /* blocks evicted by Phase 2 */
+  uint32_t p50, p90, p95, p99;            /* nearest-rank percentiles of b (Reading #11) */
+  uint32_t max_uncached, max_occupancy;   /* max b; max sum X after a request (<= capacity) */
+} tlru_result;
+
+/* Host: workspace bytes for tlru_simulate_batch on these traces / instances. */
+tlru_status tlru_sim_workspace_size(const tlru_trace* traces /*host[nt]*/, uint32_t nt,
+                                    const tlru_instance* inst /*host[ni]*/, uint32_t ni,
+                                    size_t* bytes /*host*/);
+
+/* Simulate ni instances.  inst is a HOST array (the launch planner groups
+ * instances by trace and capacity class).  uncached (device, u16) receives
+ * instance i's per-request b at uncached[offsets[i] .. offsets[i] + E_i);
+ * offsets is a host array, or NULL for packed offsets (prefix sums of E_i).
+ * results (device[ni]) receives one tlru_result per instance.
+ * Unknown policy -> TLRU_EUNSUPPORTED; trace index out of range -> TLRU_EINVAL.
+ * Does not synchronize unless a chain overflows its on-chip state, in which case
+ * the library re-runs that chain from global memory (counted, never truncated). */
+tlru_status tlru_simulate_batch(const tlru_trace* traces /*host[nt]*/, uint32_t nt,
+                                const tlru_instance* inst /*host[ni]*/, uint32_t ni, uint16_t* uncached,
+                                const uint64_t* offsets /*host[ni] or NULL*/, tlru_result* results, void* ws,
+                                size_t ws_bytes, cudaStream_t stream);
+
+/* Statistics of the last tlru_simulate_batch on this thread (host). */
+typedef struct {
+  uint64_t chains;          /* instance x segment work units launched */
+  uint64_t segment_events;  /* events per segment */
+  uint64_t warm_events;     /* events walked to rebuild segment-start states */
+  uint64_t spilled_chains;  /* chains re-run with global-memory state */
+  uint32_t kernels;         /* kernel launches issued */
+  uint32_t reserved;
+} tlru_sim_stats;
+tlru_status tlru_last_sim_stats(tlru_sim_stats* out /*host*/);
+
+/* ------------------------------------------------------------------------
+ * Tail metrics over request segments (Eq. 1-3).
+ * Segment s covers b[seg_offsets[s] .. seg_offsets[s+1]).
+ *   TEL_blocks = sum max(b - xi, 0); TEL_ms = sum max(alpha*b - xi_ms, 0) (summed
+ *   over b in ascending order, double); SLO = #{b > slo};
+ *   p-th percentile: nearest rank k = max(1, ceil(p * n / 100)) on sorted b
+ *   (integer arithmetic, p in {50, 90, 95, 99}; Reading #11); *_ms = alpha * b_(k).
+ * An empty segment yields n = 0 and zero fields.  Values of b above max_b are
+ * clamped to max_b and counted in n_clamped (max_b <= 65535).
+ * ------------------------------------------------------------------------ */
+typedef struct {
+  uint64_t n, tel_blocks, slo_violations, sum_b;
+  uint32_t p50, p90, p95, p99;
+  uint32_t max_b, n_clamped;
+  double tel_ms, p50_ms, p90_ms, p95_ms, p99_ms, mean_ms;
+} tlru_tail;
+
+tlru_status tlru_tail_workspace_size(uint32_t ns, uint32_t max_b, size_t* bytes /*host*/);
+
+tlru_status tlru_tail_metrics(const uint16_t* b, const uint64_t* seg_offsets /*device[ns+1]*/, uint32_t ns,
+                              const uint32_t* xi /*device[ns]*/, const double* xi_ms /*device[ns]*/,
+                              const uint32_t* slo /*device[ns]*/, double alpha_ms_per_block,
+                              uint32_t max_b, tlru_tail* out /*device[ns]*/, void* ws, size_t ws_bytes,
+                              cudaStream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TLRU_H_ */

@@ -1,0 +1,96 @@
+"""Seeded synthetic inputs shared by the CUDA path's tests/bench and the oracle's tests.
+
+This module holds NO arithmetic of the method: only parameter presets (the
+paper's stochastic-model rates and WildChat/ShareGPT-shaped length laws) and
+seeded numpy generators of small (conv, q, a) request sequences used as test
+inputs.  Both the oracle (oracle/) and the CUDA path (paper_2510_15152_b200)
+consume these; neither computes anything here.
+
+Input recipe:
+  * WILDCHAT preset (BASELINE configs 3-5): lambda_conv = 1/s, lambda_turn = 1/60 s,
+    mu = 1/90 s (mean 1 + lambda_turn/mu = 2.5 turns), prompt tokens
+    lognormal mean 200 (WildChat average) sigma_ln 1.2 clipped [1, 16384],
+    response tokens lognormal mean 400 sigma_ln 0.8 clipped [0, 8192],
+    128-token blocks, L_max = 1024 blocks, <= 64 turns.
+  * SHAREGPT preset (App. E): lambda_conv = 1, lambda_turn = 3,
+    mu = 1.2 (3.5 turns), prompt mean 100 tokens.
+  * tiny traces (BASELINE config 2): <= 4 conversations, <= 3 turns each,
+    q in {1,2,3}, a in {0,1,2}, random interleaving.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+WILDCHAT = dict(
+    num_conversations=1_000_000,
+    block_tokens=128,
+    birth_rate=1.0,
+    turn_rate=1.0 / 60.0,
+    death_rate=1.0 / 90.0,
+    prompt_mean_tokens=200.0,
+    prompt_sigma_ln=1.2,
+    response_mean_tokens=400.0,
+    response_sigma_ln=0.8,
+    prompt_min_tokens=1,
+    prompt_max_tokens=16384,
+    response_min_tokens=0,
+    response_max_tokens=8192,
+    max_history_blocks=1024,
+    max_turns=64,
+)
+
+SHAREGPT = dict(WILDCHAT, turn_rate=3.0, death_rate=1.2, prompt_mean_tokens=100.0,
+                response_mean_tokens=250.0, response_sigma_ln=1.0)
+
+# Fixed model conventions (SURVEY 8 / DESIGN.md): alpha = 12.5 ms per 128-token block,
+# Q_hat = 2 blocks, SLO 200 ms -> b > 16 blocks, xi_s in {50..500} ms -> xi blocks.
+ALPHA_MS = 12.5
+Q_HAT = 2
+SLO_BLOCKS = 16
+XI_BLOCKS = (4, 8, 12, 16, 24, 40)
+CAPS_CONFIG3 = (32, 64, 128, 256, 512, 1024)
+CAPS_CONFIG4 = (64, 128, 256, 512, 1024, 2048, 3072, 4096)
+
+# Figure 1: events A, B, A with 100-block prompts, no responses, C = 100.
+FIG1 = dict(conv=[0, 1, 0], q=[100, 100, 100], a=[0, 0, 0], C=100, xi=150, q_hat=100)
+
+
+def preset(name: str = "wildchat", seed: int = 0, num_conversations: int | None = None) -> dict:
+    p = dict(WILDCHAT if name == "wildchat" else SHAREGPT)
+    p["seed"] = int(seed)
+    if num_conversations is not None:
+        p["num_conversations"] = int(num_conversations)
+    return p
+
+
+def tiny_trace(seed: int, max_conv: int = 4, max_turns: int = 3, qs=(1, 2, 3), as_=(0, 1, 2)):
+    """Random interleaving of <= max_conv conversations with <= max_turns turns each."""
+    rng = np.random.default_rng(seed)
+    n = int(rng.integers(1, max_conv + 1))
+    turns = rng.integers(1, max_turns + 1, size=n)
+    order = np.repeat(np.arange(n), turns)
+    rng.shuffle(order)
+    q = rng.choice(np.asarray(qs), size=order.size)
+    a = rng.choice(np.asarray(as_), size=order.size)
+    return order.astype(np.uint32), q.astype(np.uint32), a.astype(np.uint32)
+
+
+def random_trace(seed: int, n_events: int, n_conv: int, q_max: int = 8, a_max: int = 8,
+                 locality: float = 0.7):
+    """Random (conv, q, a) request sequence with temporal locality: with probability
+    `locality` the next request comes from one of the 8 most recent conversations."""
+    rng = np.random.default_rng(seed)
+    conv = np.empty(n_events, np.uint32)
+    recent: list[int] = []
+    for i in range(n_events):
+        if recent and rng.random() < locality:
+            c = recent[int(rng.integers(0, min(8, len(recent))))]
+        else:
+            c = int(rng.integers(0, n_conv))
+        conv[i] = c
+        if c in recent:
+            recent.remove(c)
+        recent.insert(0, c)
+    q = rng.integers(1, q_max + 1, size=n_events).astype(np.uint32)
+    a = rng.integers(0, a_max + 1, size=n_events).astype(np.uint32)
+    return conv, q, a
