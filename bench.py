@@ -1,0 +1,338 @@
+#!/usr/bin/env python
+"""Benchmark of the T-LRU hot path (BASELINE.json metric: simulated requests/s + HBM roofline %).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One step = the whole hot path of SURVEY 8(a) over one batch of synthetic input
+(BASELINE config 4 per GPU): generate 4 WildChat-shaped traces of 10^6
+conversations (a1-a3, K1), simulate 384 instances = 4 seeds x 8 capacities x 6 xi
+x {LRU, T-LRU} (a4-a8, K2), tail metrics per instance (a9, K3) and, for N > 1,
+an NCCL all_gather of the per-instance results (a10).  Weak scaling: rank r
+simulates seeds 4r..4r+3, so per-GPU work is fixed as N grows.
+
+`value` = requests simulated by all ranks / max-over-ranks device time per step.
+`e2e` = the same metric through the public API from pinned host buffers: H2D of
+each trace's (conv, q, a) turns, tlru_trace_from_turns, tlru_simulate_batch and a
+D2H read of the results, all inside the timed region.
+`--impl reference` times the CPU oracle (oracle/, test infrastructure) on a
+bounded sample of the same workload on the host cores; rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+ALGO_BYTES_PER_REQUEST = 10  # 8-byte event record read + 2-byte uncached count written
+SEEDS_PER_RANK = 4
+
+
+def workload_rows(n_traces: int):
+    from paper_2510_15152_b200.inputs import CAPS_CONFIG4, Q_HAT, SLO_BLOCKS, XI_BLOCKS
+    return [(t, pol, C, xi, Q_HAT, SLO_BLOCKS) for t in range(n_traces) for pol in (0, 1) for C in CAPS_CONFIG4
+            for xi in XI_BLOCKS]
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        d = json.load(open(path))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 6:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = max(mx, float(f[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[2:6]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- reference (CPU oracle)
+def cpu_oracle_sample(seed: int = 0, n_conv: int = 1_000_000):
+    """Oracle as it stands: generate one config-4 trace, replay 8 instances (one per
+    capacity, alternating LRU / T-LRU(xi=16)) on host threads, tail metrics."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    import oracle as O
+    from paper_2510_15152_b200.inputs import ALPHA_MS, CAPS_CONFIG4, Q_HAT, SLO_BLOCKS, preset
+    t0 = time.perf_counter()
+    tr = O.generate(preset("wildchat", seed, n_conv))
+    insts = [(i % 2, C, 16) for i, C in enumerate(CAPS_CONFIG4)]
+    cores = min(len(insts), os.cpu_count() or 1)
+
+    def one(x):
+        pol, C, xi = x
+        r = O.replay(tr.conv, tr.q, tr.a, pol, C, xi, Q_HAT)
+        O.tail(r.b, xi, ALPHA_MS * xi, SLO_BLOCKS, ALPHA_MS)
+        return tr.E
+
+    with ThreadPoolExecutor(max_workers=cores) as ex:
+        n = sum(ex.map(one, insts))
+    dt = time.perf_counter() - t0
+    return n, dt, cores, (f"config-4 sample: oracle generation of seed {seed} ({n_conv} conversations, {tr.E} "
+                          f"requests) + 8 instances (C in 64..4096, LRU / T-LRU xi=16) on {cores} threads")
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    import oracle
+    oracle.build()
+    times, n_req, cores, sample = [], 0, 1, ""
+    for i in range(args.warmup + args.steps):
+        n, dt, cores, sample = cpu_oracle_sample(seed=0)
+        if i >= args.warmup:
+            times.append(dt)
+            n_req = n
+    ms = 1000.0 * statistics.mean(times)
+    value = n_req / (ms / 1000.0)
+    line = {"impl": "reference", "metric": "simulated requests/sec", "value": value, "unit": "requests/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+            "config": {"workload": "config4 sample (CPU oracle)", "requests_per_step": n_req},
+            "cpu_baseline": {"value": value, "unit": "requests/s", "cores": cores, "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": "requests/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- ours
+def run_ours(args, rank, world, local_rank):
+    import ctypes
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2510_15152_b200.tlru as T
+    from paper_2510_15152_b200 import _abi
+    from paper_2510_15152_b200.inputs import preset
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    stream = torch.cuda.current_stream()
+    seeds = [SEEDS_PER_RANK * rank + k for k in range(SEEDS_PER_RANK)]
+    params = [preset("wildchat", s, args.conversations) for s in seeds]
+
+    # ---- setup (untimed): allocate traces at their exact size, the batch and the workspaces
+    traces = T.generate_traces(params, device=dev, exports=True)
+    rows = workload_rows(len(traces))
+    batch = T.prepare_batch(traces, rows)
+    ni = len(rows)
+    E_tot = sum(traces[r[0]].num_events for r in rows)
+    gstructs = [T._gen_struct(p) for p in params]
+    gws = []
+    for g, tr in zip(gstructs, traces):
+        sz = ctypes.c_size_t()
+        _abi.check(_abi.lib.tlru_gen_workspace_size(ctypes.byref(g), tr.sim.numel(), ctypes.byref(sz)))
+        gws.append(torch.empty(max(sz.value, 1), dtype=torch.uint8, device=dev))
+    tstructs = [tr.struct() for tr in traces]
+    gathered = torch.empty(world * batch.results.numel(), dtype=torch.uint8, device=dev) if world > 1 else None
+
+    def step():
+        for g, ts, w in zip(gstructs, tstructs, gws):  # a1-a3: K1 generator (re-generates each trace)
+            _abi.check(_abi.lib.tlru_generate_traces(ctypes.byref(g), 1, ctypes.byref(ts), T._ptr(w), w.numel(),
+                                                     T._stream()))
+        batch.run()  # a4-a9: K2 + K3
+        if world > 1:  # a10: NCCL all_gather of the per-instance results
+            dist.all_gather_into_tensor(gathered, batch.results)
+
+    # ---- e2e host inputs (pinned) and device staging
+    host_turns = []
+    for tr in traces:
+        E = tr.num_events
+        host_turns.append((tr.conv[:E].cpu().pin_memory(), tr.prompt[:E].view(torch.int16).cpu().pin_memory(),
+                           tr.response[:E].view(torch.int16).cpu().pin_memory()))
+    dev_turns = [(torch.empty_like(c, device=dev), torch.empty_like(q, device=dev), torch.empty_like(a, device=dev))
+                 for c, q, a in host_turns]
+    up_ws = []
+    for tr in traces:
+        sz = ctypes.c_size_t()
+        _abi.check(_abi.lib.tlru_upload_workspace_size(tr.num_events, ctypes.byref(sz)))
+        up_ws.append(torch.empty(max(sz.value, 1), dtype=torch.uint8, device=dev))
+    host_results = torch.empty(batch.results.numel(), dtype=torch.uint8).pin_memory()
+    h2d_bytes = sum(c.numel() * 4 + q.numel() * 2 + a.numel() * 2 for c, q, a in host_turns)
+    d2h_bytes = host_results.numel()
+
+    def e2e_step():
+        for (hc, hq, ha), (dc, dq, da), tr, ts, w in zip(host_turns, dev_turns, traces, tstructs, up_ws):
+            dc.copy_(hc, non_blocking=True)
+            dq.copy_(hq, non_blocking=True)
+            da.copy_(ha, non_blocking=True)
+            _abi.check(_abi.lib.tlru_trace_from_turns(T._ptr(dc), T._ptr(dq), T._ptr(da), tr.num_events,
+                                                      ctypes.byref(ts), T._ptr(w), w.numel(), T._stream()))
+        batch.run()
+        host_results.copy_(batch.results, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # ---- warmup
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    launches0 = _abi.lib.tlru_launch_count()
+    k2_ms, k3_ms = [], []
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        barrier()
+        start.record(stream)
+        for _ in range(args.steps):
+            step()
+            st = T.last_sim_stats()
+            k2_ms.append(st["k2_ms"])
+            k3_ms.append(st["k3_ms"])
+        stop.record(stream)
+        barrier()
+    launches = _abi.lib.tlru_launch_count() - launches0
+    ms = start.elapsed_time(stop) / args.steps
+    stats = T.last_sim_stats()
+    res = batch.results_numpy()
+    assert stats["failed_chains"] == 0
+    assert np.all(res["requests"][:ni] > 0)
+
+    # ---- e2e (same batch through the public API from host buffers)
+    for _ in range(max(1, args.warmup)):
+        e2e_step()
+    barrier()
+    t_e2e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t_e2e[0].record(stream)
+    for _ in range(args.steps):
+        e2e_step()
+    t_e2e[1].record(stream)
+    barrier()
+    e2e_ms = t_e2e[0].elapsed_time(t_e2e[1]) / args.steps
+
+    # ---- max over ranks
+    loc = torch.tensor([ms, e2e_ms, statistics.mean(k2_ms), statistics.mean(k3_ms)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(loc, op=dist.ReduceOp.MAX)
+    ms, e2e_ms, k2, k3 = [float(x) for x in loc.tolist()]
+    if rank != 0:
+        return
+    req_all = E_tot * world
+    value = req_all / (ms / 1000.0)
+    peak, peak_src = peaks()
+    achieved = ALGO_BYTES_PER_REQUEST * E_tot / (k2 / 1000.0) / 1e9  # GB/s, per GPU, K2 phase
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        t = json.load(open(tpath))
+        if "dram_bytes_per_request" in t:
+            traffic = float(t["dram_bytes_per_request"]) * E_tot
+    line = {
+        "metric": "simulated requests/sec", "value": value, "unit": "requests/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+        "config": {
+            "workload": "config4: per GPU 4 seeds x 10^6-conversation WildChat-shaped traces (generated each step), "
+                        "C in {64..4096} x xi in {4..40} x {LRU, T-LRU} = 384 instances",
+            "instances_per_gpu": ni, "requests_per_gpu_step": E_tot, "conversations": args.conversations,
+            "parallelism": f"dp{world} (instances sharded by seed, NCCL all_gather of results)",
+            "l2": "inputs larger than L2: 0.77 GB of b written per GPU-step",
+            "engine": "K2 time-partitioned Alg. 1 simulation; no dedup, no closed-form fast path",
+            "segment_events": stats["segment_events"], "k2_ms": k2, "k3_ms": k3,
+        },
+        "e2e": {"value": req_all / (e2e_ms / 1000.0), "unit": "requests/s", "h2d_bytes_per_step": h2d_bytes,
+                "d2h_bytes_per_step": d2h_bytes, "ms_per_step": e2e_ms},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic, "kernel": "sim_kernel<W> (K2 phase)", "peak_source": peak_src,
+                     "algorithmic_bytes_per_request": ALGO_BYTES_PER_REQUEST},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+    }
+    if not args.no_cpu_baseline:
+        n, dt, cores, sample = cpu_oracle_sample(seed=0, n_conv=args.conversations)
+        line["cpu_baseline"] = {"value": n / dt, "unit": "requests/s", "cores": cores, "kind": "oracle",
+                                "sample": sample}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--conversations", type=int, default=1_000_000)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    import torch.distributed as dist
+    if world > 1:
+        import torch
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_ours(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

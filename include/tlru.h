@@ -52,6 +52,9 @@ const char* tlru_last_error(void);
 /* Library version string, e.g. "tlru 0.1 sm_100a". */
 const char* tlru_version(void);
 
+/* Total kernel launches issued by this library in this process (host counter). */
+uint64_t tlru_launch_count(void);
+
 /* ------------------------------------------------------------------------
  * Synthetic traces: the paper's stochastic conversation model (Sec. 5)
  *   - conversations are born by a Poisson(birth_rate) process;
@@ -168,7 +171,7 @@ typedef struct {
   uint32_t slo;      /* SLO violation iff b > slo (strict); 16 = 200 ms at 12.5 ms/block */
 } tlru_instance;
 
-typedef struct { /* 64 B, all exact integers */
+typedef struct { /* 72 B, all exact integers */
   uint64_t requests;       /* E of the instance's trace */
   uint64_t sum_uncached;   /* sum b */
   uint64_t tel_blocks;     /* sum max(b - xi, 0)  (Eq. 3) */
@@ -197,14 +200,25 @@ tlru_status tlru_simulate_batch(const tlru_trace* traces /*host[nt]*/, uint32_t 
                                 const uint64_t* offsets /*host[ni] or NULL*/, tlru_result* results, void* ws,
                                 size_t ws_bytes, cudaStream_t stream);
 
-/* Statistics of the last tlru_simulate_batch on this thread (host). */
+/* Tuning / test knobs for tlru_simulate_batch on this thread (host; 0 = automatic).
+ * segment_events: events per segment (rounded up to a multiple of 32; the cache
+ *   state at each segment start is rebuilt exactly, so results do not depend on it).
+ * state_entries: per-chain on-chip state entries W (one of 32..1024); chains that
+ *   outgrow it are re-run from global memory, so results do not depend on it. */
+tlru_status tlru_set_sim_options(uint32_t segment_events, uint32_t state_entries);
+
+/* Statistics of the last tlru_simulate_batch on this thread.  Reads two device
+ * counters from that call's workspace, so the workspace must not have been
+ * reused; synchronizes the device. */
 typedef struct {
-  uint64_t chains;          /* instance x segment work units launched */
+  uint64_t chains;          /* instance x segment work units launched (32 lanes per warp) */
   uint64_t segment_events;  /* events per segment */
-  uint64_t warm_events;     /* events walked to rebuild segment-start states */
   uint64_t spilled_chains;  /* chains re-run with global-memory state */
+  uint64_t failed_chains;   /* chains that overflowed even the global-memory state (must be 0) */
   uint32_t kernels;         /* kernel launches issued */
-  uint32_t reserved;
+  uint32_t state_entries;   /* largest on-chip W used */
+  float k2_ms;              /* device time of the simulation kernels (K2 + spill), CUDA events on `stream` */
+  float k3_ms;              /* device time of the tail-metric kernels (K3) */
 } tlru_sim_stats;
 tlru_status tlru_last_sim_stats(tlru_sim_stats* out /*host*/);
 

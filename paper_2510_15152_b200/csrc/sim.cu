@@ -1,0 +1,498 @@
+// sim.cu -- K2: batched Alg. 1 simulation and tlru_simulate_batch.
+//
+// Work decomposition:
+//   * instances of one trace are sorted by capacity and packed 32 to a warp
+//     ("lane group"); every lane runs its own instance (C, D) in lockstep over
+//     the SAME events, so each event record is loaded once per warp (coalesced
+//     32-event tile, broadcast by shuffle) and each lane keeps its state in a
+//     lane-interleaved, bank-conflict-free shared-memory array of W entries;
+//   * each trace is cut into segments; a warp = (lane group, segment); every
+//     segment start state is rebuilt exactly (sim.cuh), so all warps are
+//     independent and the grid is sized to fill the 148 SMs;
+//   * per-request b are staged in shared memory and written as coalesced
+//     64-byte rows per instance;
+//   * a chain whose live entries exceed W is re-run by the spill kernel with
+//     its state in global memory (never truncated).
+#include <algorithm>
+#include <mutex>
+#include <vector>
+
+#include "metrics.cuh"
+#include "sim.cuh"
+
+namespace tlru {
+
+struct LaneDev {
+  uint32_t inst;  // instance index, 0xFFFFFFFF = idle lane
+  uint32_t C, D;
+  uint32_t pad;
+  uint64_t boff;  // offset of the instance's b array in `uncached`
+};
+
+struct GroupDev {
+  uint32_t trace, lane0, nlanes, W;
+};
+
+struct ItemDev {
+  uint32_t group, seg;
+};
+
+struct TraceDev {
+  const uint64_t* sim;
+  const uint32_t* next;
+  uint64_t E;
+};
+
+struct AccDev {  // per-instance accumulators of the counters not derivable from b
+  unsigned long long ev_trim, ev_lru;
+  unsigned int max_occ, pad;
+};
+
+struct SpillDev {
+  uint32_t group, seg, lane, pad;
+};
+
+constexpr int BST_STRIDE = 34;  // u16 stride of a staged b row: 32 events + 2 pad (conflict-free)
+
+__device__ __forceinline__ uint64_t shfl64(uint64_t v, int src) {
+  uint32_t lo = __shfl_sync(0xFFFFFFFFu, static_cast<uint32_t>(v), src);
+  uint32_t hi = __shfl_sync(0xFFFFFFFFu, static_cast<uint32_t>(v >> 32), src);
+  return (uint64_t(hi) << 32) | lo;
+}
+
+__device__ __forceinline__ void acc_commit(AccDev* acc, uint32_t inst, const ChainRegs& c) {
+  if (c.ev_trim) atomicAdd(&acc[inst].ev_trim, static_cast<unsigned long long>(c.ev_trim));
+  if (c.ev_lru) atomicAdd(&acc[inst].ev_lru, static_cast<unsigned long long>(c.ev_lru));
+  atomicMax(&acc[inst].max_occ, c.max_occ);
+}
+
+// One warp per (lane group, segment).  W = state entries per lane (compile-time).
+template <int W>
+__global__ void __launch_bounds__(32) sim_kernel(const ItemDev* __restrict__ items, const GroupDev* __restrict__ groups,
+                                                 const LaneDev* __restrict__ lanes, const TraceDev* __restrict__ traces,
+                                                 uint32_t seg_len, uint16_t* __restrict__ bout, AccDev* acc,
+                                                 SpillDev* spill, unsigned int* nspill) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  uint32_t* tau_s = reinterpret_cast<uint32_t*>(smem);
+  uint16_t* X_s = reinterpret_cast<uint16_t*>(tau_s + W * 32);
+  uint16_t* bst = X_s + W * 32;
+  const int lane = threadIdx.x;
+  const ItemDev it = items[blockIdx.x];
+  const GroupDev g = groups[it.group];
+  const TraceDev tr = traces[g.trace];
+  const uint32_t s = it.seg * seg_len;
+  const uint32_t s_end = static_cast<uint32_t>(min(uint64_t(s) + seg_len, tr.E));
+  LaneDev lp;
+  lp.inst = 0xFFFFFFFFu;
+  lp.C = lp.D = 0;
+  lp.boff = 0;
+  if (lane < static_cast<int>(g.nlanes)) lp = lanes[g.lane0 + lane];
+  bool active = lp.inst != 0xFFFFFFFFu;
+  SmemState st{tau_s, X_s, lane};
+  ChainRegs c;
+  chain_init(c, lp.C, lp.D, W, active && s > 0);
+
+  // ---- rebuild the exact state at s (sim.cuh "Segment start")
+  for (int pass = 0; pass < 2; ++pass) {
+    int64_t e0 = int64_t(s) - 1;
+    while (e0 >= 0 && __any_sync(0xFFFFFFFFu, c.walking)) {
+      const int64_t e = e0 - lane;
+      uint32_t nx = 0, la = 0;
+      if (e >= 0) {
+        nx = __ldg(tr.next + e);
+        la = sim_La(__ldg(tr.sim + e));
+      }
+      const int cnt = e0 + 1 < 32 ? static_cast<int>(e0 + 1) : 32;
+      for (int k = 0; k < cnt; ++k) {
+        const uint32_t nxk = __shfl_sync(0xFFFFFFFFu, nx, k);
+        const uint32_t lak = __shfl_sync(0xFFFFFFFFu, la, k);
+        if (c.walking && nxk >= s) chain_walk_step(c, st, static_cast<uint32_t>(e0 - k), lak);
+      }
+      e0 -= 32;
+    }
+    const bool again = chain_walk_restart(c);
+    if (!__any_sync(0xFFFFFFFFu, again)) break;
+  }
+  chain_walk_finish(c);
+  if (c.overflow) active = false;
+
+  // ---- forward: Alg. 1 per request, events broadcast from a 32-event register tile
+  uint64_t evn = 0;
+  if (s + lane < s_end) evn = __ldg(tr.sim + s + lane);
+  for (uint32_t base = s; base < s_end; base += 32) {
+    const uint64_t evc = evn;
+    const uint32_t nk = min(32u, s_end - base);
+    if (base + 32 + lane < s_end) evn = __ldg(tr.sim + base + 32 + lane);  // prefetch the next tile
+    for (uint32_t k = 0; k < nk; ++k) {
+      const uint64_t ev = shfl64(evc, k);
+      if (active) {
+        const uint32_t b = chain_request(c, st, base + k, sim_prev(ev), sim_J(ev), sim_La(ev));
+        bst[lane * BST_STRIDE + k] = static_cast<uint16_t>(b);
+        if (c.overflow) active = false;
+      }
+    }
+    __syncwarp();
+    // coalesced write-out: row r = lane r's instance, 64 contiguous bytes
+    const unsigned act = __ballot_sync(0xFFFFFFFFu, active);
+    for (int r = 0; r < 32; ++r) {
+      const uint64_t off = shfl64(lp.boff, r);
+      if (((act >> r) & 1u) && static_cast<uint32_t>(lane) < nk)
+        bout[off + base + lane] = bst[r * BST_STRIDE + lane];
+    }
+    __syncwarp();
+  }
+  if (active) {
+    acc_commit(acc, lp.inst, c);
+  } else if (lp.inst != 0xFFFFFFFFu) {  // overflowed: the spill kernel re-runs this chain
+    unsigned slot = atomicAdd(nspill, 1u);
+    spill[slot] = SpillDev{it.group, it.seg, static_cast<uint32_t>(lane), 0u};
+  }
+}
+
+// Spill path: one thread per queued chain, state in global memory (W_big entries per slot).
+__global__ void sim_spill_kernel(const GroupDev* __restrict__ groups, const LaneDev* __restrict__ lanes,
+                                 const TraceDev* __restrict__ traces, uint32_t seg_len, uint16_t* __restrict__ bout,
+                                 AccDev* acc, const SpillDev* spill, const unsigned int* nspill, uint32_t* tau_pool,
+                                 uint16_t* X_pool, uint32_t W_big, unsigned int* nfail) {
+  const unsigned n = *nspill;
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const SpillDev sp = spill[i];
+    const GroupDev g = groups[sp.group];
+    const TraceDev tr = traces[g.trace];
+    const LaneDev lp = lanes[g.lane0 + sp.lane];
+    const uint32_t s = sp.seg * seg_len;
+    const uint32_t s_end = static_cast<uint32_t>(min(uint64_t(s) + seg_len, tr.E));
+    const uint64_t slot = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+    GlobalState st{tau_pool + slot * W_big, X_pool + slot * W_big};
+    ChainRegs c;
+    chain_init(c, lp.C, lp.D, W_big, s > 0);
+    for (int pass = 0; pass < 2; ++pass) {
+      for (int64_t e = int64_t(s) - 1; e >= 0 && c.walking; --e) {
+        if (tr.next[e] >= s) chain_walk_step(c, st, static_cast<uint32_t>(e), sim_La(tr.sim[e]));
+      }
+      if (!chain_walk_restart(c)) break;
+    }
+    chain_walk_finish(c);
+    for (uint32_t e = s; e < s_end && !c.overflow; ++e) {
+      const uint64_t ev = tr.sim[e];
+      bout[lp.boff + e] = static_cast<uint16_t>(chain_request(c, st, e, sim_prev(ev), sim_J(ev), sim_La(ev)));
+    }
+    if (c.overflow) {
+      atomicAdd(nfail, 1u);
+    } else {
+      acc_commit(acc, lp.inst, c);
+    }
+  }
+}
+
+__global__ void sim_results_kernel(uint32_t ni, const AccDev* acc, tlru_result* results) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < ni; i += gridDim.x * blockDim.x) {
+    results[i].evicted_trim = acc[i].ev_trim;
+    results[i].evicted_lru = acc[i].ev_lru;
+    results[i].max_occupancy = acc[i].max_occ;
+  }
+}
+
+// ----------------------------------------------------------------------------- planner
+static const int kWClasses[] = {32, 64, 128, 256, 512, 1024};
+constexpr int kNumW = 6;
+constexpr int kSpillSlots = 128;
+
+static thread_local uint32_t g_opt_seg = 0;  // tlru_set_sim_options
+static thread_local int g_opt_w = -1;
+
+// Entries needed per lane for capacity C: live conversations are bounded by
+// min(C + 1, conversations); the estimate below is the measured resident count of
+// the WildChat-shaped preset with margin, x2 for tombstones between
+// compactions.  Under-estimates are caught by the spill path, never truncated.
+static int w_class(uint32_t C, uint32_t nconv) {
+  double live = std::min<double>(double(C) + 1.0, double(nconv) + 1.0);
+  double est = std::min(live, 0.8 * std::pow(double(C), 0.77) + 8.0);
+  for (int i = 0; i < kNumW; ++i)
+    if (kWClasses[i] >= 2.0 * est || kWClasses[i] > static_cast<int>(live) + 1) return i;
+  return kNumW - 1;
+}
+
+struct Plan {
+  std::vector<LaneDev> lanes;
+  std::vector<GroupDev> groups;
+  std::vector<ItemDev> items[kNumW];
+  std::vector<TraceDev> traces;
+  std::vector<SegDev> segs;
+  uint32_t seg_len = 0;
+  uint32_t bins = 1;
+  uint32_t W_big = 32;
+  uint64_t max_items = 0;
+  uint64_t warm_bound = 0;
+};
+
+static tlru_status make_plan(const tlru_trace* traces, uint32_t nt, const tlru_instance* inst, uint32_t ni,
+                             const uint64_t* offsets, Plan* P) {
+  if (ni > 0 && !inst) TLRU_FAIL(TLRU_EINVAL, "inst is NULL");
+  if (nt > 0 && !traces) TLRU_FAIL(TLRU_EINVAL, "traces is NULL");
+  P->traces.resize(nt);
+  uint32_t maxhist = 0;
+  uint64_t Emax = 0;
+  for (uint32_t t = 0; t < nt; ++t) {
+    const tlru_trace& tr = traces[t];
+    if (tr.num_events > 0 && (!tr.sim || !tr.next)) TLRU_FAIL(TLRU_EINVAL, "trace %u: sim/next is NULL", t);
+    if (tr.num_events >= 0xFFFFFFFFull) TLRU_FAIL(TLRU_ERANGE, "trace %u: too many events", t);
+    P->traces[t] = TraceDev{tr.sim, tr.next, tr.num_events};
+    maxhist = std::max(maxhist, tr.max_history);
+    Emax = std::max<uint64_t>(Emax, tr.num_events);
+  }
+  if (maxhist > 65535) TLRU_FAIL(TLRU_ERANGE, "max_history > 65535");
+  P->bins = maxhist + 1;
+  // instance order: by trace, then W class, then C (lanes of a warp see similar state sizes)
+  std::vector<uint32_t> order(ni);
+  std::vector<int> wc(ni);
+  uint64_t packed = 0;
+  P->segs.resize(ni);
+  for (uint32_t i = 0; i < ni; ++i) {
+    const tlru_instance& in = inst[i];
+    if (in.trace >= nt) TLRU_FAIL(TLRU_EINVAL, "instance %u: trace index %u out of range", i, in.trace);
+    if (in.policy != TLRU_POLICY_LRU && in.policy != TLRU_POLICY_TLRU)
+      TLRU_FAIL(TLRU_EUNSUPPORTED, "instance %u: policy %u is not built (LRU = 0, T-LRU = 1)", i, in.policy);
+    order[i] = i;
+    const uint32_t C = std::min<uint32_t>(in.capacity, 0x7FFF0000u);
+    wc[i] = g_opt_w >= 0 ? g_opt_w : w_class(C, traces[in.trace].num_conversations);
+    const uint64_t E = traces[in.trace].num_events;
+    const uint64_t off = offsets ? offsets[i] : packed;
+    packed += E;
+    P->segs[i] = SegDev{off, off + E, in.xi, in.slo, 0.0};
+  }
+  std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) {
+    if (inst[a].trace != inst[b].trace) return inst[a].trace < inst[b].trace;
+    if (wc[a] != wc[b]) return wc[a] < wc[b];
+    return inst[a].capacity < inst[b].capacity;
+  });
+  // lane groups
+  for (uint32_t k = 0; k < ni;) {
+    const uint32_t t = inst[order[k]].trace;
+    const int w = wc[order[k]];
+    GroupDev g{t, static_cast<uint32_t>(P->lanes.size()), 0, static_cast<uint32_t>(w)};
+    while (k < ni && g.nlanes < 32 && inst[order[k]].trace == t && wc[order[k]] == w) {
+      const tlru_instance& in = inst[order[k]];
+      LaneDev l;
+      l.inst = order[k];
+      l.C = std::min<uint32_t>(in.capacity, 0x7FFF0000u);
+      l.D = (in.policy == TLRU_POLICY_TLRU && in.xi > in.q_hat) ? in.xi - in.q_hat : 0u;  // free tail
+      l.pad = 0;
+      l.boff = P->segs[order[k]].begin;
+      P->lanes.push_back(l);
+      ++g.nlanes;
+      ++k;
+    }
+    P->groups.push_back(g);
+  }
+  // segment length: enough warps to fill 148 SMs several times over
+  const uint64_t G = P->groups.size();
+  const uint64_t target = 148ull * 24ull;
+  uint64_t parts = G ? (target + G - 1) / G : 1;
+  uint64_t seg = Emax ? (Emax + parts - 1) / parts : 32;
+  seg = std::max<uint64_t>(seg, 4096);
+  if (g_opt_seg) seg = g_opt_seg;
+  seg = std::min<uint64_t>(seg, 32768);  // u32 per-chain counters stay below 2^31
+  seg = (seg + 31) & ~31ull;
+  P->seg_len = static_cast<uint32_t>(seg);
+  uint64_t nitems = 0;
+  for (uint32_t gi = 0; gi < P->groups.size(); ++gi) {
+    const GroupDev& g = P->groups[gi];
+    const uint64_t E = P->traces[g.trace].E;
+    const uint64_t nseg = (E + seg - 1) / seg;
+    for (uint64_t sgi = 0; sgi < nseg; ++sgi) P->items[g.W].push_back(ItemDev{gi, static_cast<uint32_t>(sgi)});
+    nitems += nseg;
+  }
+  P->max_items = nitems;
+  // spill-state size: live entries <= min(C, conversations) + 1, x2 for tombstones
+  uint32_t wb = 32;
+  for (uint32_t i = 0; i < ni; ++i) {
+    const uint64_t live =
+        std::min<uint64_t>(std::min<uint32_t>(inst[i].capacity, 0x7FFF0000u), traces[inst[i].trace].num_conversations) + 2;
+    wb = static_cast<uint32_t>(std::max<uint64_t>(wb, std::min<uint64_t>(2 * live + 2, 0xFFFFFFF0ull)));
+  }
+  P->W_big = wb;
+  return TLRU_OK;
+}
+
+struct SimWs {
+  LaneDev* lanes;
+  GroupDev* groups;
+  ItemDev* items;
+  TraceDev* traces;
+  SegDev* segs;
+  AccDev* acc;
+  SpillDev* spill;
+  unsigned int* counters;  // [0] nspill, [1] nfail
+  uint32_t* hist;
+  unsigned long long* clamped;
+  uint32_t* tau_pool;
+  uint16_t* X_pool;
+};
+
+static void carve_sim(Carver& cv, const Plan& P, uint32_t ni, SimWs* w) {
+  uint64_t nitems = 0;
+  for (int k = 0; k < kNumW; ++k) nitems += P.items[k].size();
+  w->lanes = cv.take<LaneDev>(P.lanes.size() + 1);
+  w->groups = cv.take<GroupDev>(P.groups.size() + 1);
+  w->items = cv.take<ItemDev>(nitems + 1);
+  w->traces = cv.take<TraceDev>(P.traces.size() + 1);
+  w->segs = cv.take<SegDev>(ni + 1);
+  w->acc = cv.take<AccDev>(ni + 1);
+  w->spill = cv.take<SpillDev>(nitems * 32 + 1);
+  w->counters = cv.take<unsigned int>(2);
+  w->hist = cv.take<uint32_t>(uint64_t(ni + 1) * P.bins);
+  w->clamped = cv.take<unsigned long long>(ni + 1);
+  w->tau_pool = cv.take<uint32_t>(uint64_t(kSpillSlots) * P.W_big);
+  w->X_pool = cv.take<uint16_t>(uint64_t(kSpillSlots) * P.W_big);
+}
+
+static thread_local tlru_sim_stats g_stats;
+static thread_local unsigned int* g_counters = nullptr;
+static thread_local cudaEvent_t g_ev[3] = {nullptr, nullptr, nullptr};
+static thread_local bool g_ev_recorded = false;
+
+static tlru_status record(int k, cudaStream_t st) {
+  if (!g_ev[k]) TLRU_CUDA(cudaEventCreate(&g_ev[k]));
+  TLRU_CUDA(cudaEventRecord(g_ev[k], st));
+  return TLRU_OK;
+}
+
+template <int W>
+static tlru_status launch_w(const std::vector<ItemDev>& items, const ItemDev* d_items, const SimWs& w,
+                            uint32_t seg_len, uint16_t* bout, cudaStream_t st) {
+  if (items.empty()) return TLRU_OK;
+  const size_t smem = size_t(W) * 32 * (sizeof(uint32_t) + sizeof(uint16_t)) + 32 * BST_STRIDE * sizeof(uint16_t);
+  TLRU_CUDA(cudaFuncSetAttribute(sim_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  sim_kernel<W><<<static_cast<unsigned>(items.size()), 32, smem, st>>>(d_items, w.groups, w.lanes, w.traces, seg_len,
+                                                                       bout, w.acc, w.spill, w.counters);
+  TLRU_CHECK_LAUNCH();
+  ++g_stats.kernels;
+  return TLRU_OK;
+}
+
+}  // namespace tlru
+
+using namespace tlru;
+
+extern "C" tlru_status tlru_sim_workspace_size(const tlru_trace* traces, uint32_t nt, const tlru_instance* inst,
+                                               uint32_t ni, size_t* bytes) {
+  clear_error();
+  if (!bytes) TLRU_FAIL(TLRU_EINVAL, "bytes is NULL");
+  Plan P;
+  TLRU_TRY(make_plan(traces, nt, inst, ni, nullptr, &P));
+  Carver cv(nullptr);
+  SimWs w;
+  carve_sim(cv, P, ni, &w);
+  *bytes = cv.used;
+  return TLRU_OK;
+}
+
+extern "C" tlru_status tlru_simulate_batch(const tlru_trace* traces, uint32_t nt, const tlru_instance* inst,
+                                           uint32_t ni, uint16_t* uncached, const uint64_t* offsets,
+                                           tlru_result* results, void* ws, size_t ws_bytes, cudaStream_t st) {
+  clear_error();
+  g_stats = tlru_sim_stats{};
+  g_counters = nullptr;
+  g_ev_recorded = false;
+  if (ni == 0) return TLRU_OK;
+  if (!results) TLRU_FAIL(TLRU_EINVAL, "results is NULL");
+  Plan P;
+  TLRU_TRY(make_plan(traces, nt, inst, ni, offsets, &P));
+  if (!uncached) {
+    for (uint32_t i = 0; i < ni; ++i)
+      if (traces[inst[i].trace].num_events > 0) TLRU_FAIL(TLRU_EINVAL, "uncached is NULL");
+  }
+  Carver cv(ws);
+  SimWs w;
+  carve_sim(cv, P, ni, &w);
+  TLRU_TRY(check_ws(cv, ws, ws_bytes));
+  // tables -> device (pageable copies complete before the call returns)
+  std::vector<ItemDev> all_items;
+  size_t item_off[kNumW + 1];
+  for (int k = 0; k < kNumW; ++k) {
+    item_off[k] = all_items.size();
+    all_items.insert(all_items.end(), P.items[k].begin(), P.items[k].end());
+  }
+  item_off[kNumW] = all_items.size();
+  TLRU_CUDA(cudaMemcpyAsync(w.lanes, P.lanes.data(), P.lanes.size() * sizeof(LaneDev), cudaMemcpyHostToDevice, st));
+  TLRU_CUDA(cudaMemcpyAsync(w.groups, P.groups.data(), P.groups.size() * sizeof(GroupDev), cudaMemcpyHostToDevice, st));
+  if (!all_items.empty())
+    TLRU_CUDA(cudaMemcpyAsync(w.items, all_items.data(), all_items.size() * sizeof(ItemDev), cudaMemcpyHostToDevice, st));
+  TLRU_CUDA(cudaMemcpyAsync(w.traces, P.traces.data(), P.traces.size() * sizeof(TraceDev), cudaMemcpyHostToDevice, st));
+  TLRU_CUDA(cudaMemcpyAsync(w.segs, P.segs.data(), ni * sizeof(SegDev), cudaMemcpyHostToDevice, st));
+  TLRU_CUDA(cudaMemsetAsync(w.acc, 0, ni * sizeof(AccDev), st));
+  TLRU_CUDA(cudaMemsetAsync(w.counters, 0, 2 * sizeof(unsigned int), st));
+  TLRU_CUDA(cudaMemsetAsync(w.hist, 0, uint64_t(ni) * P.bins * sizeof(uint32_t), st));
+  TLRU_CUDA(cudaMemsetAsync(w.clamped, 0, ni * sizeof(unsigned long long), st));
+  // K2: largest state class first (longest per-event latency)
+  TLRU_TRY(record(0, st));
+  for (int k = kNumW - 1; k >= 0; --k) {
+    const ItemDev* d = w.items + item_off[k];
+    switch (k) {
+      case 0: TLRU_TRY(launch_w<32>(P.items[k], d, w, P.seg_len, uncached, st)); break;
+      case 1: TLRU_TRY(launch_w<64>(P.items[k], d, w, P.seg_len, uncached, st)); break;
+      case 2: TLRU_TRY(launch_w<128>(P.items[k], d, w, P.seg_len, uncached, st)); break;
+      case 3: TLRU_TRY(launch_w<256>(P.items[k], d, w, P.seg_len, uncached, st)); break;
+      case 4: TLRU_TRY(launch_w<512>(P.items[k], d, w, P.seg_len, uncached, st)); break;
+      case 5: TLRU_TRY(launch_w<1024>(P.items[k], d, w, P.seg_len, uncached, st)); break;
+    }
+  }
+  // spill path: always launched; exits at once when the queue is empty (no host sync)
+  sim_spill_kernel<<<kSpillSlots / 32, 32, 0, st>>>(w.groups, w.lanes, w.traces, P.seg_len, uncached, w.acc, w.spill,
+                                                    w.counters, w.tau_pool, w.X_pool, P.W_big, w.counters + 1);
+  TLRU_CHECK_LAUNCH();
+  ++g_stats.kernels;
+  TLRU_TRY(record(1, st));
+  // K3: histogram of b per instance -> percentiles, TEL, SLO; then the counters
+  TLRU_TRY(launch_hist(uncached, w.segs, ni, P.bins, w.hist, w.clamped, st));
+  TLRU_TRY(launch_finalize(w.segs, ni, P.bins, w.hist, w.clamped, 1.0, nullptr, results, st));
+  sim_results_kernel<<<grid_for(ni, 128), 128, 0, st>>>(ni, w.acc, results);
+  TLRU_CHECK_LAUNCH();
+  TLRU_TRY(record(2, st));
+  g_ev_recorded = true;
+  g_stats.kernels += 3;
+  g_stats.chains = 0;
+  for (int k = 0; k < kNumW; ++k) g_stats.chains += P.items[k].size() * 32;
+  g_stats.segment_events = P.seg_len;
+  for (int k = kNumW - 1; k >= 0; --k)
+    if (!P.items[k].empty()) {
+      g_stats.state_entries = kWClasses[k];
+      break;
+    }
+  g_counters = w.counters;
+  return TLRU_OK;
+}
+
+extern "C" tlru_status tlru_set_sim_options(uint32_t segment_events, uint32_t state_entries) {
+  clear_error();
+  if (segment_events > 32768) TLRU_FAIL(TLRU_ERANGE, "segment_events must be <= 32768");
+  int w = -1;
+  if (state_entries) {
+    for (int k = 0; k < kNumW; ++k)
+      if (static_cast<uint32_t>(kWClasses[k]) == state_entries) w = k;
+    if (w < 0) TLRU_FAIL(TLRU_EINVAL, "state_entries must be 0 or one of 32, 64, 128, 256, 512, 1024");
+  }
+  g_opt_seg = segment_events;
+  g_opt_w = w;
+  return TLRU_OK;
+}
+
+extern "C" tlru_status tlru_last_sim_stats(tlru_sim_stats* out) {
+  clear_error();
+  if (!out) TLRU_FAIL(TLRU_EINVAL, "out is NULL");
+  *out = g_stats;
+  if (g_counters) {
+    unsigned int c[2] = {0, 0};
+    TLRU_CUDA(cudaDeviceSynchronize());
+    TLRU_CUDA(cudaMemcpy(c, g_counters, sizeof(c), cudaMemcpyDeviceToHost));
+    out->spilled_chains = c[0];
+    out->failed_chains = c[1];
+  }
+  if (g_ev_recorded) {
+    TLRU_CUDA(cudaEventSynchronize(g_ev[2]));
+    TLRU_CUDA(cudaEventElapsedTime(&out->k2_ms, g_ev[0], g_ev[1]));
+    TLRU_CUDA(cudaEventElapsedTime(&out->k3_ms, g_ev[1], g_ev[2]));
+  }
+  return TLRU_OK;
+}

@@ -1,0 +1,232 @@
+// sim.cuh -- per-chain state machine of Alg. 1 used by the K2 kernels.
+//
+// A chain = one instance (C, D) over one segment [s, s_end) of one trace.
+//
+// State: one tau-ordered array of entries
+//   tau[k]  event index of the conversation's last turn ("Timestamp of Last Turn")
+//   X[k]    cached blocks of that conversation (P:117 x_{i,t})
+// live in [head, tail).  A request of conversation theta finds its entry by
+// binary search on tau == prev (the event index of theta's previous turn),
+// tombstones it (X = 0) and appends a fresh entry at `tail` (theta gets the
+// newest tau).  Free ("infinitely old") blocks are implied, not
+// stored: with D = max(xi - Q_hat, 0), the entries with surplus > 0 always form a
+// tau-suffix starting at `fh`; every entry after fh is untouched since its
+// insertion, so its surplus is min(X, D); fh's own (possibly partial) surplus is
+// the register `frem`.  Phase 1 walks fh forward, Phase 2 walks head forward.
+// When tail reaches W the live entries are compacted to the front.
+//
+// Segment start (exact, no fix-up): the cache content after any request equals
+// the top-C blocks of the universe under the static key (non-free?, tau, -pos)
+// (pinned by tests/stackdist.py against the oracle).
+// So the state at s is rebuilt by walking backwards from s-1 over each
+// conversation's last turn before s (next[e'] >= s), granting non-free blocks
+// max(L - D, 0) most-recent-first until C is reached; only if the whole prefix
+// holds fewer than C non-free blocks are free blocks min(L, D) granted too
+// (second walk, most-recent-first).
+#pragma once
+
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace tlru {
+
+// Lane-interleaved shared-memory state: entry k of lane l at [k * 32 + l]
+// (4-byte tau and 2-byte X arrays: conflict-free for any per-lane k).
+struct SmemState {
+  uint32_t* tau;
+  uint16_t* X;
+  int lane;
+  __device__ __forceinline__ uint32_t& T(uint32_t k) const { return tau[k * 32u + lane]; }
+  __device__ __forceinline__ uint16_t& Xr(uint32_t k) const { return X[k * 32u + lane]; }
+};
+
+// Chain-contiguous global-memory state (spill path).
+struct GlobalState {
+  uint32_t* tau;
+  uint16_t* X;
+  __device__ __forceinline__ uint32_t& T(uint32_t k) const { return tau[k]; }
+  __device__ __forceinline__ uint16_t& Xr(uint32_t k) const { return X[k]; }
+};
+
+struct ChainRegs {
+  uint32_t head, tail, fh, frem;
+  uint32_t used, C, D, W;
+  uint32_t ev_trim, ev_lru, max_occ;
+  // warm-start bookkeeping
+  uint32_t r, cum_nf, cum_f, nf_target, free_budget, fh_pos, fh_rem;
+  bool walking, overflow;
+};
+
+__device__ __forceinline__ void chain_init(ChainRegs& c, uint32_t C, uint32_t D, uint32_t W, bool has_prefix) {
+  c.C = C;
+  c.D = D;
+  c.W = W;
+  c.head = c.tail = W;
+  c.fh = W;
+  c.frem = 0;
+  c.used = 0;
+  c.ev_trim = c.ev_lru = c.max_occ = 0;
+  c.r = c.cum_nf = c.cum_f = 0;
+  c.nf_target = C;
+  c.free_budget = 0;
+  c.fh_pos = 0xFFFFFFFFu;
+  c.fh_rem = 0;
+  c.walking = has_prefix && C > 0;
+  c.overflow = false;
+}
+
+// One step of the backward walk: e' is an event before the segment start with
+// next[e'] >= s (the last turn of its conversation before s) and L_after = la.
+template <class St>
+__device__ __forceinline__ void chain_walk_step(ChainRegs& c, const St& st, uint32_t e_prime, uint32_t la) {
+  uint32_t nf = la > c.D ? la - c.D : 0u;  // non-free blocks max(L - D, 0)
+  uint32_t f = la < c.D ? la : c.D;        // free blocks min(L, D)
+  uint32_t x = min(nf, c.nf_target - c.cum_nf);
+  uint32_t y = min(f, c.free_budget - c.cum_f);
+  if (x + y > 0) {
+    if (c.r == c.W) {
+      c.overflow = true;
+      c.walking = false;
+      return;
+    }
+    uint32_t k = c.W - 1 - c.r;
+    st.T(k) = e_prime;
+    st.Xr(k) = static_cast<uint16_t>(x + y);
+    if (y > 0) {
+      c.fh_pos = k;
+      c.fh_rem = y;
+    }
+    ++c.r;
+  }
+  c.cum_nf += x;
+  c.cum_f += y;
+  if (c.cum_nf == c.nf_target && c.cum_f == c.free_budget) c.walking = false;
+}
+
+// Called when the walk reached event 0.  Returns true if a second (free-block) walk is needed.
+__device__ __forceinline__ bool chain_walk_restart(ChainRegs& c) {
+  if (!c.walking || c.overflow) return false;
+  // Second walk already done, or LRU (no free blocks): the whole prefix is cached.
+  if (c.free_budget != 0 || c.D == 0) {
+    c.walking = false;
+    return false;
+  }
+  // Every non-free block of the prefix fits (NF_all = cum_nf < C): grant free blocks too.
+  c.nf_target = c.cum_nf;
+  c.free_budget = c.C - c.cum_nf;
+  c.r = c.cum_nf = c.cum_f = 0;
+  c.fh_pos = 0xFFFFFFFFu;
+  c.fh_rem = 0;
+  return true;
+}
+
+__device__ __forceinline__ void chain_walk_finish(ChainRegs& c) {
+  c.walking = false;
+  c.head = c.W - c.r;
+  c.tail = c.W;
+  c.used = c.cum_nf + c.cum_f;
+  if (c.fh_pos != 0xFFFFFFFFu) {
+    c.fh = c.fh_pos;
+    c.frem = c.fh_rem;
+  } else {
+    c.fh = c.tail;
+    c.frem = 0;
+  }
+}
+
+template <class St>
+__device__ __forceinline__ bool chain_compact(ChainRegs& c, const St& st) {
+  uint32_t j = 0;
+  uint32_t new_fh = 0xFFFFFFFFu;
+  const bool fh_dead = (c.fh < c.tail) && st.Xr(c.fh) == 0;
+  for (uint32_t k = c.head; k < c.tail; ++k) {
+    if (k == c.fh) new_fh = j;
+    uint16_t x = st.Xr(k);
+    if (x != 0) {
+      uint32_t t = st.T(k);
+      st.T(j) = t;
+      st.Xr(j) = x;
+      ++j;
+    }
+  }
+  if (c.fh >= c.tail) {
+    new_fh = j;
+  } else if (fh_dead) {  // fh was a tombstone: the next live entry is untouched since insertion
+    c.frem = (new_fh < j) ? min(static_cast<uint32_t>(st.Xr(new_fh)), c.D) : 0u;
+  }
+  c.head = 0;
+  c.tail = j;
+  c.fh = new_fh;
+  return j < c.W;
+}
+
+// Alg. 1 for the request at event index e with sim view (prev, J, La).
+// Returns b = J - X_theta.  Sets c.overflow if the state is full.
+template <class St>
+__device__ __forceinline__ uint32_t chain_request(ChainRegs& c, const St& st, uint32_t e, uint32_t prev, uint32_t J,
+                                                  uint32_t La) {
+  uint32_t x_old = 0;
+  if (prev != TLRU_NONE) {
+    uint32_t lo = c.head, n = c.tail - c.head;
+    while (n > 0) {  // lower_bound of prev in tau[head, tail)
+      uint32_t half = n >> 1;
+      uint32_t m = lo + half;
+      if (st.T(m) < prev) {
+        lo = m + 1;
+        n -= half + 1;
+      } else {
+        n = half;
+      }
+    }
+    if (lo < c.tail && st.T(lo) == prev) {
+      x_old = st.Xr(lo);
+      st.Xr(lo) = 0;
+      if (lo == c.fh) c.frem = 0;
+    }
+  }
+  const uint32_t b = J - x_old;
+  if (c.tail == c.W) {
+    if (!chain_compact(c, st)) {
+      c.overflow = true;
+      return b;
+    }
+  }
+  // Alg. 1 line 1: X_theta <- L_theta (whole history, Reading #7), tau_theta <- now
+  st.T(c.tail) = e;
+  st.Xr(c.tail) = static_cast<uint16_t>(La);
+  if (c.fh == c.tail) c.frem = min(La, c.D);
+  ++c.tail;
+  c.used += La - x_old;
+  if (c.used > c.C) {  // Alg. 1 line 2
+    uint32_t over = c.used - c.C;
+    // Phase 1: TEL-safe trimming, oldest tau first, theta last
+    while (over > 0 && c.fh < c.tail) {
+      uint32_t take = min(c.frem, over);
+      if (take > 0) {
+        st.Xr(c.fh) = static_cast<uint16_t>(st.Xr(c.fh) - take);
+        c.frem -= take;
+        over -= take;
+        c.ev_trim += take;
+      }
+      if (c.frem == 0) {
+        ++c.fh;
+        c.frem = (c.fh < c.tail) ? min(static_cast<uint32_t>(st.Xr(c.fh)), c.D) : 0u;
+      }
+    }
+    // Phase 2: LRU, partial, from the least recently used entry
+    while (over > 0) {
+      uint32_t x = st.Xr(c.head);
+      uint32_t take = min(x, over);
+      st.Xr(c.head) = static_cast<uint16_t>(x - take);
+      over -= take;
+      c.ev_lru += take;
+      if (x == take) ++c.head;
+    }
+    c.used = c.C;
+  }
+  c.max_occ = max(c.max_occ, c.used);
+  return b;
+}
+
+}  // namespace tlru
