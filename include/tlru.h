@@ -207,6 +207,16 @@ tlru_status tlru_simulate_batch(const tlru_trace* traces /*host[nt]*/, uint32_t 
  *   outgrow it are re-run from global memory, so results do not depend on it. */
 tlru_status tlru_set_sim_options(uint32_t segment_events, uint32_t state_entries);
 
+/* Engine of tlru_simulate_batch on this thread (host).  Both are exact and give
+ * identical bytes (tests/test_gpu_parity.py):
+ *   TLRU_ENGINE_REPLAY: K2 -- Alg. 1 replayed request by request, one lane per
+ *     instance, per-chain recency state in shared memory, segments rebuilt exactly;
+ *   TLRU_ENGINE_STACK: closed form of Alg. 1 from the stack property:
+ *     per (trace, D) window sums, every capacity of a trace in one pass; the
+ *     eviction counters by telescoping.  Default. */
+enum { TLRU_ENGINE_REPLAY = 0, TLRU_ENGINE_STACK = 1 };
+tlru_status tlru_set_sim_engine(uint32_t engine);
+
 /* Statistics of the last tlru_simulate_batch on this thread.  Reads two device
  * counters from that call's workspace, so the workspace must not have been
  * reused; synchronizes the device. */
@@ -216,8 +226,10 @@ typedef struct {
   uint64_t spilled_chains;  /* chains re-run with global-memory state */
   uint64_t failed_chains;   /* chains that overflowed even the global-memory state (must be 0) */
   uint32_t kernels;         /* kernel launches issued */
-  uint32_t state_entries;   /* largest on-chip W used */
-  float k2_ms;              /* device time of the simulation kernels (K2 + spill), CUDA events on `stream` */
+  uint32_t state_entries;   /* largest on-chip W used (replay engine) */
+  uint32_t engine;          /* TLRU_ENGINE_* used */
+  uint32_t reserved;
+  float k2_ms;              /* device time of the simulation kernels (K2 + spill, or the stack engine) */
   float k3_ms;              /* device time of the tail-metric kernels (K3) */
 } tlru_sim_stats;
 tlru_status tlru_last_sim_stats(tlru_sim_stats* out /*host*/);

@@ -16,6 +16,8 @@ LIB_PATH = os.path.join(HERE, "libtlru.so")
 TLRU_NONE = 0xFFFFFFFF
 POLICY_LRU = 0
 POLICY_TLRU = 1
+ENGINE_REPLAY = 0
+ENGINE_STACK = 1
 
 STATUS = {0: "TLRU_OK", 1: "TLRU_EINVAL", 2: "TLRU_ERANGE", 3: "TLRU_ECUDA", 4: "TLRU_EUNSUPPORTED",
           5: "TLRU_ESTATE"}
@@ -89,13 +91,14 @@ assert TAIL_DTYPE.itemsize == 104
 class SimStats(ctypes.Structure):
     _fields_ = [("chains", ctypes.c_uint64), ("segment_events", ctypes.c_uint64), ("spilled_chains", ctypes.c_uint64),
                 ("failed_chains", ctypes.c_uint64), ("kernels", ctypes.c_uint32), ("state_entries", ctypes.c_uint32),
-                ("k2_ms", ctypes.c_float), ("k3_ms", ctypes.c_float)]
+                ("k2_ms", ctypes.c_float), ("k3_ms", ctypes.c_float), ("engine", ctypes.c_uint32),
+                ("reserved", ctypes.c_uint32)]
 
 
 EXPORTS = (
     "tlru_last_error", "tlru_version", "tlru_launch_count", "tlru_trace_max_events", "tlru_gen_workspace_size", "tlru_count_events",
     "tlru_generate_traces", "tlru_upload_workspace_size", "tlru_trace_from_turns", "tlru_sim_workspace_size",
-    "tlru_simulate_batch", "tlru_set_sim_options", "tlru_last_sim_stats", "tlru_tail_workspace_size", "tlru_tail_metrics",
+    "tlru_simulate_batch", "tlru_set_sim_options", "tlru_set_sim_engine", "tlru_last_sim_stats", "tlru_tail_workspace_size", "tlru_tail_metrics",
 )
 
 
@@ -119,6 +122,7 @@ def _load():
         "tlru_sim_workspace_size": ([P(Trace), u32, P(Instance), u32, P(sz)], st),
         "tlru_simulate_batch": ([P(Trace), u32, P(Instance), u32, vp, P(u64), vp, vp, sz, vp], st),
         "tlru_set_sim_options": ([u32, u32], st),
+        "tlru_set_sim_engine": ([u32], st),
         "tlru_last_sim_stats": ([P(SimStats)], st),
         "tlru_tail_workspace_size": ([u32, u32, P(sz)], st),
         "tlru_tail_metrics": ([vp, vp, u32, vp, vp, vp, ctypes.c_double, u32, vp, vp, sz, vp], st),

@@ -19,6 +19,7 @@
 
 #include "metrics.cuh"
 #include "sim.cuh"
+#include "stack.cuh"
 
 namespace tlru {
 
@@ -200,6 +201,7 @@ constexpr int kSpillSlots = 128;
 
 static thread_local uint32_t g_opt_seg = 0;  // tlru_set_sim_options
 static thread_local int g_opt_w = -1;
+static thread_local uint32_t g_opt_engine = TLRU_ENGINE_STACK;  // tlru_set_sim_engine
 
 // Entries needed per lane for capacity C: live conversations are bounded by
 // min(C + 1, conversations); the estimate below is the measured resident count of
@@ -384,7 +386,13 @@ extern "C" tlru_status tlru_sim_workspace_size(const tlru_trace* traces, uint32_
   Carver cv(nullptr);
   SimWs w;
   carve_sim(cv, P, ni, &w);
-  *bytes = cv.used;
+  size_t sb = 0;
+  TLRU_TRY(stack_workspace(traces, nt, inst, ni, &sb));
+  Carver cv2(nullptr);
+  cv2.take<SegDev>(ni + 1);
+  cv2.take<uint32_t>(uint64_t(ni + 1) * P.bins);
+  cv2.take<unsigned long long>(ni + 1);
+  *bytes = std::max(cv.used, cv2.used + 256 + sb);
   return TLRU_OK;
 }
 
@@ -402,6 +410,29 @@ extern "C" tlru_status tlru_simulate_batch(const tlru_trace* traces, uint32_t nt
   if (!uncached) {
     for (uint32_t i = 0; i < ni; ++i)
       if (traces[inst[i].trace].num_events > 0) TLRU_FAIL(TLRU_EINVAL, "uncached is NULL");
+  }
+  g_stats.engine = g_opt_engine;
+  if (g_opt_engine == TLRU_ENGINE_STACK) {
+    Carver cv(ws);
+    SegDev* segs = cv.take<SegDev>(ni + 1);
+    uint32_t* hist = cv.take<uint32_t>(uint64_t(ni + 1) * P.bins);
+    unsigned long long* clamped = cv.take<unsigned long long>(ni + 1);
+    TLRU_TRY(check_ws(cv, ws, ws_bytes));
+    std::vector<uint64_t> boffs(ni);
+    for (uint32_t i = 0; i < ni; ++i) boffs[i] = P.segs[i].begin;
+    TLRU_CUDA(cudaMemcpyAsync(segs, P.segs.data(), ni * sizeof(SegDev), cudaMemcpyHostToDevice, st));
+    TLRU_CUDA(cudaMemsetAsync(hist, 0, uint64_t(ni) * P.bins * sizeof(uint32_t), st));
+    TLRU_CUDA(cudaMemsetAsync(clamped, 0, ni * sizeof(unsigned long long), st));
+    unsigned nk = 0;
+    TLRU_TRY(record(0, st));
+    if (!g_ev[1]) TLRU_CUDA(cudaEventCreate(&g_ev[1]));
+    TLRU_TRY(stack_simulate(traces, nt, inst, ni, boffs.data(), uncached, results, cv, segs, P.bins, hist, clamped,
+                            ws_bytes, st, &nk, g_ev[1]));  // records g_ev[1] between the engine and K3
+    TLRU_TRY(record(2, st));
+    g_ev_recorded = true;
+    g_stats.kernels = nk;
+    g_stats.segment_events = 0;
+    return TLRU_OK;
   }
   Carver cv(ws);
   SimWs w;
@@ -475,6 +506,14 @@ extern "C" tlru_status tlru_set_sim_options(uint32_t segment_events, uint32_t st
   }
   g_opt_seg = segment_events;
   g_opt_w = w;
+  return TLRU_OK;
+}
+
+extern "C" tlru_status tlru_set_sim_engine(uint32_t engine) {
+  clear_error();
+  if (engine != TLRU_ENGINE_REPLAY && engine != TLRU_ENGINE_STACK)
+    TLRU_FAIL(TLRU_EINVAL, "engine must be TLRU_ENGINE_REPLAY (0) or TLRU_ENGINE_STACK (1)");
+  g_opt_engine = engine;
   return TLRU_OK;
 }
 

@@ -13,10 +13,11 @@ import numpy as np
 import torch
 
 from . import _abi
-from ._abi import (POLICY_LRU, POLICY_TLRU, RESULT_DTYPE, TAIL_DTYPE, TLRU_NONE, GenParams, Instance, SimStats,
+from ._abi import (ENGINE_REPLAY, ENGINE_STACK, POLICY_LRU, POLICY_TLRU, RESULT_DTYPE, TAIL_DTYPE, TLRU_NONE, GenParams, Instance, SimStats,
                    Trace, TlruError, check, lib)
 
-__all__ = ["DeviceTrace", "generate_traces", "trace_from_turns", "simulate_batch", "tail_metrics", "last_sim_stats", "set_sim_options",
+__all__ = ["DeviceTrace", "generate_traces", "trace_from_turns", "simulate_batch", "tail_metrics", "last_sim_stats", "set_sim_options", "set_sim_engine",
+           "ENGINE_REPLAY", "ENGINE_STACK",
            "POLICY_LRU", "POLICY_TLRU", "TLRU_NONE", "TlruError", "RESULT_DTYPE", "TAIL_DTYPE", "version"]
 
 
@@ -200,6 +201,11 @@ def simulate_batch(traces: list[DeviceTrace], rows, stream=None) -> SimBatch:
 def set_sim_options(segment_events: int = 0, state_entries: int = 0) -> None:
     """tlru_set_sim_options (0 = automatic); results never depend on these."""
     check(lib.tlru_set_sim_options(segment_events, state_entries))
+
+
+def set_sim_engine(engine: int) -> None:
+    """tlru_set_sim_engine: ENGINE_REPLAY (Alg. 1 replay, K2) or ENGINE_STACK (closed form, default)."""
+    check(lib.tlru_set_sim_engine(engine))
 
 
 def last_sim_stats() -> dict:

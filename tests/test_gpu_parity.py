@@ -26,6 +26,10 @@ def T():
     T.set_sim_options(0, 0)
     yield T
     T.set_sim_options(0, 0)
+    T.set_sim_engine(T.ENGINE_STACK)
+
+
+ENGINES = pytest.mark.parametrize("engine", [0, 1], ids=["replay", "stack"])
 
 
 def upload(T, conv, q, a):
@@ -53,7 +57,9 @@ def check_instances(T, batch, rows, oracle_traces, alpha=ALPHA_MS):
 
 
 # ----------------------------------------------------------------------------- config 1: Figure 1
-def test_fig1_through_the_abi(T):
+@ENGINES
+def test_fig1_through_the_abi(T, engine):
+    T.set_sim_engine(engine)
     tr = upload(T, FIG1["conv"], FIG1["q"], FIG1["a"])
     rows = [(0, 0, FIG1["C"], FIG1["xi"], FIG1["q_hat"], 0), (0, 1, FIG1["C"], FIG1["xi"], FIG1["q_hat"], 0)]
     bt = T.simulate_batch([tr], rows)
@@ -67,7 +73,9 @@ def test_fig1_through_the_abi(T):
 
 
 # ----------------------------------------------------------------------------- config 2: tiny traces, full grid
-def test_tiny_traces_full_parameter_grid(T):
+@ENGINES
+def test_tiny_traces_full_parameter_grid(T, engine):
+    T.set_sim_engine(engine)
     traces, otr, rows = [], [], []
     for seed in range(120):
         conv, q, a = tiny_trace(seed)
@@ -107,6 +115,7 @@ def test_segment_warm_start_is_exact(T, seg):
         for pol, xi, qh in ((0, 0, 0), (1, 6, 2), (1, 20, 2), (1, 40, 1), (1, 2, 2)):
             for C in (0, 1, 7, 30, 120, 500, 100000):
                 rows.append((s, pol, C, xi, qh, 16))
+    T.set_sim_engine(T.ENGINE_REPLAY)
     T.set_sim_options(seg, 0)
     try:
         bt = T.simulate_batch(traces, rows)
@@ -123,6 +132,7 @@ def test_spill_path_is_exact(T):
     conv, q, a = random_trace(11, 4000, 400, q_max=3, a_max=3, locality=0.3)
     tr = upload(T, conv, q, a)
     rows = [(0, pol, C, xi, 1, 16) for pol in (0, 1) for C in (50, 200, 800) for xi in (0, 9)]
+    T.set_sim_engine(T.ENGINE_REPLAY)
     T.set_sim_options(256, 32)
     try:
         bt = T.simulate_batch([tr], rows)
@@ -138,7 +148,8 @@ def test_determinism_across_launch_configs(T):
     tr = upload(T, conv, q, a)
     rows = [(0, pol, C, 12, 2, 16) for pol in (0, 1) for C in (10, 60, 300)]
     outs = []
-    for seg, w in ((0, 0), (64, 0), (2048, 1024), (128, 64)):
+    for engine, seg, w in ((0, 0, 0), (0, 64, 0), (0, 2048, 1024), (0, 128, 64), (1, 0, 0)):
+        T.set_sim_engine(engine)
         T.set_sim_options(seg, w)
         bt = T.simulate_batch([tr], rows)
         outs.append((b"".join(bt.b(i).tobytes() for i in range(len(rows))), bt.results.cpu().numpy().tobytes()))
@@ -167,9 +178,11 @@ def test_generator_bit_exact(T, name, seed, n):
 
 
 # ----------------------------------------------------------------------------- config 3: 10^4 conversations
-def test_config3_full_parity(T):
+@ENGINES
+def test_config3_full_parity(T, engine):
     """BASELINE config 3: 10^4-conversation WildChat-shaped traces, seeds 0..9,
     C in {32..1024}, xi in {4..40} (50..500 ms), Q_hat = 2, LRU and T-LRU."""
+    T.set_sim_engine(engine)
     params = [preset("wildchat", s, 10_000) for s in range(10)]
     traces = T.generate_traces(params, exports=False)
     otr = []
@@ -183,10 +196,12 @@ def test_config3_full_parity(T):
 
 
 # ----------------------------------------------------------------------------- config 4 (bench launch), sampled
-def test_config4_bench_launch_sampled(T):
+@ENGINES
+def test_config4_bench_launch_sampled(T, engine):
     """The bench's launch configuration (10^6 conversations, 96 instances of one
     seed in one batch); every capacity checked against the oracle for one xi per
     policy, and every instance checked for properties that hold at any size."""
+    T.set_sim_engine(engine)
     p = preset("wildchat", 0, 1_000_000)
     g = T.generate_traces([p], exports=False)[0]
     o = O.generate(p)
@@ -255,11 +270,15 @@ def test_upload_errors(T):
     with pytest.raises(T.TlruError, match="ERANGE"):
         upload(T, [0, 0], [40000, 30000], [0, 0])
     tr = upload(T, [0], [1], [0])
+    with pytest.raises(T.TlruError, match="EINVAL"):
+        T.set_sim_engine(7)
     with pytest.raises(T.TlruError, match="EUNSUPPORTED"):
         T.simulate_batch([tr], [(0, 2, 10, 0, 0, 0)])
 
 
-def test_empty_trace(T):
+@ENGINES
+def test_empty_trace(T, engine):
+    T.set_sim_engine(engine)
     tr = upload(T, [], [], [])
     assert tr.num_events == 0
     bt = T.simulate_batch([tr], [(0, 1, 10, 4, 2, 16)])
