@@ -23,7 +23,6 @@ import argparse
 import json
 import os
 import statistics
-import subprocess
 import sys
 import threading
 import time
@@ -52,56 +51,44 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+    """SM clocks and throttle reasons sampled through NVML (the library nvidia-smi reads)
+    every 10 ms in a background thread while the timed region runs."""
 
-    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20, "sw_power_cap": 0x4}
 
     def __init__(self, index: int):
         self.index = index
-        self.proc = None
-        self.lines = []
+        self.sm, self.mx, self.reasons = [], 0, set()
+        self.stop = threading.Event()
+
+    def _run(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            while not self.stop.is_set():
+                self.sm.append(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
+                r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                for n, bit in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(n)
+                time.sleep(0.01)
+        except Exception as ex:  # noqa: BLE001 -- report, never fail the bench
+            self.error = repr(ex)
 
     def __enter__(self):
-        try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
-        except FileNotFoundError:
-            self.proc = None
+        self.t = threading.Thread(target=self._run, daemon=True)
+        self.t.start()
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
-
     def __exit__(self, *a):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except subprocess.TimeoutExpired:
-                self.proc.kill()
+        self.stop.set()
+        self.t.join(timeout=5)
 
     def summary(self):
-        sm, mx, reasons = [], 0.0, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            f = [x.strip() for x in ln.split(",")]
-            if len(f) < 6:
-                continue
-            try:
-                sm.append(float(f[0]))
-                mx = max(mx, float(f[1]))
-            except ValueError:
-                continue
-            for n, v in zip(names, f[2:6]):
-                if v.lower() == "active":
-                    reasons.add(n)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        return {"sm_mhz": statistics.median(self.sm) if self.sm else None, "sm_max_mhz": self.mx or None,
+                "reasons": sorted(self.reasons), "samples": len(self.sm)}
 
 
 # ----------------------------------------------------------------------------- reference (CPU oracle)
@@ -226,29 +213,39 @@ def run_ours(args, rank, world, local_rank):
             dist.barrier()
         torch.cuda.synchronize()
 
-    # ---- warmup
-    for _ in range(args.warmup):
-        step()
-    barrier()
-    launches0 = _abi.lib.tlru_launch_count()
-    k2_ms, k3_ms = [], []
-    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local_rank) as clk:
-        barrier()
-        start.record(stream)
-        for _ in range(args.steps):
+    def timed(engine: int, steps: int, warmup: int):
+        T.set_sim_engine(engine)
+        for _ in range(warmup):
             step()
-            st = T.last_sim_stats()
-            k2_ms.append(st["k2_ms"])
-            k3_ms.append(st["k3_ms"])
-        stop.record(stream)
         barrier()
-    launches = _abi.lib.tlru_launch_count() - launches0
-    ms = start.elapsed_time(stop) / args.steps
-    stats = T.last_sim_stats()
-    res = batch.results_numpy()
-    assert stats["failed_chains"] == 0
-    assert np.all(res["requests"][:ni] > 0)
+        l0 = _abi.lib.tlru_launch_count()
+        k2s, k3s = [], []
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with ClockSampler(local_rank) as clk:
+            barrier()
+            t0.record(stream)
+            for _ in range(steps):
+                step()
+                st = T.last_sim_stats()
+                k2s.append(st["k2_ms"])
+                k3s.append(st["k3_ms"])
+            t1.record(stream)
+            barrier()
+        st = T.last_sim_stats()
+        assert st["failed_chains"] == 0
+        res = batch.results_numpy()
+        assert np.all(res["requests"][:ni] > 0)
+        return dict(ms=t0.elapsed_time(t1) / steps, k2=statistics.mean(k2s), k3=statistics.mean(k3s),
+                    launches=(_abi.lib.tlru_launch_count() - l0), clocks=clk.summary(), stats=st,
+                    results=res.tobytes())
+
+    main = timed(T.ENGINE_STACK, args.steps, args.warmup)
+    rep = timed(T.ENGINE_REPLAY, max(1, args.steps // 2), 1) if not args.no_replay else None
+    if rep is not None:
+        assert rep["results"] == main["results"], "engines disagree"
+    T.set_sim_engine(T.ENGINE_STACK)
+    ms, launches, clocks, stats = main["ms"], main["launches"], main["clocks"], main["stats"]
+    k2_ms, k3_ms = [main["k2"]], [main["k3"]]
 
     # ---- e2e (same batch through the public API from host buffers)
     for _ in range(max(1, args.warmup)):
@@ -263,10 +260,11 @@ def run_ours(args, rank, world, local_rank):
     e2e_ms = t_e2e[0].elapsed_time(t_e2e[1]) / args.steps
 
     # ---- max over ranks
-    loc = torch.tensor([ms, e2e_ms, statistics.mean(k2_ms), statistics.mean(k3_ms)], dtype=torch.float64, device=dev)
+    loc = torch.tensor([ms, e2e_ms, statistics.mean(k2_ms), statistics.mean(k3_ms),
+                        rep["ms"] if rep else 0.0, rep["k2"] if rep else 0.0], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(loc, op=dist.ReduceOp.MAX)
-    ms, e2e_ms, k2, k3 = [float(x) for x in loc.tolist()]
+    ms, e2e_ms, k2, k3, rep_ms, rep_k2 = [float(x) for x in loc.tolist()]
     if rank != 0:
         return
     req_all = E_tot * world
@@ -289,17 +287,27 @@ def run_ours(args, rank, world, local_rank):
             "instances_per_gpu": ni, "requests_per_gpu_step": E_tot, "conversations": args.conversations,
             "parallelism": f"dp{world} (instances sharded by seed, NCCL all_gather of results)",
             "l2": "inputs larger than L2: 0.77 GB of b written per GPU-step",
-            "engine": "K2 time-partitioned Alg. 1 simulation; no dedup, no closed-form fast path",
-            "segment_events": stats["segment_events"], "k2_ms": k2, "k3_ms": k3,
+            "engine": "stack (closed form of Alg. 1 from the stack property, all capacities of a trace per pass; "
+                      "bit-identical to the replay engine and the oracle); no dedup of identical instances",
+            "engine_ms": k2, "k3_ms": k3,
         },
         "e2e": {"value": req_all / (e2e_ms / 1000.0), "unit": "requests/s", "h2d_bytes_per_step": h2d_bytes,
                 "d2h_bytes_per_step": d2h_bytes, "ms_per_step": e2e_ms},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "kernel": "sim_kernel<W> (K2 phase)", "peak_source": peak_src,
+                     "traffic": traffic, "kernel": "s1/s2 stack-engine kernels (simulation phase)",
+                     "peak_source": peak_src,
                      "algorithmic_bytes_per_request": ALGO_BYTES_PER_REQUEST},
-        "gpu_launches": int(launches),
-        "clocks": clk.summary(),
+        "gpu_launches": int(launches // max(args.steps, 1)),
+        "clocks": clocks,
     }
+    if rep is not None:
+        rep_achieved = ALGO_BYTES_PER_REQUEST * E_tot / (rep_k2 / 1000.0) / 1e9
+        line["replay_engine"] = {
+            "value": req_all / (rep_ms / 1000.0), "unit": "requests/s", "ms_per_step": rep_ms, "k2_ms": rep_k2,
+            "segment_events": rep["stats"]["segment_events"], "spilled_chains": rep["stats"]["spilled_chains"],
+            "roofline": {"bound": "hbm", "achieved": rep_achieved, "peak": peak, "unit": "GB/s",
+                         "frac": rep_achieved / peak, "kernel": "sim_kernel<W> (K2 replay)"},
+            "note": "Alg. 1 replayed request by request (one lane per instance); identical result bytes"}
     if not args.no_cpu_baseline:
         n, dt, cores, sample = cpu_oracle_sample(seed=0, n_conv=args.conversations)
         line["cpu_baseline"] = {"value": n / dt, "unit": "requests/s", "cores": cores, "kind": "oracle",
@@ -315,6 +323,7 @@ def main():
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--conversations", type=int, default=1_000_000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-replay", action="store_true", help="skip timing the replay engine")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

@@ -1,16 +1,19 @@
 // gen.cu -- K1: synthetic traces from the paper's stochastic conversation model
 // (Sec. 5; App. E recipe P:724) and the upload path for host traces.
 //
-//   count   : one thread per conversation replays its birth/death clocks and turn
-//             process, counting emitted turns (the context-window rule needs the
-//             lengths, so the lengths are drawn here too)
+//   count   : one thread per conversation: birth gap, death / turn clocks -> turn count;
+//             the few conversations that could reach the context cap L_max are queued
+//             and recounted exactly with their lengths (count_fix)
 //   scan    : birth ticks = inclusive scan of Exp(lambda_conv) gaps (integer, so
 //             order-independent); per-conversation event offsets = exclusive scan
-//   emit    : the same replay again, writing events in conversation order
+//   slot/draw: one thread per event slot draws its turn gap and prompt / response lengths
+//   emit    : one thread per conversation: prefix sums of gaps (time) and lengths (J, L_after)
 //   sort    : stable radix sort on the 64-bit arrival tick; conversation order is
 //             (conv, turn), so ties come out ordered by (conv, turn) (Reading #9)
 //   link    : scatter to time order, prev/next links and the 8-byte sim view
 #include <cub/cub.cuh>
+
+#include <algorithm>
 
 #include "common.cuh"
 #include "rng.cuh"
@@ -20,80 +23,127 @@ namespace tlru {
 struct GenDev {  // per-trace constants, by value to the kernels
   uint64_t seed;
   uint32_t N, B, Lmax, max_turns;
+  uint32_t safe_turns;  // a conversation with at most this many turns can never hit L_max
   double us_birth, us_turn, us_death;  // 1e6 / rate
   double p_mean, p_sigma, r_mean, r_sigma;
   uint32_t p_lo, p_hi, r_lo, r_hi;
 };
 
-// Replays conversation c.  EMIT=false: counts turns; EMIT=true: writes them at `base`.
-template <bool EMIT>
-__device__ __forceinline__ uint32_t conv_process(const GenDev& g, uint32_t c, uint64_t birth, uint32_t base,
-                                                 uint64_t* key, uint32_t* cid, uint16_t* q16, uint16_t* a16,
-                                                 uint16_t* J16, uint16_t* La16, uint8_t* last8,
-                                                 uint64_t* last_elapsed, uint32_t* last_L) {
+// Exact turn count of conversation c: death/turn clocks plus the context-window rule,
+// which needs the lengths.  Used only for conversations that may reach L_max.
+__device__ __forceinline__ uint32_t conv_count_exact(const GenDev& g, uint32_t c) {
   const uint64_t life = exp_gap_ticks(g.seed, c, 0, FIELD_DEATH, g.us_death);  // Exp(mu) lifetime
   const double p_mu = lognormal_mu(g.p_mean, g.p_sigma), r_mu = lognormal_mu(g.r_mean, g.r_sigma);
-  uint64_t elapsed = 0, emitted_elapsed = 0;
+  uint64_t elapsed = 0;
   uint32_t L = 0, n = 0;
   for (uint32_t k = 0; k < g.max_turns; ++k) {
     if (k > 0) {  // Poisson(lambda_turn) turns while alive
       elapsed += exp_gap_ticks(g.seed, c, k, FIELD_TURN_GAP, g.us_turn);
       if (elapsed >= life) break;
     }
-    // Prompt Q and response A lengths -> blocks (Reading #16)
-    uint32_t pt = lognormal_tokens(g.seed, c, k, FIELD_PROMPT, p_mu, g.p_sigma, g.p_lo, g.p_hi);
-    uint32_t rt = lognormal_tokens(g.seed, c, k, FIELD_RESPONSE, r_mu, g.r_sigma, g.r_lo, g.r_hi);
+    const uint32_t pt = lognormal_tokens(g.seed, c, k, FIELD_PROMPT, p_mu, g.p_sigma, g.p_lo, g.p_hi);
+    const uint32_t rt = lognormal_tokens(g.seed, c, k, FIELD_RESPONSE, r_mu, g.r_sigma, g.r_lo, g.r_hi);
     uint32_t q = (pt + g.B - 1) / g.B;
     if (q < 1) q = 1;
-    uint32_t a = (rt + g.B - 1) / g.B;
+    const uint32_t a = (rt + g.B - 1) / g.B;
     if (uint64_t(L) + q + a > g.Lmax) break;  // context-window end
-    if (EMIT) {
-      uint32_t j = base + n;
-      key[j] = birth + elapsed;
-      cid[j] = c;
-      q16[j] = static_cast<uint16_t>(q);
-      a16[j] = static_cast<uint16_t>(a);
-      J16[j] = static_cast<uint16_t>(L + q);
-      La16[j] = static_cast<uint16_t>(L + q + a);
-      last8[j] = 0;
-    }
     L += q + a;
-    emitted_elapsed = elapsed;
     ++n;
   }
-  if (EMIT && n > 0) last8[base + n - 1] = 1;
-  *last_elapsed = emitted_elapsed;
-  *last_L = L;
   return n;
 }
 
+// Turns allowed by the death clock and max_turns alone (no lengths drawn).
+__device__ __forceinline__ uint32_t clock_turns(const GenDev& g, uint32_t c, uint64_t* last_elapsed) {
+  const uint64_t life = exp_gap_ticks(g.seed, c, 0, FIELD_DEATH, g.us_death);
+  uint64_t elapsed = 0, kept = 0;
+  uint32_t n = 1;
+  for (uint32_t k = 1; k < g.max_turns; ++k) {
+    elapsed += exp_gap_ticks(g.seed, c, k, FIELD_TURN_GAP, g.us_turn);
+    if (elapsed >= life) break;
+    kept = elapsed;
+    ++n;
+  }
+  *last_elapsed = kept;
+  return n;
+}
+
+// Births + death/turn clocks only.  Conversations long enough to possibly reach L_max are
+// queued for an exact replay with lengths (gen_count_fix_kernel), so no warp diverges into
+// the lognormal sampling here.
 __global__ void gen_count_kernel(GenDev g, uint64_t* gaps, uint32_t* counts, unsigned long long* max_elapsed,
-                                 uint32_t* max_L, uint32_t* nconv) {
+                                 uint32_t* queue, uint32_t* nqueue) {
   for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < g.N; c += gridDim.x * blockDim.x) {
     gaps[c] = exp_gap_ticks(g.seed, c, 0, FIELD_BIRTH, g.us_birth);  // Poisson(lambda_conv) births
     uint64_t el;
-    uint32_t L;
-    uint32_t n = conv_process<false>(g, c, 0, 0, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
-                                     &el, &L);
+    const uint32_t n = clock_turns(g, c, &el);
     counts[c] = n;
-    if (n > 0) {
-      atomicMax(max_elapsed, static_cast<unsigned long long>(el));
-      atomicMax(max_L, L);
-      atomicAdd(nconv, 1u);
-    }
+    atomicMax(max_elapsed, static_cast<unsigned long long>(el));
+    if (n > g.safe_turns) queue[atomicAdd(nqueue, 1u)] = c;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) counts[g.N] = 0;
 }
 
-__global__ void gen_emit_kernel(GenDev g, const uint64_t* birth, const uint32_t* off, uint64_t* key, uint32_t* val,
-                                uint32_t* cid, uint16_t* q16, uint16_t* a16, uint16_t* J16, uint16_t* La16,
-                                uint8_t* last8) {
+__global__ void gen_count_fix_kernel(GenDev g, const uint32_t* queue, const uint32_t* nqueue, uint32_t* counts) {
+  const uint32_t nq = *nqueue;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nq; i += gridDim.x * blockDim.x) {
+    const uint32_t c = queue[i];
+    counts[c] = conv_count_exact(g, c);
+  }
+}
+
+// One thread per conversation: label its event slots with (conversation, turn).
+__global__ void gen_slot_kernel(GenDev g, const uint32_t* off, uint32_t* cid, uint16_t* turn) {
   for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < g.N; c += gridDim.x * blockDim.x) {
-    uint64_t el;
-    uint32_t L;
-    uint32_t base = off[c];
-    uint32_t n = conv_process<true>(g, c, birth[c], base, key, cid, q16, a16, J16, La16, last8, &el, &L);
-    for (uint32_t k = 0; k < n; ++k) val[base + k] = base + k;
+    const uint32_t b = off[c], n = off[c + 1] - b;
+    for (uint32_t k = 0; k < n; ++k) {
+      cid[b + k] = c;
+      turn[b + k] = static_cast<uint16_t>(k);
+    }
+  }
+}
+
+// One thread per event slot: the turn's random draws: gap to the previous turn
+// (turn > 0) and the prompt / response lengths in blocks (Reading #16).
+__global__ void gen_draw_kernel(GenDev g, uint32_t E, const uint32_t* cid, const uint16_t* turn, uint64_t* gapt,
+                                uint16_t* q16, uint16_t* a16) {
+  const double p_mu = lognormal_mu(g.p_mean, g.p_sigma), r_mu = lognormal_mu(g.r_mean, g.r_sigma);
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < E; j += gridDim.x * blockDim.x) {
+    const uint32_t c = cid[j], k = turn[j];
+    gapt[j] = k ? exp_gap_ticks(g.seed, c, k, FIELD_TURN_GAP, g.us_turn) : 0ull;
+    const uint32_t pt = lognormal_tokens(g.seed, c, k, FIELD_PROMPT, p_mu, g.p_sigma, g.p_lo, g.p_hi);
+    const uint32_t rt = lognormal_tokens(g.seed, c, k, FIELD_RESPONSE, r_mu, g.r_sigma, g.r_lo, g.r_hi);
+    uint32_t q = (pt + g.B - 1) / g.B;
+    if (q < 1) q = 1;
+    q16[j] = static_cast<uint16_t>(q);
+    a16[j] = static_cast<uint16_t>((rt + g.B - 1) / g.B);
+  }
+}
+
+// One thread per conversation, no random draws: arrival ticks and history prefix sums over its
+// (already exact) slots; J = L_before + q, L_after = J + a.
+__global__ void gen_emit_kernel(GenDev g, const uint64_t* birth, const uint32_t* off, const uint64_t* gapt,
+                                const uint16_t* q16, const uint16_t* a16, uint64_t* key, uint32_t* val,
+                                uint16_t* J16, uint16_t* La16, uint8_t* last8, uint32_t* max_L, uint32_t* nconv) {
+  for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < g.N; c += gridDim.x * blockDim.x) {
+    const uint32_t b = off[c], n = off[c + 1] - b;
+    uint64_t t = birth[c];
+    uint32_t L = 0;
+    for (uint32_t k = 0; k < n; ++k) {
+      const uint32_t j = b + k;
+      t += gapt[j];
+      key[j] = t;
+      val[j] = j;
+      L += q16[j];
+      J16[j] = static_cast<uint16_t>(L);
+      L += a16[j];
+      La16[j] = static_cast<uint16_t>(L);
+      last8[j] = (k + 1 == n) ? 1 : 0;
+    }
+    if (n > 0) {
+      atomicMax(max_L, L);
+      atomicAdd(nconv, 1u);
+    }
   }
 }
 
@@ -150,6 +200,11 @@ static GenDev make_dev(const tlru_gen_params* p) {
   g.B = p->block_tokens;
   g.Lmax = p->max_history_blocks;
   g.max_turns = p->max_turns;
+  {
+    const uint64_t qmax = std::max<uint64_t>(1, (uint64_t(p->prompt_max_tokens) + p->block_tokens - 1) / p->block_tokens);
+    const uint64_t amax = (uint64_t(p->response_max_tokens) + p->block_tokens - 1) / p->block_tokens;
+    g.safe_turns = static_cast<uint32_t>(std::min<uint64_t>(p->max_turns, p->max_history_blocks / (qmax + amax)));
+  }
   g.us_birth = 1000000.0 / p->birth_rate;
   g.us_turn = 1000000.0 / p->turn_rate;
   g.us_death = 1000000.0 / p->death_rate;
@@ -172,6 +227,10 @@ struct GenWs {
   unsigned long long* max_elapsed;
   uint32_t* max_L;
   uint32_t* nconv;
+  uint32_t* queue;   // [N] conversations needing an exact length replay in the count pass
+  uint32_t* nqueue;
+  uint16_t* turn;    // [E] turn index of each event slot
+  uint64_t* gapt;    // [E] gap ticks to the previous turn
   uint64_t* key[2];
   uint32_t* val[2];
   uint32_t* cid;
@@ -190,6 +249,10 @@ static tlru_status carve_gen(Carver& cv, uint32_t N, uint64_t cap, GenWs* w) {
   w->max_elapsed = cv.take<unsigned long long>(1);
   w->max_L = cv.take<uint32_t>(1);
   w->nconv = cv.take<uint32_t>(1);
+  w->queue = cv.take<uint32_t>(N);
+  w->nqueue = cv.take<uint32_t>(1);
+  w->turn = cv.take<uint16_t>(cap);
+  w->gapt = cv.take<uint64_t>(cap);
   for (int i = 0; i < 2; ++i) {
     w->key[i] = cv.take<uint64_t>(cap);
     w->val[i] = cv.take<uint32_t>(cap);
@@ -215,14 +278,15 @@ static tlru_status carve_gen(Carver& cv, uint32_t N, uint64_t cap, GenWs* w) {
   return TLRU_OK;
 }
 
-// Runs count + scans; fills E (host), max tick bound, max_L, nconv.  Synchronizes.
+// Runs count + scans; fills E (host) and the max tick bound.  Synchronizes.
 static tlru_status run_count(const tlru_gen_params* p, const GenWs& w, cudaStream_t st, uint64_t* E,
-                             uint64_t* max_tick, uint32_t* maxL, uint32_t* nconv) {
+                             uint64_t* max_tick) {
   GenDev g = make_dev(p);
   TLRU_CUDA(cudaMemsetAsync(w.max_elapsed, 0, sizeof(unsigned long long), st));
-  TLRU_CUDA(cudaMemsetAsync(w.max_L, 0, sizeof(uint32_t), st));
-  TLRU_CUDA(cudaMemsetAsync(w.nconv, 0, sizeof(uint32_t), st));
-  gen_count_kernel<<<grid_for(g.N, 128), 128, 0, st>>>(g, w.gaps, w.counts, w.max_elapsed, w.max_L, w.nconv);
+  TLRU_CUDA(cudaMemsetAsync(w.nqueue, 0, sizeof(uint32_t), st));
+  gen_count_kernel<<<grid_for(g.N, 128), 128, 0, st>>>(g, w.gaps, w.counts, w.max_elapsed, w.queue, w.nqueue);
+  TLRU_CHECK_LAUNCH();
+  gen_count_fix_kernel<<<grid_for(g.N / 8 + 1, 128), 128, 0, st>>>(g, w.queue, w.nqueue, w.counts);
   TLRU_CHECK_LAUNCH();
   size_t b = w.cub_bytes;
   TLRU_CUDA(cub::DeviceScan::InclusiveSum(w.cub_tmp, b, w.gaps, w.birth, static_cast<int>(g.N), st));
@@ -234,8 +298,6 @@ static tlru_status run_count(const tlru_gen_params* p, const GenWs& w, cudaStrea
   TLRU_CUDA(cudaMemcpyAsync(&totalE, w.off + g.N, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
   TLRU_CUDA(cudaMemcpyAsync(&last_birth, w.birth + (g.N - 1), sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
   TLRU_CUDA(cudaMemcpyAsync(&mel, w.max_elapsed, sizeof(mel), cudaMemcpyDeviceToHost, st));
-  TLRU_CUDA(cudaMemcpyAsync(maxL, w.max_L, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
-  TLRU_CUDA(cudaMemcpyAsync(nconv, w.nconv, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
   TLRU_CUDA(cudaStreamSynchronize(st));
   *E = totalE;
   *max_tick = last_birth + mel;
@@ -352,8 +414,7 @@ extern "C" tlru_status tlru_count_events(const tlru_gen_params* p, uint64_t* out
   TLRU_TRY(carve_gen(cv, p->num_conversations, 0, &w));
   TLRU_TRY(check_ws(cv, ws, ws_bytes));
   uint64_t mt;
-  uint32_t mL, nc;
-  return run_count(p, w, stream, out, &mt, &mL, &nc);
+  return run_count(p, w, stream, out, &mt);
 }
 
 extern "C" tlru_status tlru_generate_traces(const tlru_gen_params* params, uint32_t n, tlru_trace* traces, void* ws,
@@ -371,15 +432,26 @@ extern "C" tlru_status tlru_generate_traces(const tlru_gen_params* params, uint3
     TLRU_TRY(carve_gen(cv, p->num_conversations, tr->capacity, &w));
     TLRU_TRY(check_ws(cv, ws, ws_bytes));
     uint64_t E, max_tick;
-    uint32_t maxL, nconv;
-    TLRU_TRY(run_count(p, w, st, &E, &max_tick, &maxL, &nconv));
+    TLRU_TRY(run_count(p, w, st, &E, &max_tick));
     if (E > tr->capacity)
       TLRU_FAIL(TLRU_ERANGE, "trace %u: %llu events exceed capacity %llu", t, (unsigned long long)E,
                 (unsigned long long)tr->capacity);
     GenDev g = make_dev(p);
-    gen_emit_kernel<<<grid_for(g.N, 128), 128, 0, st>>>(g, w.birth, w.off, w.key[0], w.val[0], w.cid, w.q16, w.a16,
-                                                         w.J16, w.La16, w.last8);
+    TLRU_CUDA(cudaMemsetAsync(w.max_L, 0, sizeof(uint32_t), st));
+    TLRU_CUDA(cudaMemsetAsync(w.nconv, 0, sizeof(uint32_t), st));
+    gen_slot_kernel<<<grid_for(g.N, 128), 128, 0, st>>>(g, w.off, w.cid, w.turn);
     TLRU_CHECK_LAUNCH();
+    if (E > 0) {
+      gen_draw_kernel<<<grid_for(E, 128), 128, 0, st>>>(g, static_cast<uint32_t>(E), w.cid, w.turn, w.gapt, w.q16,
+                                                         w.a16);
+      TLRU_CHECK_LAUNCH();
+    }
+    gen_emit_kernel<<<grid_for(g.N, 128), 128, 0, st>>>(g, w.birth, w.off, w.gapt, w.q16, w.a16, w.key[0], w.val[0],
+                                                         w.J16, w.La16, w.last8, w.max_L, w.nconv);
+    TLRU_CHECK_LAUNCH();
+    uint32_t stats[2];
+    TLRU_CUDA(cudaMemcpyAsync(&stats[0], w.max_L, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    TLRU_CUDA(cudaMemcpyAsync(&stats[1], w.nconv, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
     int end_bit = 1;
     while (end_bit < 64 && (max_tick >> end_bit) != 0) ++end_bit;
     if (E > 0) {
@@ -395,9 +467,10 @@ extern "C" tlru_status tlru_generate_traces(const tlru_gen_params* params, uint3
                                                         tr->sim, tr->next);
       TLRU_CHECK_LAUNCH();
     }
+    TLRU_CUDA(cudaStreamSynchronize(st));
     tr->num_events = E;
-    tr->max_history = maxL;
-    tr->num_conversations = nconv;
+    tr->max_history = stats[0];
+    tr->num_conversations = stats[1];
   }
   return TLRU_OK;
 }

@@ -60,10 +60,10 @@ struct SatAdd {
 
 struct ChunkDev {
   uint32_t D[SND];
-  uint32_t Cmax[SND];  // largest capacity among the chunk's instances with this D
+  uint32_t Cmax[SND];     // largest capacity among the chunk's instances with this D
+  uint32_t dbeg[SND + 1]; // instances of D[d]: [inst0 + dbeg[d], inst0 + dbeg[d+1])
   uint32_t nd;
   uint32_t inst0, ninst;  // instances [inst0, inst0 + ninst) of the StackInstDev table
-  uint32_t pad;
 };
 
 struct StackInstDev {
@@ -71,9 +71,13 @@ struct StackInstDev {
   uint64_t boff;
 };
 
-struct ChunkTotals {  // per (chunk, d)
-  unsigned long long sumF[SND];
-  unsigned long long suma;
+struct ChunkTotals {  // per chunk: exact trace totals
+  unsigned long long sumF[SND];  // sum_e F(L_after_e)
+  unsigned long long nfE[SND];   // NF_all(E): non-free blocks of the final universe
+  unsigned long long fE[SND];    // F_all(E)
+  unsigned long long suma;       // sum_e a_e
+  uint32_t nsat;                 // first block whose prefix saturates every D (NF_all >= Cmax)
+  uint32_t pad;
 };
 
 __device__ __forceinline__ uint32_t nf_of(uint32_t L, uint32_t D) { return L > D ? L - D : 0u; }
@@ -98,26 +102,33 @@ __device__ __forceinline__ uint32_t L_before(const uint64_t* sim, uint64_t s) {
   return p == TLRU_NONE ? 0u : sim_La(__ldg(sim + p));
 }
 
-// s1: block aggregates of the deltas (saturating) + trace totals sum F(L_after), sum a.
-__global__ void __launch_bounds__(S_THREADS) s1_block_kernel(const uint64_t* __restrict__ sim, uint32_t E,
+// s1: per-event scan record (next | L_after << 32) for the window scans, block aggregates of
+// the universe deltas (saturating), and the exact trace totals.
+__global__ void __launch_bounds__(S_THREADS) s1_block_kernel(const uint64_t* __restrict__ sim,
+                                                             const uint32_t* __restrict__ next, uint32_t E,
                                                              const ChunkDev* __restrict__ chunk,
+                                                             uint64_t* __restrict__ scanrec,
                                                              Prefix8* __restrict__ blockagg, ChunkTotals* totals) {
   __shared__ ChunkDev ch;
   if (threadIdx.x == 0) ch = *chunk;
   __syncthreads();
   const uint32_t e = blockIdx.x * S_THREADS + threadIdx.x;
   Prefix8 v{};
-  unsigned long long sa = 0;
-  unsigned long long sf[SND];
+  unsigned long long tv[3 * SND + 1];
 #pragma unroll
-  for (int d = 0; d < SND; ++d) sf[d] = 0;
+  for (int k = 0; k < 3 * SND + 1; ++k) tv[k] = 0;
   if (e < E) {
     const uint64_t s = __ldg(sim + e);
     const uint32_t La = sim_La(s);
+    scanrec[e] = uint64_t(__ldg(next + e)) | (uint64_t(La) << 32);
     universe_delta(ch, L_before(sim, s), La, v);
-    sa = La - sim_J(s);
 #pragma unroll
-    for (int d = 0; d < SND; ++d) sf[d] = f_of(La, ch.D[d]);
+    for (int d = 0; d < SND; ++d) {
+      tv[d] = f_of(La, ch.D[d]);
+      tv[SND + d] = v.nf[d];
+      tv[2 * SND + d] = v.f[d];
+    }
+    tv[3 * SND] = La - sim_J(s);
   }
   typedef cub::BlockReduce<Prefix8, S_THREADS> BRp;
   typedef cub::BlockReduce<unsigned long long, S_THREADS> BR;
@@ -127,52 +138,90 @@ __global__ void __launch_bounds__(S_THREADS) s1_block_kernel(const uint64_t* __r
   } tmp;
   const Prefix8 agg = BRp(tmp.p).Reduce(v, SatAdd());
   if (threadIdx.x == 0) blockagg[blockIdx.x] = agg;
+  unsigned long long* dst[3] = {totals->sumF, totals->nfE, totals->fE};
 #pragma unroll
-  for (int d = 0; d < SND; ++d) {
+  for (int k = 0; k < 3 * SND + 1; ++k) {
     __syncthreads();
-    const unsigned long long t = BR(tmp.u).Sum(sf[d]);
-    if (threadIdx.x == 0 && t) atomicAdd(&totals->sumF[d], t);
+    const unsigned long long t = BR(tmp.u).Sum(tv[k]);
+    if (threadIdx.x == 0 && t) atomicAdd(k < 3 * SND ? &dst[k / SND][k % SND] : &totals->suma, t);
   }
-  __syncthreads();
-  const unsigned long long t = BR(tmp.u).Sum(sa);
-  if (threadIdx.x == 0 && t) atomicAdd(&totals->suma, t);
 }
 
-// s1b: one CTA scans the block aggregates in place (exclusive) and stores the total.
-__global__ void __launch_bounds__(S_THREADS) s1_scan_kernel(Prefix8* blockagg, uint32_t nblocks, Prefix8* total) {
+// s1b: one CTA turns block aggregates into exclusive block prefixes, 256 blocks at a time,
+// and stops at the first block whose prefix already reaches every D's largest capacity
+// (NF_all is non-decreasing, so from there on no free block is ever cached: s2 treats
+// those blocks as saturated).
+__global__ void __launch_bounds__(S_THREADS) s1_scan_kernel(Prefix8* blockagg, uint32_t nblocks,
+                                                            const ChunkDev* __restrict__ chunk, ChunkTotals* totals) {
   typedef cub::BlockScan<Prefix8, S_THREADS> BS;
   __shared__ typename BS::TempStorage tmp;
   __shared__ Prefix8 carry;
-  if (threadIdx.x == 0) carry = Prefix8{};
+  __shared__ int stop;
+  const SatAdd add;
+  if (threadIdx.x == 0) {
+    carry = Prefix8{};
+    stop = 0;
+  }
   __syncthreads();
-  for (uint32_t base = 0; base < nblocks; base += S_THREADS) {
+  uint32_t base = 0;
+  for (; base < nblocks; base += S_THREADS) {
     const uint32_t i = base + threadIdx.x;
     Prefix8 v{};
     if (i < nblocks) v = blockagg[i];
     Prefix8 ex, agg;
-    BS(tmp).ExclusiveScan(v, ex, Prefix8{}, SatAdd(), agg);
+    BS(tmp).ExclusiveScan(v, ex, Prefix8{}, add, agg);
     const Prefix8 c = carry;
-    if (i < nblocks) blockagg[i] = SatAdd()(c, ex);
+    if (i < nblocks) blockagg[i] = add(c, ex);
     __syncthreads();
-    if (threadIdx.x == 0) carry = SatAdd()(c, agg);
+    if (threadIdx.x == 0) {
+      carry = add(c, agg);
+      bool sat = true;
+      for (int d = 0; d < SND; ++d) sat &= carry.nf[d] >= chunk->Cmax[d];
+      stop = sat;
+    }
     __syncthreads();
+    if (stop) {
+      base += S_THREADS;
+      break;
+    }
   }
-  if (threadIdx.x == 0) *total = carry;
+  if (threadIdx.x == 0) totals->nsat = min(base, nblocks);
 }
+
+// s2: one CTA = 256 consecutive request events.
+//   A. natural order: event record, L_before, universe deltas -> block scan + block prefix
+//      = NF_all(e), F_all(e) (saturated past nsat); window (p, e) split into chunks of
+//      WCH events, numbered by a block scan;
+//   B. the CTA's chunks are spread over all 256 threads (balanced): each chunk is scanned
+//      backwards and summed in packed 16x2 registers (exact: wch * max L_after < 2^16), then
+//      merged into per-event shared-memory totals A_nf, A_f;
+//   C. natural order again: b for every instance, instances grouped by D, coalesced stores.
 
 template <int ND>
 __global__ void __launch_bounds__(S_THREADS) s2_main_kernel(const uint64_t* __restrict__ sim,
-                                                            const uint32_t* __restrict__ next, uint32_t E,
+                                                            const uint64_t* __restrict__ scanrec, uint32_t E,
                                                             const ChunkDev* __restrict__ chunk,
                                                             const StackInstDev* __restrict__ insts,
                                                             const Prefix8* __restrict__ blockpre,
+                                                            const ChunkTotals* __restrict__ totals, uint32_t wch,
                                                             uint16_t* __restrict__ bout, unsigned long long* sumXf) {
-  __shared__ ChunkDev ch;
+  constexpr int NP = (ND + 1) / 2;  // D pairs
   typedef cub::BlockScan<Prefix8, S_THREADS> BS;
-  __shared__ typename BS::TempStorage tmp;
+  typedef cub::BlockScan<uint32_t, S_THREADS> BSu;
+  __shared__ ChunkDev ch;
+  __shared__ union {
+    typename BS::TempStorage scan;
+    typename BSu::TempStorage scanu;
+  } tmp;
+  __shared__ uint32_t anf_s[ND][S_THREADS], af_s[ND][S_THREADS];
+  __shared__ uint32_t p_s[S_THREADS], cbeg_s[S_THREADS + 1];
   if (threadIdx.x == 0) ch = *chunk;
+  const uint32_t t = threadIdx.x;
+#pragma unroll
+  for (int d = 0; d < ND; ++d) anf_s[d][t] = af_s[d][t] = 0;
   __syncthreads();
-  const uint32_t e = blockIdx.x * S_THREADS + threadIdx.x;
+  const uint32_t e0 = blockIdx.x * S_THREADS;
+  const uint32_t e = e0 + t;
   uint64_t s = 0;
   uint32_t Lb = 0;
   Prefix8 v{};
@@ -181,77 +230,100 @@ __global__ void __launch_bounds__(S_THREADS) s2_main_kernel(const uint64_t* __re
     Lb = L_before(sim, s);
     universe_delta(ch, Lb, sim_La(s), v);
   }
-  // NF_all(e), F_all(e): universe sums over every conversation's last turn before e
-  Prefix8 ex;
-  BS(tmp).ExclusiveScan(v, ex, Prefix8{}, SatAdd());
+  // ---- A
+  Prefix8 P;
+  if (blockIdx.x < totals->nsat) {
+    Prefix8 ex;
+    BS(tmp.scan).ExclusiveScan(v, ex, Prefix8{}, SatAdd());
+    P = SatAdd()(blockpre[blockIdx.x], ex);
+  } else {
+#pragma unroll
+    for (int d = 0; d < SND; ++d) P.nf[d] = P.f[d] = 0xFFFFFFFFu;
+  }
+  const uint32_t p = (e < E) ? sim_prev(s) : TLRU_NONE;
+  p_s[t] = p;
+  const uint32_t wl = (p == TLRU_NONE) ? 0u : e - p - 1;
+  uint32_t cb, ntot;
+  __syncthreads();
+  BSu(tmp.scanu).ExclusiveSum((wl + wch - 1) / wch, cb, ntot);
+  cbeg_s[t] = cb;
+  if (t == 0) cbeg_s[S_THREADS] = ntot;
+  __syncthreads();
+  // ---- B
+  uint32_t Dpk[NP];
+#pragma unroll
+  for (int q = 0; q < NP; ++q) Dpk[q] = ch.D[2 * q] | (ch.D[min(2 * q + 1, ND - 1)] << 16);
+  for (uint32_t it = t; it < ntot; it += S_THREADS) {
+    uint32_t lo = 0, hi = S_THREADS;  // owner event: last j with cbeg_s[j] <= it
+    while (hi - lo > 1) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (cbeg_s[mid] <= it) lo = mid; else hi = mid;
+    }
+    const uint32_t j = lo, ej = e0 + j, pj = p_s[j];
+    const uint32_t top = ej - 1 - (it - cbeg_s[j]) * wch;          // chunk covers [bot, top]
+    const uint32_t bot = max(pj + 1, top >= wch - 1 ? top - (wch - 1) : 0u);
+    uint32_t nf2[NP], f2[NP];
+#pragma unroll
+    for (int q = 0; q < NP; ++q) nf2[q] = f2[q] = 0;
+    for (uint32_t x = top + 1; x-- > bot;) {
+      const uint64_t r = __ldg(scanrec + x);
+      if (static_cast<uint32_t>(r) <= ej) continue;  // x's conversation returns before ej: not its last turn
+      const uint32_t L2 = static_cast<uint32_t>(r >> 32) * 0x10001u;  // L in both halves
+#pragma unroll
+      for (int q = 0; q < NP; ++q) {
+        // NF = max(L, D) - D, F = min(L, D), two D values per 32-bit lane word
+        nf2[q] = __vadd2(nf2[q], __vsub2(__vmaxu2(L2, Dpk[q]), Dpk[q]));
+        f2[q] = __vadd2(f2[q], __vminu2(L2, Dpk[q]));
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < NP; ++q) {
+      atomicAdd(&anf_s[2 * q][j], nf2[q] & 0xFFFFu);
+      atomicAdd(&af_s[2 * q][j], f2[q] & 0xFFFFu);
+      if (2 * q + 1 < ND) {
+        atomicAdd(&anf_s[2 * q + 1][j], nf2[q] >> 16);
+        atomicAdd(&af_s[2 * q + 1][j], f2[q] >> 16);
+      }
+    }
+  }
+  __syncthreads();
   if (e >= E) return;
-  const Prefix8 P = SatAdd()(blockpre[blockIdx.x], ex);
-  const uint32_t p = sim_prev(s), J = sim_J(s);
-  uint32_t anf[ND], af[ND], nfb[ND], fb[ND], nfall[ND];
+  // ---- C: per-instance b (P:154-156 with the closed form of X_theta)
+  const uint32_t J = sim_J(s);
+  const bool hit = p != TLRU_NONE;
 #pragma unroll
   for (int d = 0; d < ND; ++d) {
-    anf[d] = af[d] = nfb[d] = fb[d] = 0;
-    nfall[d] = P.nf[d];
-  }
-  if (p != TLRU_NONE) {
-#pragma unroll
-    for (int d = 0; d < ND; ++d) {
-      nfb[d] = nf_of(Lb, ch.D[d]);
-      fb[d] = f_of(Lb, ch.D[d]);
-    }
-    // backward window scan over x in (p, e): conversations used after theta's last turn
-    for (uint32_t x = e - 1; x > p; --x) {
-      if (__ldg(next + x) <= e) continue;  // x's conversation returns before e: not its last turn
-      const uint32_t L = sim_La(__ldg(sim + x));
-      bool done = true;
-#pragma unroll
-      for (int d = 0; d < ND; ++d) {
-        anf[d] += nf_of(L, ch.D[d]);
-        af[d] += f_of(L, ch.D[d]);
-        done &= anf[d] >= ch.Cmax[d];
+    const uint32_t nfb = hit ? nf_of(Lb, ch.D[d]) : 0u;
+    const uint32_t fb = hit ? f_of(Lb, ch.D[d]) : 0u;
+    const uint32_t anf = anf_s[d][t], af = af_s[d][t], nfall = P.nf[d];
+    const uint32_t k1 = ch.inst0 + ch.dbeg[d + 1];
+    for (uint32_t k = ch.inst0 + ch.dbeg[d]; k < k1; ++k) {
+      const StackInstDev in = insts[k];
+      uint32_t X = min(nfb, sat_sub(in.C, anf));
+      if (nfall < in.C && fb > 0) {  // warm-up: free blocks can still be cached
+        const uint32_t xf = min(fb, sat_sub(sat_sub(in.C, nfall), af));
+        X += xf;
+        if (xf) atomicAdd(&sumXf[in.inst], static_cast<unsigned long long>(xf));
       }
-      // every capacity already excludes theta's non-free blocks; then NF_all >= A_nf >= C too,
-      // so no free block of theta is cached either
-      if (done) break;
+      bout[in.boff + e] = static_cast<uint16_t>(J - X);
     }
-  }
-  for (uint32_t k = 0; k < ch.ninst; ++k) {
-    const StackInstDev in = insts[ch.inst0 + k];
-    uint32_t nfb_d = 0, fb_d = 0, anf_d = 0, af_d = 0, nfall_d = 0;
-#pragma unroll
-    for (int d = 0; d < ND; ++d)
-      if (static_cast<uint32_t>(d) == in.d) {
-        nfb_d = nfb[d];
-        fb_d = fb[d];
-        anf_d = anf[d];
-        af_d = af[d];
-        nfall_d = nfall[d];
-      }
-    uint32_t X = min(nfb_d, sat_sub(in.C, anf_d));
-    if (nfall_d < in.C && fb_d > 0) {  // warm-up: free blocks can still be cached
-      const uint32_t xf = min(fb_d, sat_sub(sat_sub(in.C, nfall_d), af_d));
-      X += xf;
-      if (xf) atomicAdd(&sumXf[in.inst], static_cast<unsigned long long>(xf));
-    }
-    bout[in.boff + e] = static_cast<uint16_t>(J - X);
   }
 }
 
 __global__ void s3_results_kernel(const StackInstDev* __restrict__ insts, uint32_t ninst,
                                   const uint32_t* __restrict__ inst_chunk, const ChunkTotals* __restrict__ totals,
-                                  const Prefix8* const* __restrict__ finals, const unsigned long long* sumXf,
-                                  tlru_result* results) {
+                                  const unsigned long long* sumXf, tlru_result* results) {
   for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < ninst; k += gridDim.x * blockDim.x) {
     const StackInstDev in = insts[k];
-    const uint32_t c = inst_chunk[k];
-    const Prefix8 fin = *finals[c];
-    const uint32_t nfE = fin.nf[in.d], fE = fin.f[in.d];
-    const uint64_t U = uint64_t(nfE) + fE;
-    const uint64_t used_final = U < in.C ? U : in.C;
-    const uint64_t fc_final = min(fE, sat_sub(in.C, nfE));
+    const ChunkTotals& T = totals[inst_chunk[k]];
+    const unsigned long long nfE = T.nfE[in.d], fE = T.fE[in.d], C = in.C;
+    const unsigned long long U = nfE + fE;
+    const unsigned long long used_final = U < C ? U : C;
+    const unsigned long long room = C > nfE ? C - nfE : 0ull;
+    const unsigned long long fc_final = fE < room ? fE : room;
     tlru_result& r = results[in.inst];
-    const unsigned long long total = totals[c].suma + r.sum_uncached - used_final;
-    const unsigned long long trim = totals[c].sumF[in.d] - sumXf[in.inst] - fc_final;
+    const unsigned long long total = T.suma + r.sum_uncached - used_final;  // telescoped evictions
+    const unsigned long long trim = T.sumF[in.d] - sumXf[in.inst] - fc_final;
     r.evicted_trim = trim;
     r.evicted_lru = total - trim;
     r.max_occupancy = static_cast<uint32_t>(used_final);
@@ -292,22 +364,22 @@ static void make_stack_plan(const tlru_trace* traces, uint32_t nt, const tlru_in
       ch.dev.nd = static_cast<uint32_t>(std::min<size_t>(SND, Ds.size() - c0));
       for (uint32_t d = 0; d < SND; ++d) ch.dev.D[d] = d < ch.dev.nd ? Ds[c0 + d] : Ds[c0];
       ch.dev.inst0 = static_cast<uint32_t>(P->insts.size());
-      for (uint32_t i : ids) {
-        uint32_t D = Dof(i);
-        for (uint32_t d = 0; d < ch.dev.nd; ++d)
-          if (ch.dev.D[d] == D) {
-            StackInstDev s;
-            s.C = std::min<uint32_t>(inst[i].capacity, 0x7FFF0000u);
-            s.d = d;
-            s.inst = i;
-            s.pad = 0;
-            s.boff = boffs[i];
-            ch.dev.Cmax[d] = std::max(ch.dev.Cmax[d], s.C);
-            P->insts.push_back(s);
-            P->inst_chunk.push_back(static_cast<uint32_t>(P->chunks.size()));
-          }
+      for (uint32_t d = 0; d < ch.dev.nd; ++d) {
+        ch.dev.dbeg[d] = static_cast<uint32_t>(P->insts.size()) - ch.dev.inst0;
+        for (uint32_t i : ids) {
+          if (Dof(i) != ch.dev.D[d]) continue;
+          StackInstDev s;
+          s.C = std::min<uint32_t>(inst[i].capacity, 0x7FFF0000u);
+          s.d = d;
+          s.inst = i;
+          s.pad = 0;
+          s.boff = boffs[i];
+          ch.dev.Cmax[d] = std::max(ch.dev.Cmax[d], s.C);
+          P->insts.push_back(s);
+          P->inst_chunk.push_back(static_cast<uint32_t>(P->chunks.size()));
+        }
       }
-      for (uint32_t d = ch.dev.nd; d < SND; ++d) ch.dev.Cmax[d] = 0;
+      for (uint32_t d = ch.dev.nd; d <= SND; ++d) ch.dev.dbeg[d] = static_cast<uint32_t>(P->insts.size()) - ch.dev.inst0;
       ch.dev.ninst = static_cast<uint32_t>(P->insts.size()) - ch.dev.inst0;
       P->chunks.push_back(ch);
     }
@@ -319,10 +391,9 @@ struct StackWs {
   StackInstDev* insts;
   uint32_t* inst_chunk;
   ChunkTotals* totals;
-  Prefix8** finals;
-  Prefix8* fin;
   unsigned long long* sumXf;
   Prefix8* blockpre;  // [chunk][block] exclusive block prefixes
+  uint64_t* scanrec;  // [event] next | L_after << 32 of the trace being processed
   uint64_t nblocks_max;
 };
 
@@ -332,11 +403,10 @@ static void carve_stack(Carver& cv, const StackPlan& P, uint32_t ni, StackWs* w)
   w->insts = cv.take<StackInstDev>(P.insts.size() + 1);
   w->inst_chunk = cv.take<uint32_t>(P.insts.size() + 1);
   w->totals = cv.take<ChunkTotals>(nc);
-  w->finals = cv.take<Prefix8*>(nc);
-  w->fin = cv.take<Prefix8>(nc);
   w->sumXf = cv.take<unsigned long long>(ni + 1);
   w->nblocks_max = (P.Emax + S_THREADS - 1) / S_THREADS + 1;
   w->blockpre = cv.take<Prefix8>(nc * w->nblocks_max);
+  w->scanrec = cv.take<uint64_t>(P.Emax + 1);
 }
 
 tlru_status stack_workspace(const tlru_trace* traces, uint32_t nt, const tlru_instance* inst, uint32_t ni,
@@ -352,11 +422,13 @@ tlru_status stack_workspace(const tlru_trace* traces, uint32_t nt, const tlru_in
 }
 
 template <int ND>
-static void launch_s2(const tlru_trace& tr, const ChunkDev* ch, const Prefix8* blockpre, const StackWs& w,
-                      uint16_t* bout, cudaStream_t st) {
+static void launch_s2(const tlru_trace& tr, const ChunkDev* ch, const Prefix8* blockpre, const ChunkTotals* tot,
+                      const StackWs& w, uint16_t* bout, cudaStream_t st) {
   const uint32_t E = static_cast<uint32_t>(tr.num_events);
-  s2_main_kernel<ND><<<(E + S_THREADS - 1) / S_THREADS, S_THREADS, 0, st>>>(tr.sim, tr.next, E, ch, w.insts, blockpre,
-                                                                            bout, w.sumXf);
+  // 16x2 partial sums stay exact while wch * max L_after < 2^16
+  const uint32_t wch = std::max<uint32_t>(1u, std::min<uint32_t>(64u, 65535u / std::max<uint32_t>(tr.max_history, 1u)));
+  s2_main_kernel<ND><<<(E + S_THREADS - 1) / S_THREADS, S_THREADS, 0, st>>>(tr.sim, w.scanrec, E, ch, w.insts,
+                                                                            blockpre, tot, wch, bout, w.sumXf);
 }
 
 tlru_status stack_simulate(const tlru_trace* traces, uint32_t nt, const tlru_instance* inst, uint32_t ni,
@@ -371,14 +443,9 @@ tlru_status stack_simulate(const tlru_trace* traces, uint32_t nt, const tlru_ins
   const size_t nc = P.chunks.size();
   TLRU_CUDA(cudaMemsetAsync(results, 0, size_t(ni) * sizeof(tlru_result), st));
   std::vector<ChunkDev> chd(nc);
-  std::vector<Prefix8*> finp(nc);
-  for (size_t c = 0; c < nc; ++c) {
-    chd[c] = P.chunks[c].dev;
-    finp[c] = w.fin + c;
-  }
+  for (size_t c = 0; c < nc; ++c) chd[c] = P.chunks[c].dev;
   if (nc) {
     TLRU_CUDA(cudaMemcpyAsync(w.chunks, chd.data(), nc * sizeof(ChunkDev), cudaMemcpyHostToDevice, st));
-    TLRU_CUDA(cudaMemcpyAsync(w.finals, finp.data(), nc * sizeof(Prefix8*), cudaMemcpyHostToDevice, st));
     TLRU_CUDA(cudaMemcpyAsync(w.insts, P.insts.data(), P.insts.size() * sizeof(StackInstDev),
                               cudaMemcpyHostToDevice, st));
     TLRU_CUDA(cudaMemcpyAsync(w.inst_chunk, P.inst_chunk.data(), P.inst_chunk.size() * sizeof(uint32_t),
@@ -391,19 +458,19 @@ tlru_status stack_simulate(const tlru_trace* traces, uint32_t nt, const tlru_ins
     const uint32_t E = static_cast<uint32_t>(tr.num_events);
     const uint32_t nb = (E + S_THREADS - 1) / S_THREADS;
     Prefix8* bp = w.blockpre + c * w.nblocks_max;
-    s1_block_kernel<<<nb, S_THREADS, 0, st>>>(tr.sim, E, w.chunks + c, bp, w.totals + c);
+    s1_block_kernel<<<nb, S_THREADS, 0, st>>>(tr.sim, tr.next, E, w.chunks + c, w.scanrec, bp, w.totals + c);
     TLRU_CHECK_LAUNCH();
-    s1_scan_kernel<<<1, S_THREADS, 0, st>>>(bp, nb, w.fin + c);
+    s1_scan_kernel<<<1, S_THREADS, 0, st>>>(bp, nb, w.chunks + c, w.totals + c);
     TLRU_CHECK_LAUNCH();
     switch (P.chunks[c].dev.nd) {
-      case 1: launch_s2<1>(tr, w.chunks + c, bp, w, bout, st); break;
-      case 2: launch_s2<2>(tr, w.chunks + c, bp, w, bout, st); break;
-      case 3: launch_s2<3>(tr, w.chunks + c, bp, w, bout, st); break;
-      case 4: launch_s2<4>(tr, w.chunks + c, bp, w, bout, st); break;
-      case 5: launch_s2<5>(tr, w.chunks + c, bp, w, bout, st); break;
-      case 6: launch_s2<6>(tr, w.chunks + c, bp, w, bout, st); break;
-      case 7: launch_s2<7>(tr, w.chunks + c, bp, w, bout, st); break;
-      default: launch_s2<8>(tr, w.chunks + c, bp, w, bout, st); break;
+      case 1: launch_s2<1>(tr, w.chunks + c, bp, w.totals + c, w, bout, st); break;
+      case 2: launch_s2<2>(tr, w.chunks + c, bp, w.totals + c, w, bout, st); break;
+      case 3: launch_s2<3>(tr, w.chunks + c, bp, w.totals + c, w, bout, st); break;
+      case 4: launch_s2<4>(tr, w.chunks + c, bp, w.totals + c, w, bout, st); break;
+      case 5: launch_s2<5>(tr, w.chunks + c, bp, w.totals + c, w, bout, st); break;
+      case 6: launch_s2<6>(tr, w.chunks + c, bp, w.totals + c, w, bout, st); break;
+      case 7: launch_s2<7>(tr, w.chunks + c, bp, w.totals + c, w, bout, st); break;
+      default: launch_s2<8>(tr, w.chunks + c, bp, w.totals + c, w, bout, st); break;
     }
     TLRU_CHECK_LAUNCH();
     *nkernels += 3;
@@ -414,8 +481,7 @@ tlru_status stack_simulate(const tlru_trace* traces, uint32_t nt, const tlru_ins
   TLRU_TRY(launch_finalize(segs_dev, ni, bins, hist, clamped, 1.0, nullptr, results, st));
   if (!P.insts.empty()) {
     s3_results_kernel<<<grid_for(P.insts.size(), 128), 128, 0, st>>>(w.insts, static_cast<uint32_t>(P.insts.size()),
-                                                                     w.inst_chunk, w.totals, w.finals, w.sumXf,
-                                                                     results);
+                                                                     w.inst_chunk, w.totals, w.sumXf, results);
     TLRU_CHECK_LAUNCH();
   }
   *nkernels += 3;

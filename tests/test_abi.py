@@ -85,3 +85,29 @@ def test_product_package_never_imports_the_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".h")):
                 src = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in src and "from oracle" not in src and "liboracle" not in src, f
+
+
+def _header_struct_fields(name):
+    src = re.sub(r"/\*.*?\*/", "", open(HEADER).read(), flags=re.S)
+    m = re.search(r"typedef struct\s*\{([^{}]*)\}\s*" + name + r"\s*;", src)
+    assert m, name
+    fields = []
+    for decl in m.group(1).split(";"):
+        decl = decl.strip()
+        if not decl:
+            continue
+        ty, names = decl.split(None, 1) if not decl.startswith("const") else decl.split(None, 2)[1:]
+        for n in names.split(","):
+            fields.append(n.strip().lstrip("*"))
+    return fields
+
+
+@pytest.mark.parametrize("cname,pyname", [("tlru_gen_params", "GenParams"), ("tlru_trace", "Trace"),
+                                          ("tlru_instance", "Instance"), ("tlru_sim_stats", "SimStats")])
+def test_ctypes_structs_mirror_the_header(abi, cname, pyname):
+    assert [f for f, _ in getattr(abi, pyname)._fields_] == _header_struct_fields(cname)
+
+
+@pytest.mark.parametrize("cname,dt", [("tlru_result", "RESULT_DTYPE"), ("tlru_tail", "TAIL_DTYPE")])
+def test_numpy_dtypes_mirror_the_header(abi, cname, dt):
+    assert list(getattr(abi, dt).names) == _header_struct_fields(cname)
