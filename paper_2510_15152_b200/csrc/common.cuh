@@ -81,4 +81,35 @@ __host__ __device__ __forceinline__ uint32_t sim_prev(uint64_t s) { return uint3
 __host__ __device__ __forceinline__ uint32_t sim_J(uint64_t s) { return uint32_t(s >> 32) & 0xFFFFu; }
 __host__ __device__ __forceinline__ uint32_t sim_La(uint64_t s) { return uint32_t(s >> 48); }
 
+// ----------------------------------------------------------------------------- warp-aggregated atomics
+// One atomic per warp instead of one per lane on the hot single-address counters.
+__device__ __forceinline__ void warp_atomic_max_u64(unsigned long long* dst, unsigned long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    unsigned long long w = __shfl_xor_sync(0xFFFFFFFFu, v, o);
+    v = w > v ? w : v;
+  }
+  if ((threadIdx.x & 31) == 0 && v) atomicMax(dst, v);
+}
+
+__device__ __forceinline__ void warp_atomic_max_u32(uint32_t* dst, uint32_t v) {
+  v = __reduce_max_sync(0xFFFFFFFFu, v);
+  if ((threadIdx.x & 31) == 0 && v) atomicMax(dst, v);
+}
+
+__device__ __forceinline__ void warp_atomic_add_u32(uint32_t* dst, uint32_t v) {
+  v = __reduce_add_sync(0xFFFFFFFFu, v);
+  if ((threadIdx.x & 31) == 0 && v) atomicAdd(dst, v);
+}
+
+// Warp-aggregated queue push: returns the slot for lanes with `want`, leader does one atomicAdd.
+__device__ __forceinline__ uint32_t warp_push(uint32_t* counter, bool want) {
+  const unsigned m = __ballot_sync(0xFFFFFFFFu, want);
+  uint32_t base = 0;
+  const int lane = threadIdx.x & 31;
+  if (lane == 0 && m) base = atomicAdd(counter, static_cast<uint32_t>(__popc(m)));
+  base = __shfl_sync(0xFFFFFFFFu, base, 0);
+  return base + __popc(m & ((1u << lane) - 1u));
+}
+
 }  // namespace tlru

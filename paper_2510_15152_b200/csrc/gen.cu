@@ -73,14 +73,23 @@ __device__ __forceinline__ uint32_t clock_turns(const GenDev& g, uint32_t c, uin
 // the lognormal sampling here.
 __global__ void gen_count_kernel(GenDev g, uint64_t* gaps, uint32_t* counts, unsigned long long* max_elapsed,
                                  uint32_t* queue, uint32_t* nqueue) {
-  for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < g.N; c += gridDim.x * blockDim.x) {
-    gaps[c] = exp_gap_ticks(g.seed, c, 0, FIELD_BIRTH, g.us_birth);  // Poisson(lambda_conv) births
-    uint64_t el;
-    const uint32_t n = clock_turns(g, c, &el);
-    counts[c] = n;
-    atomicMax(max_elapsed, static_cast<unsigned long long>(el));
-    if (n > g.safe_turns) queue[atomicAdd(nqueue, 1u)] = c;
+  const uint32_t stride = gridDim.x * blockDim.x;
+  const uint32_t Npad = (g.N + 31u) & ~31u;  // whole warps stay in the loop for the warp-aggregated atomics
+  unsigned long long mel = 0;
+  for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < Npad; c += stride) {
+    uint32_t n = 0;
+    if (c < g.N) {
+      gaps[c] = exp_gap_ticks(g.seed, c, 0, FIELD_BIRTH, g.us_birth);  // Poisson(lambda_conv) births
+      uint64_t el;
+      n = clock_turns(g, c, &el);
+      counts[c] = n;
+      mel = el > mel ? el : mel;
+    }
+    const bool q = c < g.N && n > g.safe_turns;
+    const uint32_t slot = warp_push(nqueue, q);
+    if (q) queue[slot] = c;
   }
+  warp_atomic_max_u64(max_elapsed, mel);
   if (blockIdx.x == 0 && threadIdx.x == 0) counts[g.N] = 0;
 }
 
@@ -125,6 +134,7 @@ __global__ void gen_draw_kernel(GenDev g, uint32_t E, const uint32_t* cid, const
 __global__ void gen_emit_kernel(GenDev g, const uint64_t* birth, const uint32_t* off, const uint64_t* gapt,
                                 const uint16_t* q16, const uint16_t* a16, uint64_t* key, uint32_t* val,
                                 uint16_t* J16, uint16_t* La16, uint8_t* last8, uint32_t* max_L, uint32_t* nconv) {
+  uint32_t maxL = 0, nc = 0;
   for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < g.N; c += gridDim.x * blockDim.x) {
     const uint32_t b = off[c], n = off[c + 1] - b;
     uint64_t t = birth[c];
@@ -140,11 +150,11 @@ __global__ void gen_emit_kernel(GenDev g, const uint64_t* birth, const uint32_t*
       La16[j] = static_cast<uint16_t>(L);
       last8[j] = (k + 1 == n) ? 1 : 0;
     }
-    if (n > 0) {
-      atomicMax(max_L, L);
-      atomicAdd(nconv, 1u);
-    }
+    maxL = L > maxL ? L : maxL;
+    nc += n > 0;
   }
+  warp_atomic_max_u32(max_L, maxL);
+  warp_atomic_add_u32(nconv, nc);
 }
 
 __global__ void gen_scatter_kernel(uint64_t E, const uint64_t* skey, const uint32_t* sval, const uint32_t* cid,
@@ -330,11 +340,13 @@ __global__ void up_link_kernel(uint64_t E, const uint32_t* skey, const uint32_t*
                                const uint16_t* a, uint64_t* sim, uint32_t* next, uint8_t* is_last,
                                uint64_t* time_ticks, unsigned long long* bad_range, uint32_t* max_L,
                                uint32_t* nconv) {
+  uint32_t maxL = 0, nc = 0;
+  unsigned long long bad = ~0ull;
   for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < E; i += uint64_t(gridDim.x) * blockDim.x) {
     uint32_t e = sval[i];
     uint32_t La = cum[i];
     uint32_t J = La - a[e];
-    if (La > 65535u) atomicMin(bad_range, static_cast<unsigned long long>(e));
+    if (La > 65535u && e < bad) bad = e;
     bool first = (i == 0) || skey[i - 1] != skey[i];
     bool last = (i + 1 == E) || skey[i + 1] != skey[i];
     uint32_t prev = first ? TLRU_NONE : sval[i - 1];
@@ -343,9 +355,12 @@ __global__ void up_link_kernel(uint64_t E, const uint32_t* skey, const uint32_t*
     next[e] = nx;
     if (is_last) is_last[e] = last ? 1 : 0;
     if (time_ticks) time_ticks[e] = e;
-    if (first) atomicAdd(nconv, 1u);
-    if (last) atomicMax(max_L, La > 65535u ? 65535u : La);
+    nc += first;
+    if (last) maxL = max(maxL, La > 65535u ? 65535u : La);
   }
+  warp_atomic_max_u32(max_L, maxL);
+  warp_atomic_add_u32(nconv, nc);
+  if (bad != ~0ull) atomicMin(bad_range, bad);
 }
 
 struct UpWs {

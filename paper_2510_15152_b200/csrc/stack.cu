@@ -103,47 +103,62 @@ __device__ __forceinline__ uint32_t L_before(const uint64_t* sim, uint64_t s) {
 }
 
 // s1: per-event scan record (next | L_after << 32) for the window scans, block aggregates of
-// the universe deltas (saturating), and the exact trace totals.
+// the universe deltas (saturating, one per 256 events), and the exact trace totals.  A
+// persistent grid walks the 256-event blocks so the totals are reduced once per CTA.
+constexpr int NTOT = 3 * SND + 1;
+
 __global__ void __launch_bounds__(S_THREADS) s1_block_kernel(const uint64_t* __restrict__ sim,
                                                              const uint32_t* __restrict__ next, uint32_t E,
                                                              const ChunkDev* __restrict__ chunk,
                                                              uint64_t* __restrict__ scanrec,
                                                              Prefix8* __restrict__ blockagg, ChunkTotals* totals) {
+  typedef cub::BlockReduce<Prefix8, S_THREADS> BRp;
+  __shared__ typename BRp::TempStorage tmp;
   __shared__ ChunkDev ch;
+  __shared__ unsigned long long part[S_THREADS / 32][NTOT];
   if (threadIdx.x == 0) ch = *chunk;
   __syncthreads();
-  const uint32_t e = blockIdx.x * S_THREADS + threadIdx.x;
-  Prefix8 v{};
-  unsigned long long tv[3 * SND + 1];
+  unsigned long long tv[NTOT];
 #pragma unroll
-  for (int k = 0; k < 3 * SND + 1; ++k) tv[k] = 0;
-  if (e < E) {
-    const uint64_t s = __ldg(sim + e);
-    const uint32_t La = sim_La(s);
-    scanrec[e] = uint64_t(__ldg(next + e)) | (uint64_t(La) << 32);
-    universe_delta(ch, L_before(sim, s), La, v);
+  for (int k = 0; k < NTOT; ++k) tv[k] = 0;
+  const uint32_t nblocks = (E + S_THREADS - 1) / S_THREADS;
+  for (uint32_t blk = blockIdx.x; blk < nblocks; blk += gridDim.x) {
+    const uint32_t e = blk * S_THREADS + threadIdx.x;
+    Prefix8 v{};
+    if (e < E) {
+      const uint64_t s = __ldg(sim + e);
+      const uint32_t La = sim_La(s);
+      scanrec[e] = uint64_t(__ldg(next + e)) | (uint64_t(La) << 32);
+      universe_delta(ch, L_before(sim, s), La, v);
 #pragma unroll
-    for (int d = 0; d < SND; ++d) {
-      tv[d] = f_of(La, ch.D[d]);
-      tv[SND + d] = v.nf[d];
-      tv[2 * SND + d] = v.f[d];
+      for (int d = 0; d < SND; ++d) {
+        tv[d] += f_of(La, ch.D[d]);
+        tv[SND + d] += v.nf[d];
+        tv[2 * SND + d] += v.f[d];
+      }
+      tv[3 * SND] += La - sim_J(s);
     }
-    tv[3 * SND] = La - sim_J(s);
-  }
-  typedef cub::BlockReduce<Prefix8, S_THREADS> BRp;
-  typedef cub::BlockReduce<unsigned long long, S_THREADS> BR;
-  __shared__ union {
-    typename BRp::TempStorage p;
-    typename BR::TempStorage u;
-  } tmp;
-  const Prefix8 agg = BRp(tmp.p).Reduce(v, SatAdd());
-  if (threadIdx.x == 0) blockagg[blockIdx.x] = agg;
-  unsigned long long* dst[3] = {totals->sumF, totals->nfE, totals->fE};
-#pragma unroll
-  for (int k = 0; k < 3 * SND + 1; ++k) {
+    const Prefix8 agg = BRp(tmp).Reduce(v, SatAdd());
+    if (threadIdx.x == 0) blockagg[blk] = agg;
     __syncthreads();
-    const unsigned long long t = BR(tmp.u).Sum(tv[k]);
-    if (threadIdx.x == 0 && t) atomicAdd(k < 3 * SND ? &dst[k / SND][k % SND] : &totals->suma, t);
+  }
+  // totals: warp shuffles, then one atomic per value per CTA
+#pragma unroll
+  for (int k = 0; k < NTOT; ++k) {
+    unsigned long long x = tv[k];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xFFFFFFFFu, x, o);
+    if ((threadIdx.x & 31) == 0) part[threadIdx.x / 32][k] = x;
+  }
+  __syncthreads();
+  if (threadIdx.x < NTOT) {
+    unsigned long long x = 0;
+#pragma unroll
+    for (int w = 0; w < S_THREADS / 32; ++w) x += part[w][threadIdx.x];
+    const int k = threadIdx.x;
+    unsigned long long* dst = k < SND ? &totals->sumF[k] : k < 2 * SND ? &totals->nfE[k - SND]
+                              : k < 3 * SND ? &totals->fE[k - 2 * SND] : &totals->suma;
+    if (x) atomicAdd(dst, x);
   }
 }
 
@@ -215,6 +230,8 @@ __global__ void __launch_bounds__(S_THREADS) s2_main_kernel(const uint64_t* __re
   } tmp;
   __shared__ uint32_t anf_s[ND][S_THREADS], af_s[ND][S_THREADS];
   __shared__ uint32_t p_s[S_THREADS], cbeg_s[S_THREADS + 1];
+  __shared__ uint32_t J_s[S_THREADS], Lb_s[S_THREADS];
+  __shared__ uint32_t nfall_s[ND][S_THREADS];
   if (threadIdx.x == 0) ch = *chunk;
   const uint32_t t = threadIdx.x;
 #pragma unroll
@@ -242,6 +259,10 @@ __global__ void __launch_bounds__(S_THREADS) s2_main_kernel(const uint64_t* __re
   }
   const uint32_t p = (e < E) ? sim_prev(s) : TLRU_NONE;
   p_s[t] = p;
+  J_s[t] = sim_J(s);
+  Lb_s[t] = (p == TLRU_NONE) ? 0u : Lb;
+#pragma unroll
+  for (int d = 0; d < ND; ++d) nfall_s[d][t] = P.nf[d];
   const uint32_t wl = (p == TLRU_NONE) ? 0u : e - p - 1;
   uint32_t cb, ntot;
   __syncthreads();
@@ -287,25 +308,51 @@ __global__ void __launch_bounds__(S_THREADS) s2_main_kernel(const uint64_t* __re
     }
   }
   __syncthreads();
-  if (e >= E) return;
-  // ---- C: per-instance b (P:154-156 with the closed form of X_theta)
-  const uint32_t J = sim_J(s);
-  const bool hit = p != TLRU_NONE;
+  // ---- C: per-instance b (P:154-156 with the closed form of X_theta).  Thread t writes 4
+  // consecutive events (one 8-byte store when the instance row is 8-byte aligned) for every
+  // fourth instance of each D.
+  const uint32_t quad = t & 63, lane4 = t >> 6;
+  const uint32_t j0 = quad * 4;
+  const bool full = e0 + j0 + 3 < E;
+  const bool saturated = blockIdx.x >= totals->nsat;  // NF_all >= every C here: no free blocks cached
+  uint32_t Jv[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) Jv[u] = J_s[j0 + u];
 #pragma unroll
   for (int d = 0; d < ND; ++d) {
-    const uint32_t nfb = hit ? nf_of(Lb, ch.D[d]) : 0u;
-    const uint32_t fb = hit ? f_of(Lb, ch.D[d]) : 0u;
-    const uint32_t anf = anf_s[d][t], af = af_s[d][t], nfall = P.nf[d];
+    uint32_t nfb[4], fb[4], anf[4], af[4], nfa[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const bool hit = p_s[j0 + u] != TLRU_NONE;
+      const uint32_t Lbu = Lb_s[j0 + u];
+      nfb[u] = hit ? nf_of(Lbu, ch.D[d]) : 0u;
+      fb[u] = hit ? f_of(Lbu, ch.D[d]) : 0u;
+      anf[u] = anf_s[d][j0 + u];
+      af[u] = af_s[d][j0 + u];
+      nfa[u] = nfall_s[d][j0 + u];
+    }
     const uint32_t k1 = ch.inst0 + ch.dbeg[d + 1];
-    for (uint32_t k = ch.inst0 + ch.dbeg[d]; k < k1; ++k) {
+    for (uint32_t k = ch.inst0 + ch.dbeg[d] + lane4; k < k1; k += 4) {
       const StackInstDev in = insts[k];
-      uint32_t X = min(nfb, sat_sub(in.C, anf));
-      if (nfall < in.C && fb > 0) {  // warm-up: free blocks can still be cached
-        const uint32_t xf = min(fb, sat_sub(sat_sub(in.C, nfall), af));
-        X += xf;
-        if (xf) atomicAdd(&sumXf[in.inst], static_cast<unsigned long long>(xf));
+      uint32_t b[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        uint32_t X = min(nfb[u], sat_sub(in.C, anf[u]));
+        if (!saturated && nfa[u] < in.C && fb[u] > 0) {  // warm-up: free blocks can still be cached
+          const uint32_t xf = min(fb[u], sat_sub(sat_sub(in.C, nfa[u]), af[u]));
+          X += xf;
+          if (xf && e0 + j0 + u < E) atomicAdd(&sumXf[in.inst], static_cast<unsigned long long>(xf));
+        }
+        b[u] = Jv[u] - X;
       }
-      bout[in.boff + e] = static_cast<uint16_t>(J - X);
+      uint16_t* row = bout + in.boff + e0 + j0;
+      if (full && ((reinterpret_cast<uintptr_t>(row) & 7u) == 0)) {
+        *reinterpret_cast<uint2*>(row) = make_uint2(b[0] | (b[1] << 16), b[2] | (b[3] << 16));
+      } else {
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (e0 + j0 + u < E) row[u] = static_cast<uint16_t>(b[u]);
+      }
     }
   }
 }
@@ -458,7 +505,8 @@ tlru_status stack_simulate(const tlru_trace* traces, uint32_t nt, const tlru_ins
     const uint32_t E = static_cast<uint32_t>(tr.num_events);
     const uint32_t nb = (E + S_THREADS - 1) / S_THREADS;
     Prefix8* bp = w.blockpre + c * w.nblocks_max;
-    s1_block_kernel<<<nb, S_THREADS, 0, st>>>(tr.sim, tr.next, E, w.chunks + c, w.scanrec, bp, w.totals + c);
+    s1_block_kernel<<<std::min<uint32_t>(nb ? nb : 1, 148u * 4u), S_THREADS, 0, st>>>(tr.sim, tr.next, E, w.chunks + c,
+                                                                                     w.scanrec, bp, w.totals + c);
     TLRU_CHECK_LAUNCH();
     s1_scan_kernel<<<1, S_THREADS, 0, st>>>(bp, nb, w.chunks + c, w.totals + c);
     TLRU_CHECK_LAUNCH();
