@@ -130,31 +130,43 @@ __global__ void gen_draw_kernel(GenDev g, uint32_t E, const uint32_t* cid, const
 }
 
 // One thread per conversation, no random draws: arrival ticks and history prefix sums over its
-// (already exact) slots; J = L_before + q, L_after = J + a.
+// slots; J = L_before + q, L_after = J + a.  Slots are allocated from the turn
+// clocks alone, so a turn that would push the history past L_max ends the conversation here
+// (context-window end): it and the later slots get the sentinel key and sort past the end.
 __global__ void gen_emit_kernel(GenDev g, const uint64_t* birth, const uint32_t* off, const uint64_t* gapt,
-                                const uint16_t* q16, const uint16_t* a16, uint64_t* key, uint32_t* val,
-                                uint16_t* J16, uint16_t* La16, uint8_t* last8, uint32_t* max_L, uint32_t* nconv) {
-  uint32_t maxL = 0, nc = 0;
+                                const uint16_t* q16, const uint16_t* a16, uint64_t sentinel, uint64_t* key,
+                                uint32_t* val, uint16_t* J16, uint16_t* La16, uint8_t* last8, uint32_t* max_L,
+                                uint32_t* nconv, uint32_t* nvalid) {
+  uint32_t maxL = 0, nc = 0, nv = 0;
   for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < g.N; c += gridDim.x * blockDim.x) {
     const uint32_t b = off[c], n = off[c + 1] - b;
     uint64_t t = birth[c];
-    uint32_t L = 0;
-    for (uint32_t k = 0; k < n; ++k) {
+    uint32_t L = 0, k = 0;
+    for (; k < n; ++k) {
       const uint32_t j = b + k;
+      const uint32_t q = q16[j], a = a16[j];
+      if (L + q + a > g.Lmax) break;  // context-window end
       t += gapt[j];
       key[j] = t;
       val[j] = j;
-      L += q16[j];
+      L += q;
       J16[j] = static_cast<uint16_t>(L);
-      L += a16[j];
+      L += a;
       La16[j] = static_cast<uint16_t>(L);
-      last8[j] = (k + 1 == n) ? 1 : 0;
+      last8[j] = 0;
+    }
+    if (k > 0) last8[b + k - 1] = 1;
+    for (uint32_t r = k; r < n; ++r) {
+      key[b + r] = sentinel;
+      val[b + r] = b + r;
     }
     maxL = L > maxL ? L : maxL;
-    nc += n > 0;
+    nc += k > 0;
+    nv += k;
   }
   warp_atomic_max_u32(max_L, maxL);
   warp_atomic_add_u32(nconv, nc);
+  warp_atomic_add_u32(nvalid, nv);
 }
 
 __global__ void gen_scatter_kernel(uint64_t E, const uint64_t* skey, const uint32_t* sval, const uint32_t* cid,
@@ -239,6 +251,7 @@ struct GenWs {
   uint32_t* nconv;
   uint32_t* queue;   // [N] conversations needing an exact length replay in the count pass
   uint32_t* nqueue;
+  uint32_t* nvalid;
   uint16_t* turn;    // [E] turn index of each event slot
   uint64_t* gapt;    // [E] gap ticks to the previous turn
   uint64_t* key[2];
@@ -261,6 +274,7 @@ static tlru_status carve_gen(Carver& cv, uint32_t N, uint64_t cap, GenWs* w) {
   w->nconv = cv.take<uint32_t>(1);
   w->queue = cv.take<uint32_t>(N);
   w->nqueue = cv.take<uint32_t>(1);
+  w->nvalid = cv.take<uint32_t>(1);
   w->turn = cv.take<uint16_t>(cap);
   w->gapt = cv.take<uint64_t>(cap);
   for (int i = 0; i < 2; ++i) {
@@ -289,15 +303,19 @@ static tlru_status carve_gen(Carver& cv, uint32_t N, uint64_t cap, GenWs* w) {
 }
 
 // Runs count + scans; fills E (host) and the max tick bound.  Synchronizes.
+// exact = false: slots from the turn clocks only (an upper bound; context-capped turns are
+// dropped later by gen_emit_kernel).  exact = true: the exact event count.
 static tlru_status run_count(const tlru_gen_params* p, const GenWs& w, cudaStream_t st, uint64_t* E,
-                             uint64_t* max_tick) {
+                             uint64_t* max_tick, bool exact) {
   GenDev g = make_dev(p);
   TLRU_CUDA(cudaMemsetAsync(w.max_elapsed, 0, sizeof(unsigned long long), st));
   TLRU_CUDA(cudaMemsetAsync(w.nqueue, 0, sizeof(uint32_t), st));
   gen_count_kernel<<<grid_for(g.N, 128), 128, 0, st>>>(g, w.gaps, w.counts, w.max_elapsed, w.queue, w.nqueue);
   TLRU_CHECK_LAUNCH();
-  gen_count_fix_kernel<<<grid_for(g.N / 8 + 1, 128), 128, 0, st>>>(g, w.queue, w.nqueue, w.counts);
-  TLRU_CHECK_LAUNCH();
+  if (exact) {
+    gen_count_fix_kernel<<<grid_for(g.N / 8 + 1, 128), 128, 0, st>>>(g, w.queue, w.nqueue, w.counts);
+    TLRU_CHECK_LAUNCH();
+  }
   size_t b = w.cub_bytes;
   TLRU_CUDA(cub::DeviceScan::InclusiveSum(w.cub_tmp, b, w.gaps, w.birth, static_cast<int>(g.N), st));
   b = w.cub_bytes;
@@ -429,7 +447,7 @@ extern "C" tlru_status tlru_count_events(const tlru_gen_params* p, uint64_t* out
   TLRU_TRY(carve_gen(cv, p->num_conversations, 0, &w));
   TLRU_TRY(check_ws(cv, ws, ws_bytes));
   uint64_t mt;
-  return run_count(p, w, stream, out, &mt);
+  return run_count(p, w, stream, out, &mt, true);
 }
 
 extern "C" tlru_status tlru_generate_traces(const tlru_gen_params* params, uint32_t n, tlru_trace* traces, void* ws,
@@ -446,14 +464,19 @@ extern "C" tlru_status tlru_generate_traces(const tlru_gen_params* params, uint3
     GenWs w;
     TLRU_TRY(carve_gen(cv, p->num_conversations, tr->capacity, &w));
     TLRU_TRY(check_ws(cv, ws, ws_bytes));
-    uint64_t E, max_tick;
-    TLRU_TRY(run_count(p, w, st, &E, &max_tick));
+    uint64_t E, max_tick;  // E = event slots
+    TLRU_TRY(run_count(p, w, st, &E, &max_tick, false));
+    if (E > tr->capacity) TLRU_TRY(run_count(p, w, st, &E, &max_tick, true));  // no room for spare slots
     if (E > tr->capacity)
       TLRU_FAIL(TLRU_ERANGE, "trace %u: %llu events exceed capacity %llu", t, (unsigned long long)E,
                 (unsigned long long)tr->capacity);
     GenDev g = make_dev(p);
+    int end_bit = 1;  // the sentinel key (all ones below end_bit) sorts after every arrival tick
+    while (end_bit < 64 && ((max_tick + 1) >> end_bit) != 0) ++end_bit;
+    const uint64_t sentinel = end_bit >= 64 ? ~0ull : ((1ull << end_bit) - 1);
     TLRU_CUDA(cudaMemsetAsync(w.max_L, 0, sizeof(uint32_t), st));
     TLRU_CUDA(cudaMemsetAsync(w.nconv, 0, sizeof(uint32_t), st));
+    TLRU_CUDA(cudaMemsetAsync(w.nvalid, 0, sizeof(uint32_t), st));
     gen_slot_kernel<<<grid_for(g.N, 128), 128, 0, st>>>(g, w.off, w.cid, w.turn);
     TLRU_CHECK_LAUNCH();
     if (E > 0) {
@@ -461,19 +484,22 @@ extern "C" tlru_status tlru_generate_traces(const tlru_gen_params* params, uint3
                                                          w.a16);
       TLRU_CHECK_LAUNCH();
     }
-    gen_emit_kernel<<<grid_for(g.N, 128), 128, 0, st>>>(g, w.birth, w.off, w.gapt, w.q16, w.a16, w.key[0], w.val[0],
-                                                         w.J16, w.La16, w.last8, w.max_L, w.nconv);
+    gen_emit_kernel<<<grid_for(g.N, 128), 128, 0, st>>>(g, w.birth, w.off, w.gapt, w.q16, w.a16, sentinel, w.key[0],
+                                                         w.val[0], w.J16, w.La16, w.last8, w.max_L, w.nconv,
+                                                         w.nvalid);
     TLRU_CHECK_LAUNCH();
-    uint32_t stats[2];
+    uint32_t stats[3];
     TLRU_CUDA(cudaMemcpyAsync(&stats[0], w.max_L, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
     TLRU_CUDA(cudaMemcpyAsync(&stats[1], w.nconv, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
-    int end_bit = 1;
-    while (end_bit < 64 && (max_tick >> end_bit) != 0) ++end_bit;
+    TLRU_CUDA(cudaMemcpyAsync(&stats[2], w.nvalid, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    TLRU_CUDA(cudaStreamSynchronize(st));
+    const uint64_t slots = E;
+    E = stats[2];  // events that survive the context cap
     if (E > 0) {
       cub::DoubleBuffer<uint64_t> kb(w.key[0], w.key[1]);
       cub::DoubleBuffer<uint32_t> vb(w.val[0], w.val[1]);
       size_t b = w.cub_bytes;
-      TLRU_CUDA(cub::DeviceRadixSort::SortPairs(w.cub_tmp, b, kb, vb, static_cast<int>(E), 0, end_bit, st));
+      TLRU_CUDA(cub::DeviceRadixSort::SortPairs(w.cub_tmp, b, kb, vb, static_cast<int>(slots), 0, end_bit, st));
       gen_scatter_kernel<<<grid_for(E, 256), 256, 0, st>>>(E, kb.Current(), vb.Current(), w.cid, w.q16, w.a16,
                                                            w.last8, w.pos, tr->time_ticks, tr->conv, tr->prompt,
                                                            tr->response, tr->is_last);

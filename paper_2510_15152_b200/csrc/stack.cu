@@ -208,8 +208,9 @@ __global__ void __launch_bounds__(S_THREADS) s1_scan_kernel(Prefix8* blockagg, u
 //      = NF_all(e), F_all(e) (saturated past nsat); window (p, e) split into chunks of
 //      WCH events, numbered by a block scan;
 //   B. the CTA's chunks are spread over all 256 threads (balanced): each chunk is scanned
-//      backwards and summed in packed 16x2 registers (exact: wch * max L_after < 2^16), then
-//      merged into per-event shared-memory totals A_nf, A_f;
+//      backwards, branch-free, summing L and max(L, D) for D pairs in packed 16x2 registers
+//      (exact: wch * max(L_after, D) < 2^16), then merged into per-event shared-memory
+//      totals A_nf, A_f;
 //   C. natural order again: b for every instance, instances grouped by D, coalesced stores.
 
 template <int ND>
@@ -219,7 +220,8 @@ __global__ void __launch_bounds__(S_THREADS) s2_main_kernel(const uint64_t* __re
                                                             const StackInstDev* __restrict__ insts,
                                                             const Prefix8* __restrict__ blockpre,
                                                             const ChunkTotals* __restrict__ totals, uint32_t wch,
-                                                            uint16_t* __restrict__ bout, unsigned long long* sumXf) {
+                                                            uint32_t maxL, uint16_t* __restrict__ bout,
+                                                            unsigned long long* sumXf) {
   constexpr int NP = (ND + 1) / 2;  // D pairs
   typedef cub::BlockScan<Prefix8, S_THREADS> BS;
   typedef cub::BlockScan<uint32_t, S_THREADS> BSu;
@@ -271,9 +273,13 @@ __global__ void __launch_bounds__(S_THREADS) s2_main_kernel(const uint64_t* __re
   if (t == 0) cbeg_s[S_THREADS] = ntot;
   __syncthreads();
   // ---- B
-  uint32_t Dpk[NP];
+  // window sums only see L <= maxL, so D can be clamped to maxL (<= 65535): max(L - D, 0) and
+  // min(L, D) are unchanged for every L in the trace
+  uint32_t Deff[ND], Dpk[NP];
 #pragma unroll
-  for (int q = 0; q < NP; ++q) Dpk[q] = ch.D[2 * q] | (ch.D[min(2 * q + 1, ND - 1)] << 16);
+  for (int d = 0; d < ND; ++d) Deff[d] = min(ch.D[d], maxL);
+#pragma unroll
+  for (int q = 0; q < NP; ++q) Dpk[q] = Deff[2 * q] | (Deff[min(2 * q + 1, ND - 1)] << 16);
   for (uint32_t it = t; it < ntot; it += S_THREADS) {
     uint32_t lo = 0, hi = S_THREADS;  // owner event: last j with cbeg_s[j] <= it
     while (hi - lo > 1) {
@@ -283,27 +289,32 @@ __global__ void __launch_bounds__(S_THREADS) s2_main_kernel(const uint64_t* __re
     const uint32_t j = lo, ej = e0 + j, pj = p_s[j];
     const uint32_t top = ej - 1 - (it - cbeg_s[j]) * wch;          // chunk covers [bot, top]
     const uint32_t bot = max(pj + 1, top >= wch - 1 ? top - (wch - 1) : 0u);
-    uint32_t nf2[NP], f2[NP];
+    // Branch-free: a dead element (its conversation returns before ej) counts as L = 0.
+    // Per D pair accumulate sum max(L, D) (16x2); with n = elements in the chunk:
+    //   A_nf = sum max(L, D) - n D,   A_f = sum L + n D - sum max(L, D)   (max + min = L + D)
+    uint32_t mx2[NP], sumL = 0;
 #pragma unroll
-    for (int q = 0; q < NP; ++q) nf2[q] = f2[q] = 0;
+    for (int q = 0; q < NP; ++q) mx2[q] = 0;
     for (uint32_t x = top + 1; x-- > bot;) {
       const uint64_t r = __ldg(scanrec + x);
-      if (static_cast<uint32_t>(r) <= ej) continue;  // x's conversation returns before ej: not its last turn
-      const uint32_t L2 = static_cast<uint32_t>(r >> 32) * 0x10001u;  // L in both halves
+      const uint32_t L = static_cast<uint32_t>(r) > ej ? static_cast<uint32_t>(r >> 32) : 0u;
+      sumL += L;
+      const uint32_t L2 = L * 0x10001u;  // L in both 16-bit halves
 #pragma unroll
-      for (int q = 0; q < NP; ++q) {
-        // NF = max(L, D) - D, F = min(L, D), two D values per 32-bit lane word
-        nf2[q] = __vadd2(nf2[q], __vsub2(__vmaxu2(L2, Dpk[q]), Dpk[q]));
-        f2[q] = __vadd2(f2[q], __vminu2(L2, Dpk[q]));
-      }
+      for (int q = 0; q < NP; ++q) mx2[q] = __vadd2(mx2[q], __vmaxu2(L2, Dpk[q]));
     }
+    const uint32_t n = top + 1 - bot;
 #pragma unroll
     for (int q = 0; q < NP; ++q) {
-      atomicAdd(&anf_s[2 * q][j], nf2[q] & 0xFFFFu);
-      atomicAdd(&af_s[2 * q][j], f2[q] & 0xFFFFu);
-      if (2 * q + 1 < ND) {
-        atomicAdd(&anf_s[2 * q + 1][j], nf2[q] >> 16);
-        atomicAdd(&af_s[2 * q + 1][j], f2[q] >> 16);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int d = 2 * q + h;
+        if (d < ND) {
+          const uint32_t smax = h ? (mx2[q] >> 16) : (mx2[q] & 0xFFFFu);
+          const uint32_t nD = n * Deff[d];
+          atomicAdd(&anf_s[d][j], smax - nD);
+          atomicAdd(&af_s[d][j], sumL + nD - smax);
+        }
       }
     }
   }
@@ -469,13 +480,15 @@ tlru_status stack_workspace(const tlru_trace* traces, uint32_t nt, const tlru_in
 }
 
 template <int ND>
-static void launch_s2(const tlru_trace& tr, const ChunkDev* ch, const Prefix8* blockpre, const ChunkTotals* tot,
-                      const StackWs& w, uint16_t* bout, cudaStream_t st) {
+static void launch_s2(const tlru_trace& tr, const ChunkDev* ch, const ChunkDev& ch_host, const Prefix8* blockpre,
+                      const ChunkTotals* tot, const StackWs& w, uint16_t* bout, cudaStream_t st) {
   const uint32_t E = static_cast<uint32_t>(tr.num_events);
-  // 16x2 partial sums stay exact while wch * max L_after < 2^16
-  const uint32_t wch = std::max<uint32_t>(1u, std::min<uint32_t>(64u, 65535u / std::max<uint32_t>(tr.max_history, 1u)));
+  // 16x2 partial sums of max(L, min(D, maxL)) stay exact while wch * maxL < 2^16
+  const uint32_t maxL = std::max<uint32_t>(tr.max_history, 1u);
+  const uint32_t wch = std::max<uint32_t>(1u, std::min<uint32_t>(64u, 65535u / maxL));
+  (void)ch_host;
   s2_main_kernel<ND><<<(E + S_THREADS - 1) / S_THREADS, S_THREADS, 0, st>>>(tr.sim, w.scanrec, E, ch, w.insts,
-                                                                            blockpre, tot, wch, bout, w.sumXf);
+                                                                            blockpre, tot, wch, maxL, bout, w.sumXf);
 }
 
 tlru_status stack_simulate(const tlru_trace* traces, uint32_t nt, const tlru_instance* inst, uint32_t ni,
@@ -511,14 +524,14 @@ tlru_status stack_simulate(const tlru_trace* traces, uint32_t nt, const tlru_ins
     s1_scan_kernel<<<1, S_THREADS, 0, st>>>(bp, nb, w.chunks + c, w.totals + c);
     TLRU_CHECK_LAUNCH();
     switch (P.chunks[c].dev.nd) {
-      case 1: launch_s2<1>(tr, w.chunks + c, bp, w.totals + c, w, bout, st); break;
-      case 2: launch_s2<2>(tr, w.chunks + c, bp, w.totals + c, w, bout, st); break;
-      case 3: launch_s2<3>(tr, w.chunks + c, bp, w.totals + c, w, bout, st); break;
-      case 4: launch_s2<4>(tr, w.chunks + c, bp, w.totals + c, w, bout, st); break;
-      case 5: launch_s2<5>(tr, w.chunks + c, bp, w.totals + c, w, bout, st); break;
-      case 6: launch_s2<6>(tr, w.chunks + c, bp, w.totals + c, w, bout, st); break;
-      case 7: launch_s2<7>(tr, w.chunks + c, bp, w.totals + c, w, bout, st); break;
-      default: launch_s2<8>(tr, w.chunks + c, bp, w.totals + c, w, bout, st); break;
+      case 1: launch_s2<1>(tr, w.chunks + c, P.chunks[c].dev, bp, w.totals + c, w, bout, st); break;
+      case 2: launch_s2<2>(tr, w.chunks + c, P.chunks[c].dev, bp, w.totals + c, w, bout, st); break;
+      case 3: launch_s2<3>(tr, w.chunks + c, P.chunks[c].dev, bp, w.totals + c, w, bout, st); break;
+      case 4: launch_s2<4>(tr, w.chunks + c, P.chunks[c].dev, bp, w.totals + c, w, bout, st); break;
+      case 5: launch_s2<5>(tr, w.chunks + c, P.chunks[c].dev, bp, w.totals + c, w, bout, st); break;
+      case 6: launch_s2<6>(tr, w.chunks + c, P.chunks[c].dev, bp, w.totals + c, w, bout, st); break;
+      case 7: launch_s2<7>(tr, w.chunks + c, P.chunks[c].dev, bp, w.totals + c, w, bout, st); break;
+      default: launch_s2<8>(tr, w.chunks + c, P.chunks[c].dev, bp, w.totals + c, w, bout, st); break;
     }
     TLRU_CHECK_LAUNCH();
     *nkernels += 3;

@@ -92,17 +92,24 @@ def _alloc_trace(E: int, device, exports: bool) -> DeviceTrace:
     return tr
 
 
-def generate_traces(params: list[dict], device="cuda", exports: bool = True, stream=None) -> list[DeviceTrace]:
-    """tlru_generate_traces for each params dict (fields of tlru_gen_params)."""
+def generate_traces(params: list[dict], device="cuda", exports: bool = True, stream=None,
+                    capacity: str = "exact") -> list[DeviceTrace]:
+    """tlru_generate_traces for each params dict (fields of tlru_gen_params).
+
+    capacity: "exact" sizes the trace with tlru_count_events; "bound" with
+    tlru_trace_max_events (N * max_turns)."""
     out = []
     st = _stream(stream)
     for p in params:
         g = _gen_struct(p)
         sz = ctypes.c_size_t()
-        check(lib.tlru_gen_workspace_size(ctypes.byref(g), 0, ctypes.byref(sz)))
-        ws = _workspace(sz.value, device)
         E = ctypes.c_uint64()
-        check(lib.tlru_count_events(ctypes.byref(g), ctypes.byref(E), _ptr(ws), sz.value, st))
+        if capacity == "bound":
+            check(lib.tlru_trace_max_events(ctypes.byref(g), ctypes.byref(E)))
+        else:
+            check(lib.tlru_gen_workspace_size(ctypes.byref(g), 0, ctypes.byref(sz)))
+            ws = _workspace(sz.value, device)
+            check(lib.tlru_count_events(ctypes.byref(g), ctypes.byref(E), _ptr(ws), sz.value, st))
         tr = _alloc_trace(E.value, device, exports)
         check(lib.tlru_gen_workspace_size(ctypes.byref(g), tr.sim.numel(), ctypes.byref(sz)))
         ws = _workspace(sz.value, device)

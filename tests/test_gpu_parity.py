@@ -126,6 +126,22 @@ def test_segment_warm_start_is_exact(T, seg):
         T.set_sim_options(0, 0)
 
 
+@ENGINES
+def test_extreme_parameters(T, engine):
+    """Capacities 0 / 1 / huge and free tails D around max L_after and beyond 2^16."""
+    T.set_sim_engine(engine)
+    conv, q, a = random_trace(21, 3000, 200, q_max=9, a_max=9)
+    tr = upload(T, conv, q, a)
+    mL = tr.max_history
+    rows = []
+    for xi, qh in ((0, 0), (1, 0), (mL - 1, 0), (mL, 0), (mL + 1, 0), (70000, 3), (2**31, 0)):
+        for C in (0, 1, 17, 400, 2**31 - 1, 2**32 - 1):
+            rows.append((0, 1, C, xi, qh, 16))
+    rows += [(0, 0, C, 5, 2, 16) for C in (0, 1, 2**32 - 1)]
+    bt = T.simulate_batch([tr], rows)
+    check_instances(T, bt, rows, [(conv, q, a)])
+
+
 def test_spill_path_is_exact(T):
     """Force W = 32 entries with capacities that need more: chains spill to
     global memory and are re-run; results stay exact."""
@@ -175,6 +191,26 @@ def test_generator_bit_exact(T, name, seed, n):
     assert np.array_equal(prev, d.prev) and np.array_equal(J, d.J) and np.array_equal(La, d.L_after)
     assert np.array_equal(g.next[:E].cpu().numpy().view(np.uint32), d.next)
     assert g.max_history == int(d.L_after.max()) and g.num_conversations == np.unique(o.conv).size
+
+
+@pytest.mark.parametrize("capacity", ["exact", "bound"])
+def test_generator_context_cap_bit_exact(T, capacity):
+    """L_max small enough that the context window ends conversations: with exact
+    capacity the exact count path runs, with the N * max_turns bound the capped
+    slots are dropped through the sentinel sort."""
+    p = preset("wildchat", 4, 4000)
+    p["max_history_blocks"] = 30
+    g = T.generate_traces([p], capacity=capacity)[0]
+    o = O.generate(p)
+    E = g.num_events
+    assert E == o.E
+    assert np.array_equal(g.time_ticks[:E].cpu().numpy().view(np.uint64), o.ticks)
+    assert np.array_equal(g.conv[:E].cpu().numpy().view(np.uint32), o.conv)
+    assert np.array_equal(g.is_last[:E].cpu().numpy(), o.is_last.astype(np.uint8))
+    prev, J, La = g.prev_J_La()
+    d = O.derive(o.conv, o.q, o.a)
+    assert np.array_equal(prev, d.prev) and np.array_equal(La, d.L_after) and La.max() <= 30
+    assert np.array_equal(g.next[:E].cpu().numpy().view(np.uint32), d.next)
 
 
 # ----------------------------------------------------------------------------- config 3: 10^4 conversations
