@@ -93,15 +93,16 @@ class ClockSampler:
 
 # ----------------------------------------------------------------------------- reference (CPU oracle)
 def cpu_oracle_sample(seed: int = 0, n_conv: int = 1_000_000):
-    """Oracle as it stands: generate one config-4 trace, replay 8 instances (one per
-    capacity, alternating LRU / T-LRU(xi=16)) on host threads, tail metrics."""
+    """Oracle as it stands, on a bounded sample of the config-5 sweep: generate one trace
+    (seed 0), replay 9 instances (capacities 16, 32, ..., 4096 from the sweep's grid,
+    alternating LRU / T-LRU(xi=16)) on host threads, tail metrics for each."""
     from concurrent.futures import ThreadPoolExecutor
 
     import oracle as O
-    from paper_2510_15152_b200.inputs import ALPHA_MS, CAPS_CONFIG4, Q_HAT, SLO_BLOCKS, preset
+    from paper_2510_15152_b200.inputs import ALPHA_MS, CAPS_CONFIG5, Q_HAT, SLO_BLOCKS, preset
     t0 = time.perf_counter()
     tr = O.generate(preset("wildchat", seed, n_conv))
-    insts = [(i % 2, C, 16) for i, C in enumerate(CAPS_CONFIG4)]
+    insts = [(i % 2, C, 16) for i, C in enumerate(CAPS_CONFIG5[::3])]
     cores = min(len(insts), os.cpu_count() or 1)
 
     def one(x):
@@ -113,8 +114,9 @@ def cpu_oracle_sample(seed: int = 0, n_conv: int = 1_000_000):
     with ThreadPoolExecutor(max_workers=cores) as ex:
         n = sum(ex.map(one, insts))
     dt = time.perf_counter() - t0
-    return n, dt, cores, (f"config-4 sample: oracle generation of seed {seed} ({n_conv} conversations, {tr.E} "
-                          f"requests) + 8 instances (C in 64..4096, LRU / T-LRU xi=16) on {cores} threads")
+    return n, dt, cores, (f"config-5 sample: oracle generation of seed {seed} ({n_conv} conversations, {tr.E} "
+                          f"requests) + {len(insts)} instances (C = 16, 32, ..., 4096; LRU / T-LRU xi=16) "
+                          f"on {cores} threads, incl. tail metrics")
 
 
 def run_reference(args, rank, world):
@@ -133,7 +135,7 @@ def run_reference(args, rank, world):
     line = {"impl": "reference", "metric": "simulated requests/sec", "value": value, "unit": "requests/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-            "config": {"workload": "config4 sample (CPU oracle)", "requests_per_step": n_req},
+            "config": {"workload": "config5 sample (CPU oracle, see cpu_baseline.sample)", "requests_per_step": n_req},
             "cpu_baseline": {"value": value, "unit": "requests/s", "cores": cores, "kind": "oracle",
                              "sample": sample},
             "e2e": {"value": value, "unit": "requests/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -141,6 +143,21 @@ def run_reference(args, rank, world):
 
 
 # ----------------------------------------------------------------------------- ours
+def workload(name: str, rank: int):
+    """(seeds, rows, description) of one GPU's share.  Weak scaling: rank r takes the seeds
+    after rank r-1's, so per-GPU work is fixed as N grows."""
+    from paper_2510_15152_b200.inputs import SEEDS_CONFIG5, config5_rows
+    if name == "config5":
+        seeds = [SEEDS_CONFIG5 * rank + k for k in range(SEEDS_CONFIG5)]
+        return seeds, config5_rows(len(seeds)), (
+            "config5 sweep per GPU: 10 seeds x 10^6-conversation WildChat-shaped traces (generated each step) x "
+            "25 capacities (16..4096 blocks, geometric) x 20 xi (2..40 blocks) x {LRU, T-LRU} = 10^4 instances")
+    seeds = [SEEDS_PER_RANK * rank + k for k in range(SEEDS_PER_RANK)]
+    return seeds, workload_rows(len(seeds)), (
+        "config4 per GPU: 4 seeds x 10^6-conversation WildChat-shaped traces (generated each step), "
+        "C in {64..4096} x xi in {4..40} x {LRU, T-LRU} = 384 instances")
+
+
 def run_ours(args, rank, world, local_rank):
     import ctypes
 
@@ -154,12 +171,11 @@ def run_ours(args, rank, world, local_rank):
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
     stream = torch.cuda.current_stream()
-    seeds = [SEEDS_PER_RANK * rank + k for k in range(SEEDS_PER_RANK)]
+    seeds, rows, wl_desc = workload(args.config, rank)
     params = [preset("wildchat", s, args.conversations) for s in seeds]
 
-    # ---- setup (untimed): allocate traces at their exact size, the batch and the workspaces
+    # ---- setup (untimed): traces at their exact size, the batch and the workspaces
     traces = T.generate_traces(params, device=dev, exports=True)
-    rows = workload_rows(len(traces))
     batch = T.prepare_batch(traces, rows)
     ni = len(rows)
     E_tot = sum(traces[r[0]].num_events for r in rows)
@@ -172,15 +188,69 @@ def run_ours(args, rank, world, local_rank):
     tstructs = [tr.struct() for tr in traces]
     gathered = torch.empty(world * batch.results.numel(), dtype=torch.uint8, device=dev) if world > 1 else None
 
-    def step():
-        for g, ts, w in zip(gstructs, tstructs, gws):  # a1-a3: K1 generator (re-generates each trace)
+    def generate():  # a1-a3: K1 re-generates every trace in place
+        for g, ts, w in zip(gstructs, tstructs, gws):
             _abi.check(_abi.lib.tlru_generate_traces(ctypes.byref(g), 1, ctypes.byref(ts), T._ptr(w), w.numel(),
                                                      T._stream()))
-        batch.run()  # a4-a9: K2 + K3
+
+    def step():
+        generate()
+        batch.run()  # a4-a9: simulation engine + K3
         if world > 1:  # a10: NCCL all_gather of the per-instance results
             dist.all_gather_into_tensor(gathered, batch.results)
 
-    # ---- e2e host inputs (pinned) and device staging
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def timed(fn, steps: int, warmup: int, engine_stats: bool = True):
+        for _ in range(warmup):
+            fn()
+        barrier()
+        l0 = _abi.lib.tlru_launch_count()
+        k2s, k3s = [], []
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with ClockSampler(local_rank) as clk:
+            barrier()
+            t0.record(stream)
+            for _ in range(steps):
+                fn()
+                if engine_stats:
+                    st = T.last_sim_stats()
+                    k2s.append(st["k2_ms"])
+                    k3s.append(st["k3_ms"])
+            t1.record(stream)
+            barrier()
+        return dict(ms=t0.elapsed_time(t1) / steps, k2=statistics.mean(k2s) if k2s else 0.0,
+                    k3=statistics.mean(k3s) if k3s else 0.0, launches=(_abi.lib.tlru_launch_count() - l0),
+                    clocks=clk.summary())
+
+    # ---- main arm: default (stack) engine
+    T.set_sim_engine(T.ENGINE_STACK)
+    main = timed(step, args.steps, args.warmup)
+    stats = T.last_sim_stats()
+    assert stats["failed_chains"] == 0
+    res = batch.results_numpy()
+    assert np.all(res["requests"][:ni] > 0)
+
+    # ---- replay engine (Alg. 1 request by request) on seed 0's instances; must give identical bytes
+    rep = None
+    if not args.no_replay:
+        sub = [r for r in rows if r[0] == 0]
+        sub_idx = [i for i, r in enumerate(rows) if r[0] == 0]
+        if args.replay_instances:
+            sub, sub_idx = sub[:args.replay_instances], sub_idx[:args.replay_instances]
+        rbatch = T.prepare_batch(traces[:1], sub)
+        T.set_sim_engine(T.ENGINE_REPLAY)
+        r = timed(rbatch.run, 1, 1)
+        rst = T.last_sim_stats()
+        T.set_sim_engine(T.ENGINE_STACK)
+        assert rbatch.results_numpy().tobytes() == res[sub_idx].tobytes(), "engines disagree"
+        rep = dict(r, requests=sum(traces[0].num_events for _ in sub), instances=len(sub), stats=rst)
+        del rbatch
+
+    # ---- e2e: same batch through the public API from pinned host buffers
     host_turns = []
     for tr in traces:
         E = tr.num_events
@@ -208,60 +278,12 @@ def run_ours(args, rank, world, local_rank):
         host_results.copy_(batch.results, non_blocking=True)
         torch.cuda.current_stream().synchronize()
 
-    def barrier():
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
-
-    def timed(engine: int, steps: int, warmup: int):
-        T.set_sim_engine(engine)
-        for _ in range(warmup):
-            step()
-        barrier()
-        l0 = _abi.lib.tlru_launch_count()
-        k2s, k3s = [], []
-        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        with ClockSampler(local_rank) as clk:
-            barrier()
-            t0.record(stream)
-            for _ in range(steps):
-                step()
-                st = T.last_sim_stats()
-                k2s.append(st["k2_ms"])
-                k3s.append(st["k3_ms"])
-            t1.record(stream)
-            barrier()
-        st = T.last_sim_stats()
-        assert st["failed_chains"] == 0
-        res = batch.results_numpy()
-        assert np.all(res["requests"][:ni] > 0)
-        return dict(ms=t0.elapsed_time(t1) / steps, k2=statistics.mean(k2s), k3=statistics.mean(k3s),
-                    launches=(_abi.lib.tlru_launch_count() - l0), clocks=clk.summary(), stats=st,
-                    results=res.tobytes())
-
-    main = timed(T.ENGINE_STACK, args.steps, args.warmup)
-    rep = timed(T.ENGINE_REPLAY, max(1, args.steps // 2), 1) if not args.no_replay else None
-    if rep is not None:
-        assert rep["results"] == main["results"], "engines disagree"
-    T.set_sim_engine(T.ENGINE_STACK)
-    ms, launches, clocks, stats = main["ms"], main["launches"], main["clocks"], main["stats"]
-    k2_ms, k3_ms = [main["k2"]], [main["k3"]]
-
-    # ---- e2e (same batch through the public API from host buffers)
-    for _ in range(max(1, args.warmup)):
-        e2e_step()
-    barrier()
-    t_e2e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    t_e2e[0].record(stream)
-    for _ in range(args.steps):
-        e2e_step()
-    t_e2e[1].record(stream)
-    barrier()
-    e2e_ms = t_e2e[0].elapsed_time(t_e2e[1]) / args.steps
+    e2e = timed(e2e_step, args.steps, max(1, min(args.warmup, 2)), engine_stats=False)
+    assert host_results.numpy().tobytes() == res.tobytes()
 
     # ---- max over ranks
-    loc = torch.tensor([ms, e2e_ms, statistics.mean(k2_ms), statistics.mean(k3_ms),
-                        rep["ms"] if rep else 0.0, rep["k2"] if rep else 0.0], dtype=torch.float64, device=dev)
+    loc = torch.tensor([main["ms"], e2e["ms"], main["k2"], main["k3"], rep["ms"] if rep else 0.0,
+                        rep["k2"] if rep else 0.0], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(loc, op=dist.ReduceOp.MAX)
     ms, e2e_ms, k2, k3, rep_ms, rep_k2 = [float(x) for x in loc.tolist()]
@@ -270,7 +292,7 @@ def run_ours(args, rank, world, local_rank):
     req_all = E_tot * world
     value = req_all / (ms / 1000.0)
     peak, peak_src = peaks()
-    achieved = ALGO_BYTES_PER_REQUEST * E_tot / (k2 / 1000.0) / 1e9  # GB/s, per GPU, K2 phase
+    achieved = ALGO_BYTES_PER_REQUEST * E_tot / (k2 / 1000.0) / 1e9  # GB/s per GPU, simulation phase
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
@@ -282,11 +304,10 @@ def run_ours(args, rank, world, local_rank):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "u32", "data": "synthetic",
         "config": {
-            "workload": "config4: per GPU 4 seeds x 10^6-conversation WildChat-shaped traces (generated each step), "
-                        "C in {64..4096} x xi in {4..40} x {LRU, T-LRU} = 384 instances",
-            "instances_per_gpu": ni, "requests_per_gpu_step": E_tot, "conversations": args.conversations,
+            "workload": wl_desc, "instances_per_gpu": ni, "requests_per_gpu_step": E_tot,
+            "conversations": args.conversations,
             "parallelism": f"dp{world} (instances sharded by seed, NCCL all_gather of results)",
-            "l2": "inputs larger than L2: 0.77 GB of b written per GPU-step",
+            "l2": f"inputs larger than L2: {2 * E_tot / 1e9:.1f} GB of b written per GPU-step",
             "engine": "stack (closed form of Alg. 1 from the stack property, all capacities of a trace per pass; "
                       "bit-identical to the replay engine and the oracle); no dedup of identical instances",
             "engine_ms": k2, "k3_ms": k3,
@@ -294,20 +315,21 @@ def run_ours(args, rank, world, local_rank):
         "e2e": {"value": req_all / (e2e_ms / 1000.0), "unit": "requests/s", "h2d_bytes_per_step": h2d_bytes,
                 "d2h_bytes_per_step": d2h_bytes, "ms_per_step": e2e_ms},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "kernel": "s1/s2 stack-engine kernels (simulation phase)",
-                     "peak_source": peak_src,
-                     "algorithmic_bytes_per_request": ALGO_BYTES_PER_REQUEST},
-        "gpu_launches": int(launches // max(args.steps, 1)),
-        "clocks": clocks,
+                     "traffic": traffic, "kernel": "stack engine s1/s2 (simulation phase, all launches of a step)",
+                     "peak_source": peak_src, "algorithmic_bytes_per_request": ALGO_BYTES_PER_REQUEST},
+        "gpu_launches": int(main["launches"] // max(args.steps, 1)),
+        "clocks": main["clocks"],
     }
     if rep is not None:
-        rep_achieved = ALGO_BYTES_PER_REQUEST * E_tot / (rep_k2 / 1000.0) / 1e9
+        rep_achieved = ALGO_BYTES_PER_REQUEST * rep["requests"] / (rep_k2 / 1000.0) / 1e9
         line["replay_engine"] = {
-            "value": req_all / (rep_ms / 1000.0), "unit": "requests/s", "ms_per_step": rep_ms, "k2_ms": rep_k2,
+            "value": rep["requests"] / (rep_k2 / 1000.0), "unit": "requests/s (K2 kernels only)",
+            "instances": rep["instances"], "k2_ms": rep_k2, "ms_per_call": rep_ms,
             "segment_events": rep["stats"]["segment_events"], "spilled_chains": rep["stats"]["spilled_chains"],
             "roofline": {"bound": "hbm", "achieved": rep_achieved, "peak": peak, "unit": "GB/s",
                          "frac": rep_achieved / peak, "kernel": "sim_kernel<W> (K2 replay)"},
-            "note": "Alg. 1 replayed request by request (one lane per instance); identical result bytes"}
+            "note": "Alg. 1 replayed request by request (one lane per instance) on seed 0's instances; "
+                    "result bytes identical to the stack engine"}
     if not args.no_cpu_baseline:
         n, dt, cores, sample = cpu_oracle_sample(seed=0, n_conv=args.conversations)
         line["cpu_baseline"] = {"value": n / dt, "unit": "requests/s", "cores": cores, "kind": "oracle",
@@ -324,6 +346,8 @@ def main():
     ap.add_argument("--conversations", type=int, default=1_000_000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-replay", action="store_true", help="skip timing the replay engine")
+    ap.add_argument("--replay-instances", type=int, default=0, help="limit the replay-engine sample (0 = all of seed 0)")
+    ap.add_argument("--config", choices=("config5", "config4"), default="config5")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

@@ -329,6 +329,7 @@ __global__ void __launch_bounds__(S_THREADS) s2_main_kernel(const uint64_t* __re
   uint32_t Jv[4];
 #pragma unroll
   for (int u = 0; u < 4; ++u) Jv[u] = J_s[j0 + u];
+  const uint32_t J01 = Jv[0] | (Jv[1] << 16), J23 = Jv[2] | (Jv[3] << 16);
 #pragma unroll
   for (int d = 0; d < ND; ++d) {
     uint32_t nfb[4], fb[4], anf[4], af[4], nfa[4];
@@ -342,27 +343,42 @@ __global__ void __launch_bounds__(S_THREADS) s2_main_kernel(const uint64_t* __re
       af[u] = af_s[d][j0 + u];
       nfa[u] = nfall_s[d][j0 + u];
     }
+    // packed 16x2 operands for capacities <= 65535: X = min(nfb, max(C, A) - A) with A = A_nf
+    // clamped to 65535 (exact: if A > 65535 >= C then both sides give 0)
+    const uint32_t A01 = min(anf[0], 65535u) | (min(anf[1], 65535u) << 16);
+    const uint32_t A23 = min(anf[2], 65535u) | (min(anf[3], 65535u) << 16);
+    const uint32_t N01 = nfb[0] | (nfb[1] << 16), N23 = nfb[2] | (nfb[3] << 16);
     const uint32_t k1 = ch.inst0 + ch.dbeg[d + 1];
     for (uint32_t k = ch.inst0 + ch.dbeg[d] + lane4; k < k1; k += 4) {
       const StackInstDev in = insts[k];
-      uint32_t b[4];
+      uint32_t w01, w23;
+      if (saturated && in.C <= 65535u) {
+        const uint32_t C2 = in.C * 0x10001u;
+        w01 = __vsub2(J01, __vminu2(N01, __vsub2(__vmaxu2(C2, A01), A01)));
+        w23 = __vsub2(J23, __vminu2(N23, __vsub2(__vmaxu2(C2, A23), A23)));
+      } else {
+        uint32_t b[4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        uint32_t X = min(nfb[u], sat_sub(in.C, anf[u]));
-        if (!saturated && nfa[u] < in.C && fb[u] > 0) {  // warm-up: free blocks can still be cached
-          const uint32_t xf = min(fb[u], sat_sub(sat_sub(in.C, nfa[u]), af[u]));
-          X += xf;
-          if (xf && e0 + j0 + u < E) atomicAdd(&sumXf[in.inst], static_cast<unsigned long long>(xf));
+        for (int u = 0; u < 4; ++u) {
+          uint32_t X = min(nfb[u], sat_sub(in.C, anf[u]));
+          if (!saturated && nfa[u] < in.C && fb[u] > 0) {  // warm-up: free blocks can still be cached
+            const uint32_t xf = min(fb[u], sat_sub(sat_sub(in.C, nfa[u]), af[u]));
+            X += xf;
+            if (xf && e0 + j0 + u < E) atomicAdd(&sumXf[in.inst], static_cast<unsigned long long>(xf));
+          }
+          b[u] = Jv[u] - X;
         }
-        b[u] = Jv[u] - X;
+        w01 = b[0] | (b[1] << 16);
+        w23 = b[2] | (b[3] << 16);
       }
       uint16_t* row = bout + in.boff + e0 + j0;
       if (full && ((reinterpret_cast<uintptr_t>(row) & 7u) == 0)) {
-        *reinterpret_cast<uint2*>(row) = make_uint2(b[0] | (b[1] << 16), b[2] | (b[3] << 16));
+        *reinterpret_cast<uint2*>(row) = make_uint2(w01, w23);
       } else {
+        const uint32_t bb[4] = {w01 & 0xFFFFu, w01 >> 16, w23 & 0xFFFFu, w23 >> 16};
 #pragma unroll
         for (int u = 0; u < 4; ++u)
-          if (e0 + j0 + u < E) row[u] = static_cast<uint16_t>(b[u]);
+          if (e0 + j0 + u < E) row[u] = static_cast<uint16_t>(bb[u]);
       }
     }
   }

@@ -50,6 +50,16 @@ SLO_BLOCKS = 16
 XI_BLOCKS = (4, 8, 12, 16, 24, 40)
 CAPS_CONFIG3 = (32, 64, 128, 256, 512, 1024)
 CAPS_CONFIG4 = (64, 128, 256, 512, 1024, 2048, 3072, 4096)
+# BASELINE config 5 (the sweep): 25 capacities geometric 16..4096, 20 xi values 2..40
+CAPS_CONFIG5 = tuple(int(round(16 * 256 ** (k / 24))) for k in range(25))
+XI_CONFIG5 = tuple(range(2, 41, 2))
+SEEDS_CONFIG5 = 10
+
+
+def config5_rows(n_traces: int = SEEDS_CONFIG5):
+    """(trace, policy, C, xi, Q_hat, slo) for the config-5 sweep over n_traces seeds."""
+    return [(t, pol, C, xi, Q_HAT, SLO_BLOCKS) for t in range(n_traces) for pol in (0, 1) for C in CAPS_CONFIG5
+            for xi in XI_CONFIG5]
 
 # Figure 1 (P:37): events A, B, A with 100-block prompts, no responses, C = 100.
 FIG1 = dict(conv=[0, 1, 0], q=[100, 100, 100], a=[0, 0, 0], C=100, xi=150, q_hat=100)

@@ -10,8 +10,9 @@ import pytest
 import torch
 
 import oracle as O
-from paper_2510_15152_b200.inputs import (CAPS_CONFIG3, CAPS_CONFIG4, FIG1, Q_HAT, SLO_BLOCKS, XI_BLOCKS, ALPHA_MS,
-                                          preset, random_trace, tiny_trace)
+from paper_2510_15152_b200.inputs import (CAPS_CONFIG3, CAPS_CONFIG4, CAPS_CONFIG5, FIG1, Q_HAT, SLO_BLOCKS,
+                                          XI_BLOCKS, XI_CONFIG5, ALPHA_MS, config5_rows, preset, random_trace,
+                                          tiny_trace)
 
 pytestmark = pytest.mark.gpu
 
@@ -266,6 +267,48 @@ def test_config4_bench_launch_sampled(T, engine):
             if prevb is not None:
                 assert np.all(b <= prevb)
             prevb = b
+
+
+# ----------------------------------------------------------------------------- config 5 (the bench workload)
+def test_config5_bench_launch_sampled(T):
+    """bench.py's launch: the 10^4-instance config-5 sweep (10 seeds x 25 C x 20 xi x
+    {LRU, T-LRU}) in ONE tlru_simulate_batch on 10^6-conversation traces, default engine.
+    Sampled instances of three seeds against the oracle element by element; every
+    instance against properties that hold at any size."""
+    T.set_sim_engine(T.ENGINE_STACK)
+    params = [preset("wildchat", s, 1_000_000) for s in range(10)]
+    traces = T.generate_traces(params, exports=False)
+    rows = config5_rows(10)
+    bt = T.simulate_batch(traces, rows)
+    res = bt.results_numpy()
+    rng = np.random.default_rng(5)
+    for t in (0, 4, 9):
+        o = O.generate(params[t])
+        assert traces[t].num_events == o.E
+        idx = [i for i, r in enumerate(rows) if r[0] == t]
+        for i in rng.choice(idx, size=3, replace=False):
+            _, pol, C, xi, qh, slo = rows[i]
+            r = O.replay(o.conv, o.q, o.a, pol, C, xi, qh)
+            assert np.array_equal(bt.b(i).astype(np.uint64), r.b), rows[i]
+            tl = O.tail(r.b, xi, ALPHA_MS * xi, slo, ALPHA_MS)
+            assert (res[i]["tel_blocks"], res[i]["slo_violations"], res[i]["p90"], res[i]["p95"]) == \
+                (tl.tel_blocks, tl.slo_violations, tl.p90, tl.p95)
+            assert (res[i]["evicted_trim"], res[i]["evicted_lru"], res[i]["max_occupancy"]) == \
+                (r.evicted_trim, r.evicted_lru, r.max_occupancy)
+    key = {r: i for i, r in enumerate(rows)}
+    for i, (t, pol, C, xi, qh, slo) in enumerate(rows):
+        assert res[i]["requests"] == traces[t].num_events and res[i]["max_occupancy"] <= C
+        if pol == 0:  # LRU ignores xi except in TEL: identical b statistics across xi
+            j = key[(t, 0, C, XI_CONFIG5[0], qh, slo)]
+            assert res[i]["sum_uncached"] == res[j]["sum_uncached"] and res[i]["p99"] == res[j]["p99"]
+        if pol == 1 and xi <= qh:  # T-LRU with xi <= Q_hat is LRU
+            j = key[(t, 0, C, xi, qh, slo)]
+            assert res[i].tobytes() == res[j].tobytes()
+    for t in range(10):  # inclusion: sum b non-increasing in C, per policy and xi
+        for pol in (0, 1):
+            for xi in XI_CONFIG5:
+                sums = [res[key[(t, pol, C, xi, Q_HAT, SLO_BLOCKS)]]["sum_uncached"] for C in CAPS_CONFIG5]
+                assert all(a >= b for a, b in zip(sums, sums[1:]))
 
 
 # ----------------------------------------------------------------------------- tail metrics
