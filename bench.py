@@ -32,7 +32,13 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-ALGO_BYTES_PER_REQUEST = 10  # 8-byte event record read + 2-byte uncached count written
+# Algorithmic HBM bytes:
+#  * replay engine (SURVEY 8(d) model): 8-byte event record read per request + 2-byte b written = 10 B/request;
+#  * stack engine: 2-byte b written per request + each trace pass reads the 8-byte sim view and 4-byte next
+#    link and writes/reads the 8-byte scan record once per event (20 B/event/pass), shared by all instances.
+ALGO_BYTES_PER_REQUEST = 10
+STACK_B_BYTES = 2
+STACK_PASS_BYTES_PER_EVENT = 20
 SEEDS_PER_RANK = 4
 
 
@@ -292,13 +298,20 @@ def run_ours(args, rank, world, local_rank):
     req_all = E_tot * world
     value = req_all / (ms / 1000.0)
     peak, peak_src = peaks()
-    achieved = ALGO_BYTES_PER_REQUEST * E_tot / (k2 / 1000.0) / 1e9  # GB/s per GPU, simulation phase
+    nd_per_trace = {}
+    for r in rows:
+        D = (r[3] - r[4]) if (r[1] == 1 and r[3] > r[4]) else 0
+        nd_per_trace.setdefault(r[0], set()).add(D)
+    passes = sum((len(v) + 7) // 8 for v in nd_per_trace.values())  # D chunks of <= 8 values per trace
+    stack_bytes = STACK_B_BYTES * E_tot + STACK_PASS_BYTES_PER_EVENT * sum(
+        traces[t].num_events * ((len(v) + 7) // 8) for t, v in nd_per_trace.items())
+    achieved = stack_bytes / (k2 / 1000.0) / 1e9  # GB/s per GPU over the simulation phase
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
         t = json.load(open(tpath))
-        if "dram_bytes_per_request" in t:
-            traffic = float(t["dram_bytes_per_request"]) * E_tot
+        if "s2_dram_bytes_per_request" in t:
+            traffic = float(t["s2_dram_bytes_per_request"]) * E_tot
     line = {
         "metric": "simulated requests/sec", "value": value, "unit": "requests/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
@@ -315,8 +328,11 @@ def run_ours(args, rank, world, local_rank):
         "e2e": {"value": req_all / (e2e_ms / 1000.0), "unit": "requests/s", "h2d_bytes_per_step": h2d_bytes,
                 "d2h_bytes_per_step": d2h_bytes, "ms_per_step": e2e_ms},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "kernel": "stack engine s1/s2 (simulation phase, all launches of a step)",
-                     "peak_source": peak_src, "algorithmic_bytes_per_request": ALGO_BYTES_PER_REQUEST},
+                     "traffic": traffic, "kernel": "stack engine (s1 + s2_main, all launches of a step)",
+                     "peak_source": peak_src,
+                     "algorithmic_bytes": f"{STACK_B_BYTES} B/request (b) + {STACK_PASS_BYTES_PER_EVENT} B/event "
+                                          f"per trace pass ({passes} passes)",
+                     "survey_model_frac": ALGO_BYTES_PER_REQUEST * E_tot / (k2 / 1000.0) / 1e9 / peak},
         "gpu_launches": int(main["launches"] // max(args.steps, 1)),
         "clocks": main["clocks"],
     }

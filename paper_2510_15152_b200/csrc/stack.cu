@@ -213,8 +213,10 @@ __global__ void __launch_bounds__(S_THREADS) s1_scan_kernel(Prefix8* blockagg, u
 //      totals A_nf, A_f;
 //   C. natural order again: b for every instance, instances grouped by D, coalesced stores.
 
+constexpr uint32_t IT = 512;  // instance-table tile staged in shared memory by s2
+
 template <int ND>
-__global__ void __launch_bounds__(S_THREADS) s2_main_kernel(const uint64_t* __restrict__ sim,
+__global__ void __launch_bounds__(S_THREADS, 4) s2_main_kernel(const uint64_t* __restrict__ sim,
                                                             const uint64_t* __restrict__ scanrec, uint32_t E,
                                                             const ChunkDev* __restrict__ chunk,
                                                             const StackInstDev* __restrict__ insts,
@@ -226,9 +228,14 @@ __global__ void __launch_bounds__(S_THREADS) s2_main_kernel(const uint64_t* __re
   typedef cub::BlockScan<Prefix8, S_THREADS> BS;
   typedef cub::BlockScan<uint32_t, S_THREADS> BSu;
   __shared__ ChunkDev ch;
+  struct InstTile {  // phase C instance-table tile (reuses the scan storage)
+    uint64_t off[IT];
+    uint32_t C[IT], inst[IT];
+  };
   __shared__ union {
     typename BS::TempStorage scan;
     typename BSu::TempStorage scanu;
+    InstTile it;
   } tmp;
   __shared__ uint32_t anf_s[ND][S_THREADS], af_s[ND][S_THREADS];
   __shared__ uint32_t p_s[S_THREADS], cbeg_s[S_THREADS + 1];
@@ -330,55 +337,70 @@ __global__ void __launch_bounds__(S_THREADS) s2_main_kernel(const uint64_t* __re
 #pragma unroll
   for (int u = 0; u < 4; ++u) Jv[u] = J_s[j0 + u];
   const uint32_t J01 = Jv[0] | (Jv[1] << 16), J23 = Jv[2] | (Jv[3] << 16);
-#pragma unroll
-  for (int d = 0; d < ND; ++d) {
-    uint32_t nfb[4], fb[4], anf[4], af[4], nfa[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const bool hit = p_s[j0 + u] != TLRU_NONE;
-      const uint32_t Lbu = Lb_s[j0 + u];
-      nfb[u] = hit ? nf_of(Lbu, ch.D[d]) : 0u;
-      fb[u] = hit ? f_of(Lbu, ch.D[d]) : 0u;
-      anf[u] = anf_s[d][j0 + u];
-      af[u] = af_s[d][j0 + u];
-      nfa[u] = nfall_s[d][j0 + u];
+  // The chunk's instance table goes through shared memory in tiles of IT entries.
+  for (uint32_t tb = 0; tb < ch.ninst; tb += IT) {
+    const uint32_t te = min(ch.ninst, tb + IT);
+    __syncthreads();
+    for (uint32_t k = tb + t; k < te; k += S_THREADS) {
+      const StackInstDev in = insts[ch.inst0 + k];
+      tmp.it.C[k - tb] = in.C;
+      tmp.it.inst[k - tb] = in.inst;
+      tmp.it.off[k - tb] = in.boff;
     }
-    // packed 16x2 operands for capacities <= 65535: X = min(nfb, max(C, A) - A) with A = A_nf
-    // clamped to 65535 (exact: if A > 65535 >= C then both sides give 0)
-    const uint32_t A01 = min(anf[0], 65535u) | (min(anf[1], 65535u) << 16);
-    const uint32_t A23 = min(anf[2], 65535u) | (min(anf[3], 65535u) << 16);
-    const uint32_t N01 = nfb[0] | (nfb[1] << 16), N23 = nfb[2] | (nfb[3] << 16);
-    const uint32_t k1 = ch.inst0 + ch.dbeg[d + 1];
-    for (uint32_t k = ch.inst0 + ch.dbeg[d] + lane4; k < k1; k += 4) {
-      const StackInstDev in = insts[k];
-      uint32_t w01, w23;
-      if (saturated && in.C <= 65535u) {
-        const uint32_t C2 = in.C * 0x10001u;
-        w01 = __vsub2(J01, __vminu2(N01, __vsub2(__vmaxu2(C2, A01), A01)));
-        w23 = __vsub2(J23, __vminu2(N23, __vsub2(__vmaxu2(C2, A23), A23)));
-      } else {
-        uint32_t b[4];
+    __syncthreads();
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          uint32_t X = min(nfb[u], sat_sub(in.C, anf[u]));
-          if (!saturated && nfa[u] < in.C && fb[u] > 0) {  // warm-up: free blocks can still be cached
-            const uint32_t xf = min(fb[u], sat_sub(sat_sub(in.C, nfa[u]), af[u]));
-            X += xf;
-            if (xf && e0 + j0 + u < E) atomicAdd(&sumXf[in.inst], static_cast<unsigned long long>(xf));
-          }
-          b[u] = Jv[u] - X;
-        }
-        w01 = b[0] | (b[1] << 16);
-        w23 = b[2] | (b[3] << 16);
+    for (int d = 0; d < ND; ++d) {
+      const uint32_t kb = max(ch.dbeg[d], tb), ke = min(ch.dbeg[d + 1], te);
+      if (kb >= ke) continue;
+      uint32_t nfb[4], fb[4], anf[4], af[4], nfa[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const bool hit = p_s[j0 + u] != TLRU_NONE;
+        const uint32_t Lbu = Lb_s[j0 + u];
+        nfb[u] = hit ? nf_of(Lbu, ch.D[d]) : 0u;
+        fb[u] = hit ? f_of(Lbu, ch.D[d]) : 0u;
+        anf[u] = anf_s[d][j0 + u];
+        af[u] = af_s[d][j0 + u];
+        nfa[u] = nfall_s[d][j0 + u];
       }
-      uint16_t* row = bout + in.boff + e0 + j0;
-      if (full && ((reinterpret_cast<uintptr_t>(row) & 7u) == 0)) {
-        *reinterpret_cast<uint2*>(row) = make_uint2(w01, w23);
-      } else {
-        const uint32_t bb[4] = {w01 & 0xFFFFu, w01 >> 16, w23 & 0xFFFFu, w23 >> 16};
+      // packed 16x2 operands for capacities <= 65535: X = min(nfb, max(C, A) - A) with A = A_nf
+      // clamped to 65535 (exact: if A > 65535 >= C then both sides give 0)
+      const uint32_t A01 = min(anf[0], 65535u) | (min(anf[1], 65535u) << 16);
+      const uint32_t A23 = min(anf[2], 65535u) | (min(anf[3], 65535u) << 16);
+      const uint32_t N01 = nfb[0] | (nfb[1] << 16), N23 = nfb[2] | (nfb[3] << 16);
+#pragma unroll 4
+      for (uint32_t k = kb + lane4; k < ke; k += 4) {
+        const uint32_t C = tmp.it.C[k - tb];
+        uint32_t w01, w23;
+        if (saturated && C <= 65535u) {
+          const uint32_t C2 = C * 0x10001u;
+          w01 = __vsub2(J01, __vminu2(N01, __vsub2(__vmaxu2(C2, A01), A01)));
+          w23 = __vsub2(J23, __vminu2(N23, __vsub2(__vmaxu2(C2, A23), A23)));
+        } else {
+          uint32_t b[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
-          if (e0 + j0 + u < E) row[u] = static_cast<uint16_t>(bb[u]);
+          for (int u = 0; u < 4; ++u) {
+            uint32_t X = min(nfb[u], sat_sub(C, anf[u]));
+            if (!saturated && nfa[u] < C && fb[u] > 0) {  // warm-up: free blocks can still be cached
+              const uint32_t xf = min(fb[u], sat_sub(sat_sub(C, nfa[u]), af[u]));
+              X += xf;
+              if (xf && e0 + j0 + u < E)
+                atomicAdd(&sumXf[tmp.it.inst[k - tb]], static_cast<unsigned long long>(xf));
+            }
+            b[u] = Jv[u] - X;
+          }
+          w01 = b[0] | (b[1] << 16);
+          w23 = b[2] | (b[3] << 16);
+        }
+        uint16_t* row = bout + tmp.it.off[k - tb] + e0 + j0;
+        if (full && ((reinterpret_cast<uintptr_t>(row) & 7u) == 0)) {
+          *reinterpret_cast<uint2*>(row) = make_uint2(w01, w23);
+        } else {
+          const uint32_t bb[4] = {w01 & 0xFFFFu, w01 >> 16, w23 & 0xFFFFu, w23 >> 16};
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (e0 + j0 + u < E) row[u] = static_cast<uint16_t>(bb[u]);
+        }
       }
     }
   }
