@@ -7,7 +7,7 @@
 // of conversation theta with previous turn p (history Lb = L_after[p]):
 //   A_nf(e) = sum NF(L_x), A_f(e) = sum F(L_x) over x in (p, e) with next[x] > e
 //             (the conversations used after theta's previous turn, each at its latest L),
-//   NF_all(e), F_all(e) = the same sums over every conversation's last turn before e,
+//   NF_all(e) = the same non-free sum over every conversation's last turn before e,
 //   X_theta = min(NF(Lb), (C - A_nf)^+) + min(F(Lb), (C - NF_all - A_f)^+),
 //   b = J - X_theta
 // and, telescoping Alg. 1's per-request evictions over the trace (used and the cached
@@ -16,17 +16,22 @@
 //   evicted_trim  = sum_e F(L_after_e) - sum_e X_f(e) - Fc_final       (Phase 1)
 //   evicted_lru   = evicted_total - evicted_trim                        (Phase 2)
 //   max_occupancy = min(C, U_final)
-// Pinned against the oracle by tests/test_gpu_parity.py (both engines, every config)
-// and, on CPU, tests/stackdist.py.
+// Pinned against the oracle by tests/test_gpu_parity.py (both engines, every config).
 //
-// Kernels per (trace, chunk of <= 8 distinct D):
-//   s1_block : block aggregates (saturating) of the per-event universe deltas
-//              (NF(L_after) - NF(L_before), F(...) - F(...)) for each D, plus sum F(L_after), sum a
-//   s1_scan  : one CTA: exclusive scan of the block aggregates
-//   s2_main  : one thread per request event: block scan of the deltas + the block prefix
-//              = NF_all(e), F_all(e); backward window scan for A_nf / A_f of every D (early
-//              exit once every D's non-free sum reaches its largest C); then b for every
-//              instance of the chunk, coalesced 2-byte stores
+// Kernels per (trace, chunk of <= 24 distinct D):
+//   s1_block  : per event the scan record (next | L_after << 32); per 256-event block the
+//               growth of NF_all for every D; histograms of L_after over all events and over
+//               final turns (for the exact totals); sum a
+//   s1_totals : one CTA: exact totals per D from the histograms, and per D the block prefixes
+//               of NF_all up to nsat[d] = the first block from which NF_all >= the largest
+//               capacity of that D (NF_all is non-decreasing): no free block is cached after it
+//   s2_warm   : (block, D) pairs before nsat[d]: the general closed form (exact NF_all, free blocks)
+//   s2_sat    : (block, D) pairs from nsat[d]: one CTA = 256 events: (A) window lengths; (B) every
+//               window (p, e) cut into <= 64-event chunks spread over all 256 threads,
+//               scanned branch-free with sum max(L, D) for D pairs in packed 16x2 registers;
+//               (C) b for every instance, 4 events per thread, packed 16x2 arithmetic,
+//               8-byte stores, instance table staged in shared memory
+//   s3_results: eviction counters and occupancy from the telescoped identities
 #include <cub/cub.cuh>
 
 #include <algorithm>
@@ -37,33 +42,18 @@
 
 namespace tlru {
 
-constexpr int SND = 8;  // D values per chunk
-
-struct Prefix8 {  // saturating per-D prefix sums of non-free / free blocks
-  uint32_t nf[SND];
-  uint32_t f[SND];
-};
-
-struct SatAdd {
-  __host__ __device__ __forceinline__ Prefix8 operator()(const Prefix8& a, const Prefix8& b) const {
-    Prefix8 r;
-#pragma unroll
-    for (int d = 0; d < SND; ++d) {
-      uint32_t x = a.nf[d] + b.nf[d];
-      r.nf[d] = x < a.nf[d] ? 0xFFFFFFFFu : x;
-      uint32_t y = a.f[d] + b.f[d];
-      r.f[d] = y < a.f[d] ? 0xFFFFFFFFu : y;
-    }
-    return r;
-  }
-};
+constexpr int SND = 24;         // D values per chunk
+constexpr int S_THREADS = 256;  // events per s2 block
+constexpr uint32_t IT = 512;    // instance-table tile staged in shared memory by s2
+constexpr uint32_t WCH_MAX = 64;
 
 struct ChunkDev {
   uint32_t D[SND];
-  uint32_t Cmax[SND];     // largest capacity among the chunk's instances with this D
-  uint32_t dbeg[SND + 1]; // instances of D[d]: [inst0 + dbeg[d], inst0 + dbeg[d+1])
-  uint32_t nd;
-  uint32_t inst0, ninst;  // instances [inst0, inst0 + ninst) of the StackInstDev table
+  uint32_t Cmax[SND];      // largest capacity among the chunk's instances with this D
+  uint32_t dbeg[SND + 1];  // instances of D[d]: [inst0 + dbeg[d], inst0 + dbeg[d+1]), sorted by C
+  uint32_t dbig[SND];      // first instance of D[d] with C > 65535 (packed 16x2 path before it)
+  uint32_t nd;             // real D values (the rest pad with D[0] and own no instances)
+  uint32_t inst0, ninst;   // instances [inst0, inst0 + ninst) of the StackInstDev table
 };
 
 struct StackInstDev {
@@ -76,228 +66,178 @@ struct ChunkTotals {  // per chunk: exact trace totals
   unsigned long long nfE[SND];   // NF_all(E): non-free blocks of the final universe
   unsigned long long fE[SND];    // F_all(E)
   unsigned long long suma;       // sum_e a_e
-  uint32_t nsat;                 // first block whose prefix saturates every D (NF_all >= Cmax)
-  uint32_t pad;
+  uint32_t nsat[SND];            // first 256-event block where NF_all(D[d]) >= Cmax[d]
+  uint32_t nsat_min, nsat_max;   // over the real D values
 };
 
 __device__ __forceinline__ uint32_t nf_of(uint32_t L, uint32_t D) { return L > D ? L - D : 0u; }
 __device__ __forceinline__ uint32_t f_of(uint32_t L, uint32_t D) { return L < D ? L : D; }
 __device__ __forceinline__ uint32_t sat_sub(uint32_t a, uint32_t b) { return a > b ? a - b : 0u; }
 
-constexpr int S_THREADS = 256;  // events per block in s1 / s2 (one thread per event)
-
-// Per-event deltas of the universe sums (non-free, free) for each D: at event e the
-// conversation's history goes from L_before to L_after.
-__device__ __forceinline__ void universe_delta(const ChunkDev& ch, uint32_t Lb, uint32_t La, Prefix8& v) {
-#pragma unroll
-  for (int d = 0; d < SND; ++d) {
-    const uint32_t D = ch.D[d];
-    v.nf[d] = nf_of(La, D) - nf_of(Lb, D);
-    v.f[d] = f_of(La, D) - f_of(Lb, D);
-  }
-}
-
 __device__ __forceinline__ uint32_t L_before(const uint64_t* sim, uint64_t s) {
   const uint32_t p = sim_prev(s);
   return p == TLRU_NONE ? 0u : sim_La(__ldg(sim + p));
 }
 
-// s1: per-event scan record (next | L_after << 32) for the window scans, block aggregates of
-// the universe deltas (saturating, one per 256 events), and the exact trace totals.  A
-// persistent grid walks the 256-event blocks so the totals are reduced once per CTA.
-constexpr int NTOT = 3 * SND + 1;
-
+// ----------------------------------------------------------------------------- s1
+// Persistent grid over 256-event blocks: scan records, per-block growth of NF_all for every D
+// (blockagg[blk * SND + d]), L_after histograms (all events / final turns) and sum a.
 __global__ void __launch_bounds__(S_THREADS) s1_block_kernel(const uint64_t* __restrict__ sim,
                                                              const uint32_t* __restrict__ next, uint32_t E,
                                                              const ChunkDev* __restrict__ chunk,
                                                              uint64_t* __restrict__ scanrec,
-                                                             Prefix8* __restrict__ blockagg, ChunkTotals* totals) {
-  typedef cub::BlockReduce<Prefix8, S_THREADS> BRp;
-  __shared__ typename BRp::TempStorage tmp;
-  __shared__ ChunkDev ch;
-  __shared__ unsigned long long part[S_THREADS / 32][NTOT];
-  if (threadIdx.x == 0) ch = *chunk;
+                                                             uint32_t* __restrict__ blockagg, uint32_t bins,
+                                                             uint32_t* hist_all, uint32_t* hist_last,
+                                                             ChunkTotals* totals) {
+  extern __shared__ uint32_t sh[];  // [2 * bins] when bins fit, else unused
+  __shared__ uint32_t wsum[S_THREADS / 32][SND];
+  __shared__ uint32_t Ds[SND];
+  const bool smem_hist = bins <= 8192;
+  uint32_t* ha = smem_hist ? sh : hist_all;
+  uint32_t* hl = smem_hist ? sh + bins : hist_last;
+  if (smem_hist)
+    for (uint32_t k = threadIdx.x; k < 2 * bins; k += S_THREADS) sh[k] = 0;
+  if (threadIdx.x < SND) Ds[threadIdx.x] = chunk->D[threadIdx.x];
+  const uint32_t nd = chunk->nd;
   __syncthreads();
-  unsigned long long tv[NTOT];
-#pragma unroll
-  for (int k = 0; k < NTOT; ++k) tv[k] = 0;
+  unsigned long long sa = 0;
   const uint32_t nblocks = (E + S_THREADS - 1) / S_THREADS;
+  const uint32_t warp = threadIdx.x / 32, lane = threadIdx.x & 31;
   for (uint32_t blk = blockIdx.x; blk < nblocks; blk += gridDim.x) {
     const uint32_t e = blk * S_THREADS + threadIdx.x;
-    Prefix8 v{};
+    uint32_t La = 0, Lb = 0;
     if (e < E) {
       const uint64_t s = __ldg(sim + e);
-      const uint32_t La = sim_La(s);
-      scanrec[e] = uint64_t(__ldg(next + e)) | (uint64_t(La) << 32);
-      universe_delta(ch, L_before(sim, s), La, v);
-#pragma unroll
-      for (int d = 0; d < SND; ++d) {
-        tv[d] += f_of(La, ch.D[d]);
-        tv[SND + d] += v.nf[d];
-        tv[2 * SND + d] += v.f[d];
-      }
-      tv[3 * SND] += La - sim_J(s);
+      const uint32_t nx = __ldg(next + e);
+      La = sim_La(s);
+      Lb = L_before(sim, s);
+      scanrec[e] = uint64_t(nx) | (uint64_t(La) << 32);
+      sa += La - sim_J(s);
+      atomicAdd(&ha[La], 1u);
+      if (nx == TLRU_NONE) atomicAdd(&hl[La], 1u);
     }
-    const Prefix8 agg = BRp(tmp).Reduce(v, SatAdd());
-    if (threadIdx.x == 0) blockagg[blk] = agg;
+    for (uint32_t d = 0; d < nd; ++d) {  // growth of NF_all for D[d]; <= 256 * 65535: no overflow
+      const uint32_t v = __reduce_add_sync(0xFFFFFFFFu, nf_of(La, Ds[d]) - nf_of(Lb, Ds[d]));
+      if (lane == 0) wsum[warp][d] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < nd) {
+      uint32_t v = 0;
+#pragma unroll
+      for (int w = 0; w < S_THREADS / 32; ++w) v += wsum[w][threadIdx.x];
+      blockagg[uint64_t(blk) * SND + threadIdx.x] = v;
+    }
     __syncthreads();
   }
-  // totals: warp shuffles, then one atomic per value per CTA
-#pragma unroll
-  for (int k = 0; k < NTOT; ++k) {
-    unsigned long long x = tv[k];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xFFFFFFFFu, x, o);
-    if ((threadIdx.x & 31) == 0) part[threadIdx.x / 32][k] = x;
+  if (smem_hist) {
+    for (uint32_t k = threadIdx.x; k < bins; k += S_THREADS) {
+      if (sh[k]) atomicAdd(&hist_all[k], sh[k]);
+      if (sh[bins + k]) atomicAdd(&hist_last[k], sh[bins + k]);
+    }
   }
-  __syncthreads();
-  if (threadIdx.x < NTOT) {
-    unsigned long long x = 0;
 #pragma unroll
-    for (int w = 0; w < S_THREADS / 32; ++w) x += part[w][threadIdx.x];
-    const int k = threadIdx.x;
-    unsigned long long* dst = k < SND ? &totals->sumF[k] : k < 2 * SND ? &totals->nfE[k - SND]
-                              : k < 3 * SND ? &totals->fE[k - 2 * SND] : &totals->suma;
-    if (x) atomicAdd(dst, x);
-  }
+  for (int o = 16; o > 0; o >>= 1) sa += __shfl_xor_sync(0xFFFFFFFFu, sa, o);
+  if (lane == 0 && sa) atomicAdd(&totals->suma, sa);
 }
 
-// s1b: one CTA turns block aggregates into exclusive block prefixes, 256 blocks at a time,
-// and stops at the first block whose prefix already reaches every D's largest capacity
-// (NF_all is non-decreasing, so from there on no free block is ever cached: s2 treats
-// those blocks as saturated).
-__global__ void __launch_bounds__(S_THREADS) s1_scan_kernel(Prefix8* blockagg, uint32_t nblocks,
-                                                            const ChunkDev* __restrict__ chunk, ChunkTotals* totals) {
-  typedef cub::BlockScan<Prefix8, S_THREADS> BS;
-  __shared__ typename BS::TempStorage tmp;
-  __shared__ Prefix8 carry;
-  __shared__ int stop;
-  const SatAdd add;
-  if (threadIdx.x == 0) {
-    carry = Prefix8{};
-    stop = 0;
-  }
-  __syncthreads();
-  uint32_t base = 0;
-  for (; base < nblocks; base += S_THREADS) {
-    const uint32_t i = base + threadIdx.x;
-    Prefix8 v{};
-    if (i < nblocks) v = blockagg[i];
-    Prefix8 ex, agg;
-    BS(tmp).ExclusiveScan(v, ex, Prefix8{}, add, agg);
-    const Prefix8 c = carry;
-    if (i < nblocks) blockagg[i] = add(c, ex);
+// One CTA: exact totals per D from the L_after histograms; then, one warp per D, the block
+// prefixes of NF_all(D) (in place, exclusive) up to nsat[d] = the first block whose prefix
+// reaches Cmax[d] (NF_all is non-decreasing, so no free block of that D is cached after it).
+constexpr int T_THREADS = 32 * SND;
+
+__global__ void __launch_bounds__(T_THREADS) s1_totals_kernel(const ChunkDev* __restrict__ chunk, uint32_t bins,
+                                                              const uint32_t* __restrict__ hist_all,
+                                                              const uint32_t* __restrict__ hist_last,
+                                                              uint32_t* __restrict__ blockagg, uint32_t nblocks,
+                                                              ChunkTotals* totals) {
+  typedef cub::BlockReduce<unsigned long long, T_THREADS> BR;
+  __shared__ typename BR::TempStorage red;
+  __shared__ uint32_t ns_s[SND];
+  const ChunkDev& ch = *chunk;
+  for (int d = 0; d < SND; ++d) {
+    const uint32_t D = ch.D[d];
+    unsigned long long sF = 0, nE = 0, fE = 0;
+    for (uint32_t L = threadIdx.x; L < bins; L += T_THREADS) {
+      const unsigned long long a = hist_all[L], l = hist_last[L];
+      sF += a * f_of(L, D);
+      nE += l * nf_of(L, D);
+      fE += l * f_of(L, D);
+    }
+    sF = BR(red).Sum(sF);
+    __syncthreads();
+    nE = BR(red).Sum(nE);
+    __syncthreads();
+    fE = BR(red).Sum(fE);
     __syncthreads();
     if (threadIdx.x == 0) {
-      carry = add(c, agg);
-      bool sat = true;
-      for (int d = 0; d < SND; ++d) sat &= carry.nf[d] >= chunk->Cmax[d];
-      stop = sat;
-    }
-    __syncthreads();
-    if (stop) {
-      base += S_THREADS;
-      break;
+      totals->sumF[d] = sF;
+      totals->nfE[d] = nE;
+      totals->fE[d] = fE;
     }
   }
-  if (threadIdx.x == 0) totals->nsat = min(base, nblocks);
+  const uint32_t d = threadIdx.x / 32, lane = threadIdx.x & 31;
+  uint32_t nsat = 0;
+  if (d < ch.nd) {
+    const unsigned long long cmax = ch.Cmax[d];
+    unsigned long long carry = 0;
+    nsat = nblocks;
+    for (uint32_t base = 0; base < nblocks; base += 32) {
+      const uint32_t i = base + lane;
+      const unsigned long long v = i < nblocks ? blockagg[uint64_t(i) * SND + d] : 0ull;
+      unsigned long long inc = v;  // warp inclusive scan
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long y = __shfl_up_sync(0xFFFFFFFFu, inc, o);
+        if (lane >= o) inc += y;
+      }
+      const unsigned long long start = carry + inc - v;  // NF_all(D[d]) at the first event of block i
+      const unsigned hit = __ballot_sync(0xFFFFFFFFu, i < nblocks && start >= cmax);
+      if (i < nblocks) blockagg[uint64_t(i) * SND + d] = static_cast<uint32_t>(start < 0xFFFFFFFFull ? start
+                                                                                                    : 0xFFFFFFFFull);
+      if (hit) {
+        nsat = base + __ffs(hit) - 1;
+        break;
+      }
+      carry += __shfl_sync(0xFFFFFFFFu, inc, 31);
+    }
+  }
+  if (lane == 0 && d < SND) ns_s[d] = d < ch.nd ? nsat : 0u;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t lo = nblocks, hi = 0;
+    for (uint32_t k = 0; k < ch.nd; ++k) {
+      totals->nsat[k] = ns_s[k];
+      lo = min(lo, ns_s[k]);
+      hi = max(hi, ns_s[k]);
+    }
+    for (uint32_t k = ch.nd; k < SND; ++k) totals->nsat[k] = 0;
+    totals->nsat_min = ch.nd ? lo : 0u;
+    totals->nsat_max = hi;
+  }
 }
 
-// s2: one CTA = 256 consecutive request events.
-//   A. natural order: event record, L_before, universe deltas -> block scan + block prefix
-//      = NF_all(e), F_all(e) (saturated past nsat); window (p, e) split into chunks of
-//      WCH events, numbered by a block scan;
-//   B. the CTA's chunks are spread over all 256 threads (balanced): each chunk is scanned
-//      backwards, branch-free, summing L and max(L, D) for D pairs in packed 16x2 registers
-//      (exact: wch * max(L_after, D) < 2^16), then merged into per-event shared-memory
-//      totals A_nf, A_f;
-//   C. natural order again: b for every instance, instances grouped by D, coalesced stores.
-
-constexpr uint32_t IT = 512;  // instance-table tile staged in shared memory by s2
-
-template <int ND>
-__global__ void __launch_bounds__(S_THREADS, 4) s2_main_kernel(const uint64_t* __restrict__ sim,
-                                                            const uint64_t* __restrict__ scanrec, uint32_t E,
-                                                            const ChunkDev* __restrict__ chunk,
-                                                            const StackInstDev* __restrict__ insts,
-                                                            const Prefix8* __restrict__ blockpre,
-                                                            const ChunkTotals* __restrict__ totals, uint32_t wch,
-                                                            uint32_t maxL, uint16_t* __restrict__ bout,
-                                                            unsigned long long* sumXf) {
-  constexpr int NP = (ND + 1) / 2;  // D pairs
-  typedef cub::BlockScan<Prefix8, S_THREADS> BS;
-  typedef cub::BlockScan<uint32_t, S_THREADS> BSu;
-  __shared__ ChunkDev ch;
-  struct InstTile {  // phase C instance-table tile (reuses the scan storage)
-    uint64_t off[IT];
-    uint32_t C[IT], inst[IT];
-  };
-  __shared__ union {
-    typename BS::TempStorage scan;
-    typename BSu::TempStorage scanu;
-    InstTile it;
-  } tmp;
-  __shared__ uint32_t anf_s[ND][S_THREADS], af_s[ND][S_THREADS];
-  __shared__ uint32_t p_s[S_THREADS], cbeg_s[S_THREADS + 1];
-  __shared__ uint32_t J_s[S_THREADS], Lb_s[S_THREADS];
-  __shared__ uint32_t nfall_s[ND][S_THREADS];
-  if (threadIdx.x == 0) ch = *chunk;
-  const uint32_t t = threadIdx.x;
-#pragma unroll
-  for (int d = 0; d < ND; ++d) anf_s[d][t] = af_s[d][t] = 0;
-  __syncthreads();
-  const uint32_t e0 = blockIdx.x * S_THREADS;
-  const uint32_t e = e0 + t;
-  uint64_t s = 0;
-  uint32_t Lb = 0;
-  Prefix8 v{};
-  if (e < E) {
-    s = __ldg(sim + e);
-    Lb = L_before(sim, s);
-    universe_delta(ch, Lb, sim_La(s), v);
-  }
-  // ---- A
-  Prefix8 P;
-  if (blockIdx.x < totals->nsat) {
-    Prefix8 ex;
-    BS(tmp.scan).ExclusiveScan(v, ex, Prefix8{}, SatAdd());
-    P = SatAdd()(blockpre[blockIdx.x], ex);
-  } else {
-#pragma unroll
-    for (int d = 0; d < SND; ++d) P.nf[d] = P.f[d] = 0xFFFFFFFFu;
-  }
-  const uint32_t p = (e < E) ? sim_prev(s) : TLRU_NONE;
-  p_s[t] = p;
-  J_s[t] = sim_J(s);
-  Lb_s[t] = (p == TLRU_NONE) ? 0u : Lb;
-#pragma unroll
-  for (int d = 0; d < ND; ++d) nfall_s[d][t] = P.nf[d];
-  const uint32_t wl = (p == TLRU_NONE) ? 0u : e - p - 1;
-  uint32_t cb, ntot;
-  __syncthreads();
-  BSu(tmp.scanu).ExclusiveSum((wl + wch - 1) / wch, cb, ntot);
-  cbeg_s[t] = cb;
-  if (t == 0) cbeg_s[S_THREADS] = ntot;
-  __syncthreads();
-  // ---- B
-  // window sums only see L <= maxL, so D can be clamped to maxL (<= 65535): max(L - D, 0) and
-  // min(L, D) are unchanged for every L in the trace
-  uint32_t Deff[ND], Dpk[NP];
-#pragma unroll
-  for (int d = 0; d < ND; ++d) Deff[d] = min(ch.D[d], maxL);
+// ----------------------------------------------------------------------------- s2 common
+// Phase B of both s2 kernels: each thread takes window chunks `it` of the block and
+// accumulates, branch-free, sum L and sum max(L, Deff) per D pair over the chunk.
+template <int ND, bool WITH_F>
+__device__ __forceinline__ void window_phase(const uint64_t* __restrict__ scanrec, uint32_t e0, uint32_t wch,
+                                             const uint32_t* p_s, const uint32_t* cbeg_s, uint32_t ntot,
+                                             const uint32_t* Deff, uint32_t (*anf_s)[S_THREADS],
+                                             uint32_t (*af_s)[S_THREADS]) {
+  constexpr int NP = (ND + 1) / 2;
+  uint32_t Dpk[NP];
 #pragma unroll
   for (int q = 0; q < NP; ++q) Dpk[q] = Deff[2 * q] | (Deff[min(2 * q + 1, ND - 1)] << 16);
-  for (uint32_t it = t; it < ntot; it += S_THREADS) {
+  for (uint32_t it = threadIdx.x; it < ntot; it += S_THREADS) {
     uint32_t lo = 0, hi = S_THREADS;  // owner event: last j with cbeg_s[j] <= it
     while (hi - lo > 1) {
       const uint32_t mid = (lo + hi) >> 1;
       if (cbeg_s[mid] <= it) lo = mid; else hi = mid;
     }
     const uint32_t j = lo, ej = e0 + j, pj = p_s[j];
-    const uint32_t top = ej - 1 - (it - cbeg_s[j]) * wch;          // chunk covers [bot, top]
+    const uint32_t top = ej - 1 - (it - cbeg_s[j]) * wch;  // chunk covers [bot, top]
     const uint32_t bot = max(pj + 1, top >= wch - 1 ? top - (wch - 1) : 0u);
-    // Branch-free: a dead element (its conversation returns before ej) counts as L = 0.
-    // Per D pair accumulate sum max(L, D) (16x2); with n = elements in the chunk:
+    // a dead element (its conversation returns before ej) counts as L = 0; with n elements:
     //   A_nf = sum max(L, D) - n D,   A_f = sum L + n D - sum max(L, D)   (max + min = L + D)
     uint32_t mx2[NP], sumL = 0;
 #pragma unroll
@@ -305,7 +245,7 @@ __global__ void __launch_bounds__(S_THREADS, 4) s2_main_kernel(const uint64_t* _
     for (uint32_t x = top + 1; x-- > bot;) {
       const uint64_t r = __ldg(scanrec + x);
       const uint32_t L = static_cast<uint32_t>(r) > ej ? static_cast<uint32_t>(r >> 32) : 0u;
-      sumL += L;
+      if (WITH_F) sumL += L;
       const uint32_t L2 = L * 0x10001u;  // L in both 16-bit halves
 #pragma unroll
       for (int q = 0; q < NP; ++q) mx2[q] = __vadd2(mx2[q], __vmaxu2(L2, Dpk[q]));
@@ -320,92 +260,263 @@ __global__ void __launch_bounds__(S_THREADS, 4) s2_main_kernel(const uint64_t* _
           const uint32_t smax = h ? (mx2[q] >> 16) : (mx2[q] & 0xFFFFu);
           const uint32_t nD = n * Deff[d];
           atomicAdd(&anf_s[d][j], smax - nD);
-          atomicAdd(&af_s[d][j], sumL + nD - smax);
-        }
-      }
-    }
-  }
-  __syncthreads();
-  // ---- C: per-instance b (P:154-156 with the closed form of X_theta).  Thread t writes 4
-  // consecutive events (one 8-byte store when the instance row is 8-byte aligned) for every
-  // fourth instance of each D.
-  const uint32_t quad = t & 63, lane4 = t >> 6;
-  const uint32_t j0 = quad * 4;
-  const bool full = e0 + j0 + 3 < E;
-  const bool saturated = blockIdx.x >= totals->nsat;  // NF_all >= every C here: no free blocks cached
-  uint32_t Jv[4];
-#pragma unroll
-  for (int u = 0; u < 4; ++u) Jv[u] = J_s[j0 + u];
-  const uint32_t J01 = Jv[0] | (Jv[1] << 16), J23 = Jv[2] | (Jv[3] << 16);
-  // The chunk's instance table goes through shared memory in tiles of IT entries.
-  for (uint32_t tb = 0; tb < ch.ninst; tb += IT) {
-    const uint32_t te = min(ch.ninst, tb + IT);
-    __syncthreads();
-    for (uint32_t k = tb + t; k < te; k += S_THREADS) {
-      const StackInstDev in = insts[ch.inst0 + k];
-      tmp.it.C[k - tb] = in.C;
-      tmp.it.inst[k - tb] = in.inst;
-      tmp.it.off[k - tb] = in.boff;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int d = 0; d < ND; ++d) {
-      const uint32_t kb = max(ch.dbeg[d], tb), ke = min(ch.dbeg[d + 1], te);
-      if (kb >= ke) continue;
-      uint32_t nfb[4], fb[4], anf[4], af[4], nfa[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const bool hit = p_s[j0 + u] != TLRU_NONE;
-        const uint32_t Lbu = Lb_s[j0 + u];
-        nfb[u] = hit ? nf_of(Lbu, ch.D[d]) : 0u;
-        fb[u] = hit ? f_of(Lbu, ch.D[d]) : 0u;
-        anf[u] = anf_s[d][j0 + u];
-        af[u] = af_s[d][j0 + u];
-        nfa[u] = nfall_s[d][j0 + u];
-      }
-      // packed 16x2 operands for capacities <= 65535: X = min(nfb, max(C, A) - A) with A = A_nf
-      // clamped to 65535 (exact: if A > 65535 >= C then both sides give 0)
-      const uint32_t A01 = min(anf[0], 65535u) | (min(anf[1], 65535u) << 16);
-      const uint32_t A23 = min(anf[2], 65535u) | (min(anf[3], 65535u) << 16);
-      const uint32_t N01 = nfb[0] | (nfb[1] << 16), N23 = nfb[2] | (nfb[3] << 16);
-#pragma unroll 4
-      for (uint32_t k = kb + lane4; k < ke; k += 4) {
-        const uint32_t C = tmp.it.C[k - tb];
-        uint32_t w01, w23;
-        if (saturated && C <= 65535u) {
-          const uint32_t C2 = C * 0x10001u;
-          w01 = __vsub2(J01, __vminu2(N01, __vsub2(__vmaxu2(C2, A01), A01)));
-          w23 = __vsub2(J23, __vminu2(N23, __vsub2(__vmaxu2(C2, A23), A23)));
-        } else {
-          uint32_t b[4];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            uint32_t X = min(nfb[u], sat_sub(C, anf[u]));
-            if (!saturated && nfa[u] < C && fb[u] > 0) {  // warm-up: free blocks can still be cached
-              const uint32_t xf = min(fb[u], sat_sub(sat_sub(C, nfa[u]), af[u]));
-              X += xf;
-              if (xf && e0 + j0 + u < E)
-                atomicAdd(&sumXf[tmp.it.inst[k - tb]], static_cast<unsigned long long>(xf));
-            }
-            b[u] = Jv[u] - X;
-          }
-          w01 = b[0] | (b[1] << 16);
-          w23 = b[2] | (b[3] << 16);
-        }
-        uint16_t* row = bout + tmp.it.off[k - tb] + e0 + j0;
-        if (full && ((reinterpret_cast<uintptr_t>(row) & 7u) == 0)) {
-          *reinterpret_cast<uint2*>(row) = make_uint2(w01, w23);
-        } else {
-          const uint32_t bb[4] = {w01 & 0xFFFFu, w01 >> 16, w23 & 0xFFFFu, w23 >> 16};
-#pragma unroll
-          for (int u = 0; u < 4; ++u)
-            if (e0 + j0 + u < E) row[u] = static_cast<uint16_t>(bb[u]);
+          if (WITH_F) atomicAdd(&af_s[d][j], sumL + nD - smax);
         }
       }
     }
   }
 }
 
+// Phase A shared by both s2 kernels: event record, L_before, window length -> chunk numbering.
+__device__ __forceinline__ uint32_t block_setup(const uint64_t* __restrict__ sim, uint32_t E, uint32_t e0,
+                                                uint32_t wch, uint32_t* p_s, uint32_t* J_s, uint32_t* Lb_s,
+                                                uint32_t* cbeg_s, uint32_t& Lb_out, uint64_t& s_out,
+                                                typename cub::BlockScan<uint32_t, S_THREADS>::TempStorage& tmp) {
+  const uint32_t t = threadIdx.x, e = e0 + t;
+  uint64_t s = 0;
+  uint32_t Lb = 0;
+  if (e < E) {
+    s = __ldg(sim + e);
+    Lb = L_before(sim, s);
+  }
+  const uint32_t p = (e < E) ? sim_prev(s) : TLRU_NONE;
+  p_s[t] = p;
+  J_s[t] = sim_J(s);
+  Lb_s[t] = Lb;
+  const uint32_t wl = (p == TLRU_NONE) ? 0u : e - p - 1;
+  uint32_t cb, ntot;
+  cub::BlockScan<uint32_t, S_THREADS>(tmp).ExclusiveSum((wl + wch - 1) / wch, cb, ntot);
+  cbeg_s[t] = cb;
+  if (t == 0) cbeg_s[S_THREADS] = ntot;
+  Lb_out = Lb;
+  s_out = s;
+  return ntot;
+}
+
+__device__ __forceinline__ void store4(uint16_t* row, bool full, uint32_t w01, uint32_t w23, uint32_t e_first,
+                                       uint32_t E) {
+  if (full && ((reinterpret_cast<uintptr_t>(row) & 7u) == 0)) {
+    *reinterpret_cast<uint2*>(row) = make_uint2(w01, w23);
+  } else {
+    const uint32_t bb[4] = {w01 & 0xFFFFu, w01 >> 16, w23 & 0xFFFFu, w23 >> 16};
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (e_first + u < E) row[u] = static_cast<uint16_t>(bb[u]);
+  }
+}
+
+struct InstTile {
+  uint64_t off[IT];
+  uint32_t C[IT];  // C * 0x10001 (both 16-bit halves) on the packed path, C on the big-C path
+};
+
+struct InstTileW {
+  uint64_t off[IT];
+  uint32_t C[IT], inst[IT];
+};
+
+// ----------------------------------------------------------------------------- s2_sat
+template <int ND>
+__global__ void __launch_bounds__(S_THREADS, 4) s2_sat_kernel(const uint64_t* __restrict__ sim,
+                                                              const uint64_t* __restrict__ scanrec, uint32_t E,
+                                                              const ChunkDev* __restrict__ chunk,
+                                                              const StackInstDev* __restrict__ insts,
+                                                              const ChunkTotals* __restrict__ totals, uint32_t wch,
+                                                              uint32_t maxL, bool aligned,
+                                                              uint16_t* __restrict__ bout) {
+  typedef cub::BlockScan<uint32_t, S_THREADS> BSu;
+  __shared__ ChunkDev ch;
+  __shared__ union {
+    typename BSu::TempStorage scan;
+    InstTile it;
+  } tmp;
+  __shared__ uint32_t anf_s[ND][S_THREADS];
+  __shared__ uint32_t p_s[S_THREADS], cbeg_s[S_THREADS + 1], J_s[S_THREADS], Lb_s[S_THREADS];
+  if (blockIdx.x < totals->nsat_min) return;  // no D is saturated yet: s2_warm owns the block
+  __shared__ uint32_t nsat_s[SND];
+  if (threadIdx.x < SND) nsat_s[threadIdx.x] = totals->nsat[threadIdx.x];
+  const uint32_t t = threadIdx.x;
+  if (t == 0) ch = *chunk;
+#pragma unroll
+  for (int d = 0; d < ND; ++d) anf_s[d][t] = 0;
+  const uint32_t e0 = blockIdx.x * S_THREADS;
+  uint32_t Lb;
+  uint64_t s;
+  const uint32_t ntot = block_setup(sim, E, e0, wch, p_s, J_s, Lb_s, cbeg_s, Lb, s, tmp.scan);
+  __syncthreads();
+  // window sums only see L <= maxL, so D can be clamped to maxL (<= 65535): max(L - D, 0) and
+  // min(L, D) are unchanged for every L in the trace
+  uint32_t Deff[ND];
+#pragma unroll
+  for (int d = 0; d < ND; ++d) Deff[d] = min(ch.D[d], maxL);
+  window_phase<ND, false>(scanrec, e0, wch, p_s, cbeg_s, ntot, Deff, anf_s, nullptr);
+  // ---- C: per-instance b; X = min(NF(Lb), (C - A_nf)^+) (no free block is cached here)
+  const uint32_t quad = t & 63, lane4 = t >> 6;
+  const uint32_t j0 = quad * 4;
+  const bool full = e0 + j0 + 3 < E;
+  uint32_t Jv[4];
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < 4; ++u) Jv[u] = J_s[j0 + u];
+  const uint32_t J01 = Jv[0] | (Jv[1] << 16), J23 = Jv[2] | (Jv[3] << 16);
+  constexpr uint32_t j0_base = 0;  // tile offsets already include e0; each thread adds its j0
+  const uint32_t joff = j0;
+  const bool vec = full && aligned;  // every instance row offset is a multiple of 4 requests
+  for (uint32_t tb = 0; tb < ch.ninst; tb += IT) {
+    const uint32_t te = min(ch.ninst, tb + IT);
+    __syncthreads();
+    for (uint32_t k = tb + t; k < te; k += S_THREADS) {
+      const StackInstDev in = insts[ch.inst0 + k];
+      tmp.it.C[k - tb] = in.C <= 65535u ? in.C * 0x10001u : in.C;
+      tmp.it.off[k - tb] = in.boff + e0 + j0_base;
+    }
+    __syncthreads();
+#pragma unroll 1
+    for (int d = 0; d < ND; ++d) {  // runtime loop: a fully unrolled one overflows the instruction cache
+      const uint32_t kb = max(ch.dbeg[d], tb), ke = min(ch.dbeg[d + 1], te);
+      if (kb >= ke || blockIdx.x < nsat_s[d]) continue;  // D[d] still in warm-up here: s2_warm
+      uint32_t nfb[4], anf[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        nfb[u] = p_s[j0 + u] != TLRU_NONE ? nf_of(Lb_s[j0 + u], ch.D[d]) : 0u;
+        anf[u] = anf_s[d][j0 + u];
+      }
+      // packed 16x2: X = min(nfb, max(C, A) - A), A clamped to 65535 (exact for C <= 65535)
+      const uint32_t A01 = min(anf[0], 65535u) | (min(anf[1], 65535u) << 16);
+      const uint32_t A23 = min(anf[2], 65535u) | (min(anf[3], 65535u) << 16);
+      const uint32_t N01 = nfb[0] | (nfb[1] << 16), N23 = nfb[2] | (nfb[3] << 16);
+      const uint32_t kmid = min(max(ch.dbig[d], kb), ke);
+      if (vec) {
+#pragma unroll 4
+        for (uint32_t k = kb + lane4; k < kmid; k += 4) {
+          const uint32_t C2 = tmp.it.C[k - tb];
+          const uint32_t w01 = __vsub2(J01, __vminu2(N01, __vsub2(__vmaxu2(C2, A01), A01)));
+          const uint32_t w23 = __vsub2(J23, __vminu2(N23, __vsub2(__vmaxu2(C2, A23), A23)));
+          *reinterpret_cast<uint2*>(bout + tmp.it.off[k - tb] + joff) = make_uint2(w01, w23);
+        }
+      } else {
+        for (uint32_t k = kb + lane4; k < kmid; k += 4) {
+          const uint32_t C2 = tmp.it.C[k - tb];
+          const uint32_t w01 = __vsub2(J01, __vminu2(N01, __vsub2(__vmaxu2(C2, A01), A01)));
+          const uint32_t w23 = __vsub2(J23, __vminu2(N23, __vsub2(__vmaxu2(C2, A23), A23)));
+          store4(bout + tmp.it.off[k - tb] + joff, false, w01, w23, e0 + j0, E);
+        }
+      }
+      for (uint32_t k = max(kmid, kb) + ((lane4 + 4 - (max(kmid, kb) - kb) % 4) % 4); k < ke; k += 4) {
+        const uint32_t C = tmp.it.C[k - tb];  // capacities above 65535: 32-bit arithmetic
+        uint32_t b[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) b[u] = Jv[u] - min(nfb[u], sat_sub(C, anf[u]));
+        store4(bout + tmp.it.off[k - tb] + joff, full && aligned, b[0] | (b[1] << 16), b[2] | (b[3] << 16),
+               e0 + j0, E);
+      }
+    }
+  }
+}
+
+// ----------------------------------------------------------------------------- s2_warm
+// Blocks before nsat: exact NF_all(e) per D (sum of the universe deltas of every earlier event)
+// and the free-block term.  Few blocks, so this kernel favours simplicity; dynamic shared memory.
+template <int ND>
+__global__ void __launch_bounds__(S_THREADS) s2_warm_kernel(const uint64_t* __restrict__ sim,
+                                                            const uint64_t* __restrict__ scanrec, uint32_t E,
+                                                            const ChunkDev* __restrict__ chunk,
+                                                            const StackInstDev* __restrict__ insts,
+                                                            const ChunkTotals* __restrict__ totals,
+                                                            const uint32_t* __restrict__ blockpre, uint32_t wch,
+                                                            uint32_t maxL, uint16_t* __restrict__ bout,
+                                                            unsigned long long* sumXf) {
+  typedef cub::BlockScan<uint32_t, S_THREADS> BSu;
+  extern __shared__ uint32_t dyn[];
+  uint32_t(*anf_s)[S_THREADS] = reinterpret_cast<uint32_t(*)[S_THREADS]>(dyn);
+  uint32_t(*af_s)[S_THREADS] = reinterpret_cast<uint32_t(*)[S_THREADS]>(dyn + ND * S_THREADS);
+  uint32_t(*nfall_s)[S_THREADS] = reinterpret_cast<uint32_t(*)[S_THREADS]>(dyn + 2 * ND * S_THREADS);
+  __shared__ ChunkDev ch;
+  __shared__ typename BSu::TempStorage scan;
+  __shared__ uint32_t p_s[S_THREADS], cbeg_s[S_THREADS + 1], J_s[S_THREADS], Lb_s[S_THREADS];
+  __shared__ uint32_t nsat_s[SND];
+  __shared__ InstTileW itile;
+  const uint32_t t = threadIdx.x;
+  if (t == 0) ch = *chunk;
+  if (t < SND) nsat_s[t] = totals->nsat[t];
+  const uint32_t nwarm = totals->nsat_max;  // blocks from nsat_max on are saturated for every D: s2_sat
+  __syncthreads();
+  for (uint32_t blk = blockIdx.x; blk < nwarm; blk += gridDim.x) {  // small persistent grid
+    for (int d = 0; d < ND; ++d) anf_s[d][t] = af_s[d][t] = 0;
+    const uint32_t e0 = blk * S_THREADS;
+    uint32_t Lb;
+    uint64_t s;
+    const uint32_t ntot = block_setup(sim, E, e0, wch, p_s, J_s, Lb_s, cbeg_s, Lb, s, scan);
+    __syncthreads();
+    // NF_all(D[d]) at e: the block prefix from s1_totals plus the block's own exclusive scan
+    const uint32_t La_t = sim_La(s);
+#pragma unroll 1
+    for (int d = 0; d < ND; ++d) {
+      if (blk >= nsat_s[d] || d >= static_cast<int>(ch.nd)) continue;  // uniform across the block
+      const uint32_t delta = (e0 + t < E) ? nf_of(La_t, ch.D[d]) - nf_of(Lb, ch.D[d]) : 0u;
+      uint32_t ex;
+      BSu(scan).ExclusiveSum(delta, ex);
+      nfall_s[d][t] = blockpre[uint64_t(blk) * SND + d] + ex;  // < Cmax[d] + 256 * 65535
+      __syncthreads();
+    }
+    uint32_t Deff[ND];
+#pragma unroll
+    for (int d = 0; d < ND; ++d) Deff[d] = min(ch.D[d], maxL);
+    window_phase<ND, true>(scanrec, e0, wch, p_s, cbeg_s, ntot, Deff, anf_s, af_s);
+    __syncthreads();
+    // phase C for the D values still in warm-up: 4 events per thread, instance stride 4, the
+    // instance table staged in shared memory (as in s2_sat), general formula with free blocks
+    const uint32_t quad = t & 63, lane4 = t >> 6, j0 = quad * 4;
+    const bool full = e0 + j0 + 3 < E;
+    for (uint32_t tb = 0; tb < ch.ninst; tb += IT) {
+      const uint32_t te = min(ch.ninst, tb + IT);
+      __syncthreads();
+      for (uint32_t k = tb + t; k < te; k += S_THREADS) {
+        const StackInstDev in = insts[ch.inst0 + k];
+        itile.C[k - tb] = in.C;
+        itile.off[k - tb] = in.boff;
+        itile.inst[k - tb] = in.inst;
+      }
+      __syncthreads();
+#pragma unroll 1
+      for (int d = 0; d < ND; ++d) {
+        const uint32_t kb = max(ch.dbeg[d], tb), ke = min(ch.dbeg[d + 1], te);
+        if (kb >= ke || blk >= nsat_s[d]) continue;  // saturated: s2_sat writes these instances
+        uint32_t nfb[4], fb[4], anf[4], af[4], nfa[4], Jv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const bool hit = p_s[j0 + u] != TLRU_NONE;
+          nfb[u] = hit ? nf_of(Lb_s[j0 + u], ch.D[d]) : 0u;
+          fb[u] = hit ? f_of(Lb_s[j0 + u], ch.D[d]) : 0u;
+          anf[u] = anf_s[d][j0 + u];
+          af[u] = af_s[d][j0 + u];
+          nfa[u] = nfall_s[d][j0 + u];
+          Jv[u] = J_s[j0 + u];
+        }
+        for (uint32_t k = kb + lane4; k < ke; k += 4) {
+          const uint32_t C = itile.C[k - tb];
+          uint32_t b[4];
+          unsigned long long xfs = 0;
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            uint32_t X = min(nfb[u], sat_sub(C, anf[u]));
+            if (nfa[u] < C && fb[u] > 0 && e0 + j0 + u < E) {  // free blocks can still be cached
+              const uint32_t xf = min(fb[u], sat_sub(sat_sub(C, nfa[u]), af[u]));
+              X += xf;
+              xfs += xf;
+            }
+            b[u] = Jv[u] - X;
+          }
+          if (xfs) atomicAdd(&sumXf[itile.inst[k - tb]], xfs);
+          store4(bout + itile.off[k - tb] + e0 + j0, full, b[0] | (b[1] << 16), b[2] | (b[3] << 16), e0 + j0, E);
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ----------------------------------------------------------------------------- s3
 __global__ void s3_results_kernel(const StackInstDev* __restrict__ insts, uint32_t ninst,
                                   const uint32_t* __restrict__ inst_chunk, const ChunkTotals* __restrict__ totals,
                                   const unsigned long long* sumXf, tlru_result* results) {
@@ -427,28 +538,35 @@ __global__ void s3_results_kernel(const StackInstDev* __restrict__ insts, uint32
 }
 
 // ----------------------------------------------------------------------------- host
+static const int kNDs[] = {2, 4, 8, 12, 16, 20, 24};
+
 struct StackPlan {
   struct Chunk {
     uint32_t trace;
+    uint32_t ndk;  // template width
     ChunkDev dev;
   };
   std::vector<Chunk> chunks;
   std::vector<StackInstDev> insts;
   std::vector<uint32_t> inst_chunk;
   uint64_t Emax = 0;
+  uint32_t maxbins = 1;
 };
 
 static void make_stack_plan(const tlru_trace* traces, uint32_t nt, const tlru_instance* inst, uint32_t ni,
                             const uint64_t* boffs, StackPlan* P) {
-  for (uint32_t t = 0; t < nt; ++t) P->Emax = std::max<uint64_t>(P->Emax, traces[t].num_events);
   for (uint32_t t = 0; t < nt; ++t) {
-    std::vector<uint32_t> ids;
-    for (uint32_t i = 0; i < ni; ++i)
-      if (inst[i].trace == t) ids.push_back(i);
+    P->Emax = std::max<uint64_t>(P->Emax, traces[t].num_events);
+    P->maxbins = std::max<uint32_t>(P->maxbins, traces[t].max_history + 1);
+  }
+  std::vector<std::vector<uint32_t>> by_trace(nt);
+  for (uint32_t i = 0; i < ni; ++i) by_trace[inst[i].trace].push_back(i);
+  auto Dof = [&](uint32_t i) {
+    return (inst[i].policy == TLRU_POLICY_TLRU && inst[i].xi > inst[i].q_hat) ? inst[i].xi - inst[i].q_hat : 0u;
+  };
+  for (uint32_t t = 0; t < nt; ++t) {
+    const std::vector<uint32_t>& ids = by_trace[t];
     if (ids.empty() || traces[t].num_events == 0) continue;
-    auto Dof = [&](uint32_t i) {
-      return (inst[i].policy == TLRU_POLICY_TLRU && inst[i].xi > inst[i].q_hat) ? inst[i].xi - inst[i].q_hat : 0u;
-    };
     std::vector<uint32_t> Ds;
     for (uint32_t i : ids) Ds.push_back(Dof(i));
     std::sort(Ds.begin(), Ds.end());
@@ -458,12 +576,25 @@ static void make_stack_plan(const tlru_trace* traces, uint32_t nt, const tlru_in
       ch.trace = t;
       memset(&ch.dev, 0, sizeof(ch.dev));
       ch.dev.nd = static_cast<uint32_t>(std::min<size_t>(SND, Ds.size() - c0));
+      ch.ndk = SND;
+      for (int k : kNDs)
+        if (static_cast<uint32_t>(k) >= ch.dev.nd) {
+          ch.ndk = k;
+          break;
+        }
       for (uint32_t d = 0; d < SND; ++d) ch.dev.D[d] = d < ch.dev.nd ? Ds[c0 + d] : Ds[c0];
       ch.dev.inst0 = static_cast<uint32_t>(P->insts.size());
       for (uint32_t d = 0; d < ch.dev.nd; ++d) {
         ch.dev.dbeg[d] = static_cast<uint32_t>(P->insts.size()) - ch.dev.inst0;
-        for (uint32_t i : ids) {
-          if (Dof(i) != ch.dev.D[d]) continue;
+        std::vector<uint32_t> mine;
+        for (uint32_t i : ids)
+          if (Dof(i) == ch.dev.D[d]) mine.push_back(i);
+        std::stable_sort(mine.begin(), mine.end(), [&](uint32_t a, uint32_t b) {
+          return std::min<uint32_t>(inst[a].capacity, 0x7FFF0000u) < std::min<uint32_t>(inst[b].capacity, 0x7FFF0000u);
+        });
+        ch.dev.dbig[d] = ch.dev.dbeg[d];
+        for (uint32_t i : mine) {
+          if (std::min<uint32_t>(inst[i].capacity, 0x7FFF0000u) <= 65535u) ++ch.dev.dbig[d];
           StackInstDev s;
           s.C = std::min<uint32_t>(inst[i].capacity, 0x7FFF0000u);
           s.d = d;
@@ -488,9 +619,9 @@ struct StackWs {
   uint32_t* inst_chunk;
   ChunkTotals* totals;
   unsigned long long* sumXf;
-  Prefix8* blockpre;  // [chunk][block] exclusive block prefixes
-  uint64_t* scanrec;  // [event] next | L_after << 32 of the trace being processed
-  uint64_t nblocks_max;
+  uint32_t* blockagg;  // [block][SND] growth of NF_all per D, then block prefixes; reused per chunk
+  uint32_t* hist;      // [2][maxbins] L_after histograms, reused per chunk
+  uint64_t* scanrec;   // [event] next | L_after << 32 of the trace being processed
 };
 
 static void carve_stack(Carver& cv, const StackPlan& P, uint32_t ni, StackWs* w) {
@@ -500,8 +631,8 @@ static void carve_stack(Carver& cv, const StackPlan& P, uint32_t ni, StackWs* w)
   w->inst_chunk = cv.take<uint32_t>(P.insts.size() + 1);
   w->totals = cv.take<ChunkTotals>(nc);
   w->sumXf = cv.take<unsigned long long>(ni + 1);
-  w->nblocks_max = (P.Emax + S_THREADS - 1) / S_THREADS + 1;
-  w->blockpre = cv.take<Prefix8>(nc * w->nblocks_max);
+  w->blockagg = cv.take<uint32_t>(((P.Emax + S_THREADS - 1) / S_THREADS + 1) * SND);
+  w->hist = cv.take<uint32_t>(2 * uint64_t(P.maxbins));
   w->scanrec = cv.take<uint64_t>(P.Emax + 1);
 }
 
@@ -518,15 +649,22 @@ tlru_status stack_workspace(const tlru_trace* traces, uint32_t nt, const tlru_in
 }
 
 template <int ND>
-static void launch_s2(const tlru_trace& tr, const ChunkDev* ch, const ChunkDev& ch_host, const Prefix8* blockpre,
-                      const ChunkTotals* tot, const StackWs& w, uint16_t* bout, cudaStream_t st) {
+static tlru_status launch_s2(const tlru_trace& tr, const ChunkDev* ch, const ChunkTotals* tot, const StackWs& w,
+                             bool aligned, uint16_t* bout, cudaStream_t st) {
   const uint32_t E = static_cast<uint32_t>(tr.num_events);
+  const uint32_t nb = (E + S_THREADS - 1) / S_THREADS;
   // 16x2 partial sums of max(L, min(D, maxL)) stay exact while wch * maxL < 2^16
   const uint32_t maxL = std::max<uint32_t>(tr.max_history, 1u);
-  const uint32_t wch = std::max<uint32_t>(1u, std::min<uint32_t>(64u, 65535u / maxL));
-  (void)ch_host;
-  s2_main_kernel<ND><<<(E + S_THREADS - 1) / S_THREADS, S_THREADS, 0, st>>>(tr.sim, w.scanrec, E, ch, w.insts,
-                                                                            blockpre, tot, wch, maxL, bout, w.sumXf);
+  const uint32_t wch = std::max<uint32_t>(1u, std::min<uint32_t>(WCH_MAX, 65535u / maxL));
+  const size_t warm_smem = size_t(3) * ND * S_THREADS * sizeof(uint32_t);
+  TLRU_CUDA(cudaFuncSetAttribute(s2_warm_kernel<ND>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(warm_smem)));
+  s2_warm_kernel<ND><<<std::min<uint32_t>(nb ? nb : 1, 2u * 148u), S_THREADS, warm_smem, st>>>(
+      tr.sim, w.scanrec, E, ch, w.insts, tot, w.blockagg, wch, maxL, bout, w.sumXf);
+  TLRU_CHECK_LAUNCH();
+  s2_sat_kernel<ND><<<nb, S_THREADS, 0, st>>>(tr.sim, w.scanrec, E, ch, w.insts, tot, wch, maxL, aligned, bout);
+  TLRU_CHECK_LAUNCH();
+  return TLRU_OK;
 }
 
 tlru_status stack_simulate(const tlru_trace* traces, uint32_t nt, const tlru_instance* inst, uint32_t ni,
@@ -551,28 +689,31 @@ tlru_status stack_simulate(const tlru_trace* traces, uint32_t nt, const tlru_ins
   }
   TLRU_CUDA(cudaMemsetAsync(w.totals, 0, (nc + 1) * sizeof(ChunkTotals), st));
   TLRU_CUDA(cudaMemsetAsync(w.sumXf, 0, (ni + 1) * sizeof(unsigned long long), st));
+  // 8-byte b stores need every instance row to start at a multiple of 4 requests (16-byte base)
+  bool aligned = (reinterpret_cast<uintptr_t>(bout) & 7u) == 0;
+  for (const StackInstDev& in : P.insts) aligned &= (in.boff & 3u) == 0;
   for (size_t c = 0; c < nc; ++c) {
     const tlru_trace& tr = traces[P.chunks[c].trace];
     const uint32_t E = static_cast<uint32_t>(tr.num_events);
     const uint32_t nb = (E + S_THREADS - 1) / S_THREADS;
-    Prefix8* bp = w.blockpre + c * w.nblocks_max;
-    s1_block_kernel<<<std::min<uint32_t>(nb ? nb : 1, 148u * 4u), S_THREADS, 0, st>>>(tr.sim, tr.next, E, w.chunks + c,
-                                                                                     w.scanrec, bp, w.totals + c);
+    const uint32_t hb = tr.max_history + 1;
+    TLRU_CUDA(cudaMemsetAsync(w.hist, 0, 2 * size_t(hb) * sizeof(uint32_t), st));
+    const size_t s1_smem = hb <= 8192 ? 2 * size_t(hb) * sizeof(uint32_t) : 0;
+    s1_block_kernel<<<std::min<uint32_t>(nb ? nb : 1, 148u * 4u), S_THREADS, s1_smem, st>>>(
+        tr.sim, tr.next, E, w.chunks + c, w.scanrec, w.blockagg, hb, w.hist, w.hist + hb, w.totals + c);
     TLRU_CHECK_LAUNCH();
-    s1_scan_kernel<<<1, S_THREADS, 0, st>>>(bp, nb, w.chunks + c, w.totals + c);
+    s1_totals_kernel<<<1, T_THREADS, 0, st>>>(w.chunks + c, hb, w.hist, w.hist + hb, w.blockagg, nb, w.totals + c);
     TLRU_CHECK_LAUNCH();
-    switch (P.chunks[c].dev.nd) {
-      case 1: launch_s2<1>(tr, w.chunks + c, P.chunks[c].dev, bp, w.totals + c, w, bout, st); break;
-      case 2: launch_s2<2>(tr, w.chunks + c, P.chunks[c].dev, bp, w.totals + c, w, bout, st); break;
-      case 3: launch_s2<3>(tr, w.chunks + c, P.chunks[c].dev, bp, w.totals + c, w, bout, st); break;
-      case 4: launch_s2<4>(tr, w.chunks + c, P.chunks[c].dev, bp, w.totals + c, w, bout, st); break;
-      case 5: launch_s2<5>(tr, w.chunks + c, P.chunks[c].dev, bp, w.totals + c, w, bout, st); break;
-      case 6: launch_s2<6>(tr, w.chunks + c, P.chunks[c].dev, bp, w.totals + c, w, bout, st); break;
-      case 7: launch_s2<7>(tr, w.chunks + c, P.chunks[c].dev, bp, w.totals + c, w, bout, st); break;
-      default: launch_s2<8>(tr, w.chunks + c, P.chunks[c].dev, bp, w.totals + c, w, bout, st); break;
+    switch (P.chunks[c].ndk) {
+      case 2: TLRU_TRY(launch_s2<2>(tr, w.chunks + c, w.totals + c, w, aligned, bout, st)); break;
+      case 4: TLRU_TRY(launch_s2<4>(tr, w.chunks + c, w.totals + c, w, aligned, bout, st)); break;
+      case 8: TLRU_TRY(launch_s2<8>(tr, w.chunks + c, w.totals + c, w, aligned, bout, st)); break;
+      case 12: TLRU_TRY(launch_s2<12>(tr, w.chunks + c, w.totals + c, w, aligned, bout, st)); break;
+      case 16: TLRU_TRY(launch_s2<16>(tr, w.chunks + c, w.totals + c, w, aligned, bout, st)); break;
+      case 20: TLRU_TRY(launch_s2<20>(tr, w.chunks + c, w.totals + c, w, aligned, bout, st)); break;
+      default: TLRU_TRY(launch_s2<24>(tr, w.chunks + c, w.totals + c, w, aligned, bout, st)); break;
     }
-    TLRU_CHECK_LAUNCH();
-    *nkernels += 3;
+    *nkernels += 4;
   }
   // K3 over b, then the eviction counters from the telescoped identities
   if (ev_mid) TLRU_CUDA(cudaEventRecord(ev_mid, st));
