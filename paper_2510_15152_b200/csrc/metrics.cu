@@ -197,7 +197,9 @@ __global__ void __launch_bounds__(FIN_THREADS) finalize_kernel(const SegDev* seg
 tlru_status launch_hist(const uint16_t* b, const SegDev* segs, uint32_t ns, uint32_t bins, uint32_t* hist,
                         unsigned long long* clamped, cudaStream_t st) {
   if (ns == 0) return TLRU_OK;
-  const unsigned gx = 148u * 4u / (ns < 4 ? 1u : (ns > 148 ? 148u : ns)) + 1u;
+  // at least ~2 waves of 8 resident CTAs per SM over all segments
+  const unsigned target = 148u * 8u * 2u;
+  const unsigned gx = (target + ns - 1) / ns;
   dim3 grid(gx < 1 ? 1 : gx, ns);
   const bool aligned = (reinterpret_cast<uintptr_t>(b) % 16) == 0;
   if (aligned && size_t(bins) * HIST_WARPS * 4 <= SMEM_HIST_BYTES) {
