@@ -46,6 +46,7 @@ constexpr int SND = 24;         // D values per chunk
 constexpr int S_THREADS = 256;  // events per s2 block
 constexpr uint32_t IT = 512;    // instance-table tile staged in shared memory by s2
 constexpr uint32_t WCH_MAX = 64;
+constexpr uint32_t GI_MAX = 64;  // instances per s2_out group
 
 struct ChunkDev {
   uint32_t D[SND];
@@ -516,6 +517,198 @@ __global__ void __launch_bounds__(S_THREADS) s2_warm_kernel(const uint64_t* __re
   }
 }
 
+// ----------------------------------------------------------------------------- s2_win / s2_out (fused K3)
+// s2_win: phases A and B of s2_sat for every block from nsat_min on, writing the window sums
+// A_nf (clamped to AT's range; AT = u16 when every capacity of the chunk is <= 65535) and
+// (L_before | J << 16) per event, so the per-instance work can run instance-group-major.
+template <int ND, typename AT>
+__global__ void __launch_bounds__(S_THREADS, 4) s2_win_kernel(const uint64_t* __restrict__ sim,
+                                                              const uint64_t* __restrict__ scanrec, uint32_t E,
+                                                              const ChunkDev* __restrict__ chunk,
+                                                              const ChunkTotals* __restrict__ totals, uint32_t wch,
+                                                              uint32_t maxL, AT* __restrict__ A, uint32_t Astride,
+                                                              uint32_t* __restrict__ LbJ) {
+  typedef cub::BlockScan<uint32_t, S_THREADS> BSu;
+  __shared__ ChunkDev ch;
+  __shared__ typename BSu::TempStorage scan;
+  __shared__ uint32_t anf_s[ND][S_THREADS];
+  __shared__ uint32_t p_s[S_THREADS], cbeg_s[S_THREADS + 1], J_s[S_THREADS], Lb_s[S_THREADS];
+  if (blockIdx.x < totals->nsat_min) return;  // every D warm here: s2_out reads s2_warm's b
+  const uint32_t t = threadIdx.x;
+  if (t == 0) ch = *chunk;
+#pragma unroll
+  for (int d = 0; d < ND; ++d) anf_s[d][t] = 0;
+  const uint32_t e0 = blockIdx.x * S_THREADS;
+  uint32_t Lb;
+  uint64_t s;
+  const uint32_t ntot = block_setup(sim, E, e0, wch, p_s, J_s, Lb_s, cbeg_s, Lb, s, scan);
+  __syncthreads();
+  uint32_t Deff[ND];
+#pragma unroll
+  for (int d = 0; d < ND; ++d) Deff[d] = min(ch.D[d], maxL);
+  window_phase<ND, false>(scanrec, e0, wch, p_s, cbeg_s, ntot, Deff, anf_s, nullptr);
+  __syncthreads();
+  const uint32_t e = e0 + t;
+  if (e >= E) return;
+  LbJ[e] = Lb_s[t] | (J_s[t] << 16);
+  const uint32_t amax = static_cast<uint32_t>(static_cast<AT>(~AT(0)));
+  for (uint32_t d = 0; d < ch.nd; ++d) A[uint64_t(d) * Astride + e] = static_cast<AT>(min(anf_s[d][t], amax));
+}
+
+struct GroupDev {  // <= group-size instances of one chunk sharing D[d]: [inst0 + k0, inst0 + k0 + n)
+  uint32_t d, k0, n, pad;
+};
+
+// s2_out: one CTA = (instance group, event range).  Per 4 events per thread: b for every
+// instance of the group (X = min(NF(Lb), (C - A_nf)^+) on saturated blocks; the
+// warm-up blocks' b come back from s2_warm's output), one 8-byte store per instance, and the
+// group's histograms of b in shared memory (K3 without re-reading b).  The group's instances
+// share D and are sorted by C, so for one event b_i = J - clamp(C_i - A, 0, N) is J on a prefix
+// of instances (C_i <= A), J - N on a suffix (C_i >= A + N) and individual only in between: the
+// histograms are kept as a difference array along the instance axis (row i holds
+// hist[i] - hist[i-1]), a few shared-memory atomics per event instead of one per instance.
+template <typename AT>
+__global__ void __launch_bounds__(256) s2_out_kernel(const ChunkDev* __restrict__ chunk,
+                                                     const StackInstDev* __restrict__ insts,
+                                                     const GroupDev* __restrict__ groups,
+                                                     const ChunkTotals* __restrict__ totals,
+                                                     const AT* __restrict__ A, uint32_t Astride,
+                                                     const uint32_t* __restrict__ LbJ, uint32_t E, uint32_t range_len,
+                                                     uint32_t bins, bool aligned, uint16_t* __restrict__ bout,
+                                                     uint32_t* __restrict__ hist) {
+  extern __shared__ int hd[];  // [group size + 1][bins] difference rows
+  __shared__ uint32_t C2_s[GI_MAX], C_s[GI_MAX], inst_s[GI_MAX];
+  __shared__ uint64_t off_s[GI_MAX];
+  const GroupDev g = groups[blockIdx.y];
+  const uint32_t t = threadIdx.x, n = g.n;
+  const uint32_t D = chunk->D[g.d], nsat = totals->nsat[g.d], inst0 = chunk->inst0;
+  if (t < GI_MAX) {
+    if (t < n) {
+      const StackInstDev in = insts[inst0 + g.k0 + t];
+      C_s[t] = in.C;
+      C2_s[t] = in.C * 0x10001u;  // used only when C <= 65535
+      inst_s[t] = in.inst;
+      off_s[t] = in.boff;
+    } else {
+      C_s[t] = 0xFFFFFFFFu;  // sentinel: the branch-free searches below never count it
+    }
+  }
+  for (uint32_t k = t; k < (n + 1) * bins; k += blockDim.x) hd[k] = 0;
+  __syncthreads();
+  const bool packed_all = C_s[n - 1] <= 65535u;  // capacities are sorted
+  auto point = [&](uint32_t i, uint32_t v) {  // +1 at hist[i][v]
+    atomicAdd(&hd[i * bins + v], 1);
+    atomicAdd(&hd[(i + 1) * bins + v], -1);
+  };
+  const AT* Ad = A + uint64_t(g.d) * Astride;
+  const uint32_t e_begin = blockIdx.x * range_len, e_end = min(E, e_begin + range_len);
+  const uint32_t stride = 4 * blockDim.x;
+  // software pipeline: the next tile's (L_before | J) and A_nf are loaded one iteration ahead
+  uint4 lj_n = make_uint4(0, 0, 0, 0);
+  uint32_t av_n[4] = {0, 0, 0, 0};
+  auto load = [&](uint32_t e, uint4& lj, uint32_t* av) {
+    if (e + 3 < e_end) {
+      lj = *reinterpret_cast<const uint4*>(LbJ + e);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) av[u] = static_cast<uint32_t>(Ad[e + u]);
+    } else if (e < e_end) {
+      uint32_t l[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        l[u] = e + u < e_end ? LbJ[e + u] : 0u;
+        av[u] = e + u < e_end ? static_cast<uint32_t>(Ad[e + u]) : 0u;
+      }
+      lj = make_uint4(l[0], l[1], l[2], l[3]);
+    }
+  };
+  load(e_begin + 4 * t, lj_n, av_n);
+  for (uint32_t base = e_begin; base < e_end; base += stride) {
+    const uint32_t e = base + 4 * t;
+    const uint4 lj = lj_n;
+    uint32_t Av[4] = {av_n[0], av_n[1], av_n[2], av_n[3]};
+    if (base + stride < e_end) load(e + stride, lj_n, av_n);
+    if (e >= e_end) continue;
+    const uint32_t nv = min(4u, e_end - e);
+    const bool full = nv == 4;
+    const bool vec = full && aligned;
+    const bool warm = (e / S_THREADS) < nsat;  // the 4 events share a 256-event block
+    if (warm) {  // b written by s2_warm: histogram only
+      for (uint32_t i = 0; i < n; ++i) {
+        const uint16_t* row = bout + off_s[i] + e;
+        for (uint32_t u = 0; u < nv; ++u) point(i, row[u]);
+      }
+      continue;
+    }
+    const uint32_t l4[4] = {lj.x, lj.y, lj.z, lj.w};
+    uint32_t J[4], N[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      J[u] = l4[u] >> 16;
+      N[u] = nf_of(l4[u] & 0xFFFFu, D);  // first turns have L_before = 0 -> NF = 0
+    }
+    // ---- histograms: per event, prefix (b = J), middle (individual), suffix (b = J - N).
+    // k1 = #{C_i <= a}, k2 = #{C_i < a + N}: branch-free searches, the 4 events interleaved
+    uint32_t k1[4] = {0, 0, 0, 0}, k2[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (uint32_t step = GI_MAX / 2; step > 0; step >>= 1) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (C_s[k1[u] + step - 1] <= Av[u]) k1[u] += step;
+        if (C_s[k2[u] + step - 1] < Av[u] + N[u]) k2[u] += step;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {  // the steps sum to GI_MAX - 1: one last compare reaches GI_MAX
+      k1[u] += C_s[k1[u]] <= Av[u];
+      k2[u] += C_s[k2[u]] < Av[u] + N[u];
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (static_cast<uint32_t>(u) >= nv) break;
+      const uint32_t a = Av[u], b0 = J[u], b1 = J[u] - N[u];
+      const uint32_t lo = k1[u], hi = max(k2[u], k1[u]);
+      if (lo > 0) {
+        atomicAdd(&hd[b0], 1);
+        atomicAdd(&hd[lo * bins + b0], -1);
+      }
+      for (uint32_t i = lo; i < hi; ++i) point(i, b0 - (C_s[i] - a));
+      if (hi < n) {
+        atomicAdd(&hd[hi * bins + b1], 1);
+        atomicAdd(&hd[n * bins + b1], -1);
+      }
+    }
+    // ---- b for every instance of the group
+    const uint32_t J01 = J[0] | (J[1] << 16), J23 = J[2] | (J[3] << 16);
+    const uint32_t N01 = N[0] | (N[1] << 16), N23 = N[2] | (N[3] << 16);
+    if (packed_all && vec) {
+      const uint32_t A01 = min(Av[0], 65535u) | (min(Av[1], 65535u) << 16);
+      const uint32_t A23 = min(Av[2], 65535u) | (min(Av[3], 65535u) << 16);
+#pragma unroll 4
+      for (uint32_t i = 0; i < n; ++i) {
+        const uint32_t C2 = C2_s[i];
+        const uint32_t w01 = __vsub2(J01, __vminu2(N01, __vsub2(__vmaxu2(C2, A01), A01)));
+        const uint32_t w23 = __vsub2(J23, __vminu2(N23, __vsub2(__vmaxu2(C2, A23), A23)));
+        *reinterpret_cast<uint2*>(bout + off_s[i] + e) = make_uint2(w01, w23);
+      }
+    } else {
+      for (uint32_t i = 0; i < n; ++i) {
+        uint32_t b[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) b[u] = J[u] - min(N[u], sat_sub(C_s[i], Av[u]));
+        store4(bout + off_s[i] + e, vec, b[0] | (b[1] << 16), b[2] | (b[3] << 16), e, e_end);
+      }
+    }
+  }
+  __syncthreads();
+  for (uint32_t v = t; v < bins; v += blockDim.x) {  // prefix over the instance axis -> histograms
+    int run = 0;
+    for (uint32_t i = 0; i < n; ++i) {
+      run += hd[i * bins + v];
+      if (run) atomicAdd(&hist[uint64_t(inst_s[i]) * bins + v], static_cast<uint32_t>(run));
+    }
+  }
+}
+
 // ----------------------------------------------------------------------------- s3
 __global__ void s3_results_kernel(const StackInstDev* __restrict__ insts, uint32_t ninst,
                                   const uint32_t* __restrict__ inst_chunk, const ChunkTotals* __restrict__ totals,
@@ -549,8 +742,12 @@ struct StackPlan {
   std::vector<Chunk> chunks;
   std::vector<StackInstDev> insts;
   std::vector<uint32_t> inst_chunk;
+  std::vector<GroupDev> groups;        // s2_out instance groups, chunk-major
+  std::vector<uint32_t> group0;        // first group of each chunk (+ end)
   uint64_t Emax = 0;
   uint32_t maxbins = 1;
+  uint32_t gi = 0;                     // instances per s2_out group (0 = unfused path)
+  bool any_big = false;                // some capacity > 65535 -> u32 window sums
 };
 
 static void make_stack_plan(const tlru_trace* traces, uint32_t nt, const tlru_instance* inst, uint32_t ni,
@@ -608,9 +805,20 @@ static void make_stack_plan(const tlru_trace* traces, uint32_t nt, const tlru_in
       }
       for (uint32_t d = ch.dev.nd; d <= SND; ++d) ch.dev.dbeg[d] = static_cast<uint32_t>(P->insts.size()) - ch.dev.inst0;
       ch.dev.ninst = static_cast<uint32_t>(P->insts.size()) - ch.dev.inst0;
+      for (uint32_t d = 0; d < ch.dev.nd; ++d) P->any_big |= ch.dev.Cmax[d] > 65535u;
       P->chunks.push_back(ch);
     }
   }
+  // s2_out groups: the shared-memory histograms of a group hold gi x bins u32 counters
+  P->gi = P->maxbins <= 384 ? 64u : P->maxbins <= 768 ? 32u : P->maxbins <= 1536 ? 15u : 0u;
+  for (const StackPlan::Chunk& ch : P->chunks) {
+    P->group0.push_back(static_cast<uint32_t>(P->groups.size()));
+    if (!P->gi) continue;
+    for (uint32_t d = 0; d < ch.dev.nd; ++d)
+      for (uint32_t k = ch.dev.dbeg[d]; k < ch.dev.dbeg[d + 1]; k += P->gi)
+        P->groups.push_back(GroupDev{d, k, std::min(P->gi, ch.dev.dbeg[d + 1] - k), 0u});
+  }
+  P->group0.push_back(static_cast<uint32_t>(P->groups.size()));
 }
 
 struct StackWs {
@@ -622,6 +830,10 @@ struct StackWs {
   uint32_t* blockagg;  // [block][SND] growth of NF_all per D, then block prefixes; reused per chunk
   uint32_t* hist;      // [2][maxbins] L_after histograms, reused per chunk
   uint64_t* scanrec;   // [event] next | L_after << 32 of the trace being processed
+  GroupDev* groups;    // s2_out groups of every chunk
+  uint32_t* A;         // [SND][Astride] window sums A_nf (u16 or u32), reused per chunk
+  uint32_t* LbJ;       // [event] L_before | J << 16
+  uint32_t Astride;
 };
 
 static void carve_stack(Carver& cv, const StackPlan& P, uint32_t ni, StackWs* w) {
@@ -634,6 +846,11 @@ static void carve_stack(Carver& cv, const StackPlan& P, uint32_t ni, StackWs* w)
   w->blockagg = cv.take<uint32_t>(((P.Emax + S_THREADS - 1) / S_THREADS + 1) * SND);
   w->hist = cv.take<uint32_t>(2 * uint64_t(P.maxbins));
   w->scanrec = cv.take<uint64_t>(P.Emax + 1);
+  w->groups = cv.take<GroupDev>(P.groups.size() + 1);
+  w->Astride = static_cast<uint32_t>((P.Emax + 7) & ~7ull);
+  const size_t abytes = P.gi ? size_t(SND) * w->Astride * (P.any_big ? 4 : 2) : 4;
+  w->A = cv.take<uint32_t>((abytes + 3) / 4);
+  w->LbJ = cv.take<uint32_t>(P.gi ? P.Emax + 8 : 1);
 }
 
 tlru_status stack_workspace(const tlru_trace* traces, uint32_t nt, const tlru_instance* inst, uint32_t ni,
@@ -650,7 +867,8 @@ tlru_status stack_workspace(const tlru_trace* traces, uint32_t nt, const tlru_in
 
 template <int ND>
 static tlru_status launch_s2(const tlru_trace& tr, const ChunkDev* ch, const ChunkTotals* tot, const StackWs& w,
-                             bool aligned, uint16_t* bout, cudaStream_t st) {
+                             const StackPlan& P, uint32_t c, uint32_t bins, bool aligned, uint16_t* bout,
+                             uint32_t* hist, cudaStream_t st) {
   const uint32_t E = static_cast<uint32_t>(tr.num_events);
   const uint32_t nb = (E + S_THREADS - 1) / S_THREADS;
   // 16x2 partial sums of max(L, min(D, maxL)) stay exact while wch * maxL < 2^16
@@ -662,7 +880,36 @@ static tlru_status launch_s2(const tlru_trace& tr, const ChunkDev* ch, const Chu
   s2_warm_kernel<ND><<<std::min<uint32_t>(nb ? nb : 1, 2u * 148u), S_THREADS, warm_smem, st>>>(
       tr.sim, w.scanrec, E, ch, w.insts, tot, w.blockagg, wch, maxL, bout, w.sumXf);
   TLRU_CHECK_LAUNCH();
-  s2_sat_kernel<ND><<<nb, S_THREADS, 0, st>>>(tr.sim, w.scanrec, E, ch, w.insts, tot, wch, maxL, aligned, bout);
+  if (!P.gi) {  // unfused: b written by s2_sat, histograms by the generic K3 afterwards
+    s2_sat_kernel<ND><<<nb, S_THREADS, 0, st>>>(tr.sim, w.scanrec, E, ch, w.insts, tot, wch, maxL, aligned, bout);
+    TLRU_CHECK_LAUNCH();
+    return TLRU_OK;
+  }
+  const uint32_t g0 = P.group0[c], ng = P.group0[c + 1] - g0;
+  const uint32_t target = 148u * 8u;  // CTAs for s2_out
+  const uint32_t nr = std::max<uint32_t>(1u, (target + ng - 1) / std::max<uint32_t>(ng, 1u));
+  uint32_t rl = (E + nr - 1) / nr;
+  rl = (rl + 1023u) & ~1023u;
+  const uint32_t nranges = (E + rl - 1) / rl;
+  const size_t out_smem = size_t(P.gi + 1) * bins * sizeof(uint32_t);
+  if (P.any_big) {
+    s2_win_kernel<ND, uint32_t><<<nb, S_THREADS, 0, st>>>(tr.sim, w.scanrec, E, ch, tot, wch, maxL, w.A, w.Astride,
+                                                          w.LbJ);
+    TLRU_CHECK_LAUNCH();
+    TLRU_CUDA(cudaFuncSetAttribute(s2_out_kernel<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(out_smem)));
+    if (ng) s2_out_kernel<uint32_t><<<dim3(nranges, ng), 256, out_smem, st>>>(
+        ch, w.insts, w.groups + g0, tot, w.A, w.Astride, w.LbJ, E, rl, bins, aligned, bout, hist);
+  } else {
+    uint16_t* A16 = reinterpret_cast<uint16_t*>(w.A);
+    s2_win_kernel<ND, uint16_t><<<nb, S_THREADS, 0, st>>>(tr.sim, w.scanrec, E, ch, tot, wch, maxL, A16, w.Astride,
+                                                          w.LbJ);
+    TLRU_CHECK_LAUNCH();
+    TLRU_CUDA(cudaFuncSetAttribute(s2_out_kernel<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(out_smem)));
+    if (ng) s2_out_kernel<uint16_t><<<dim3(nranges, ng), 256, out_smem, st>>>(
+        ch, w.insts, w.groups + g0, tot, A16, w.Astride, w.LbJ, E, rl, bins, aligned, bout, hist);
+  }
   TLRU_CHECK_LAUNCH();
   return TLRU_OK;
 }
@@ -686,6 +933,9 @@ tlru_status stack_simulate(const tlru_trace* traces, uint32_t nt, const tlru_ins
                               cudaMemcpyHostToDevice, st));
     TLRU_CUDA(cudaMemcpyAsync(w.inst_chunk, P.inst_chunk.data(), P.inst_chunk.size() * sizeof(uint32_t),
                               cudaMemcpyHostToDevice, st));
+    if (!P.groups.empty())
+      TLRU_CUDA(cudaMemcpyAsync(w.groups, P.groups.data(), P.groups.size() * sizeof(GroupDev),
+                                cudaMemcpyHostToDevice, st));
   }
   TLRU_CUDA(cudaMemsetAsync(w.totals, 0, (nc + 1) * sizeof(ChunkTotals), st));
   TLRU_CUDA(cudaMemsetAsync(w.sumXf, 0, (ni + 1) * sizeof(unsigned long long), st));
@@ -705,19 +955,20 @@ tlru_status stack_simulate(const tlru_trace* traces, uint32_t nt, const tlru_ins
     s1_totals_kernel<<<1, T_THREADS, 0, st>>>(w.chunks + c, hb, w.hist, w.hist + hb, w.blockagg, nb, w.totals + c);
     TLRU_CHECK_LAUNCH();
     switch (P.chunks[c].ndk) {
-      case 2: TLRU_TRY(launch_s2<2>(tr, w.chunks + c, w.totals + c, w, aligned, bout, st)); break;
-      case 4: TLRU_TRY(launch_s2<4>(tr, w.chunks + c, w.totals + c, w, aligned, bout, st)); break;
-      case 8: TLRU_TRY(launch_s2<8>(tr, w.chunks + c, w.totals + c, w, aligned, bout, st)); break;
-      case 12: TLRU_TRY(launch_s2<12>(tr, w.chunks + c, w.totals + c, w, aligned, bout, st)); break;
-      case 16: TLRU_TRY(launch_s2<16>(tr, w.chunks + c, w.totals + c, w, aligned, bout, st)); break;
-      case 20: TLRU_TRY(launch_s2<20>(tr, w.chunks + c, w.totals + c, w, aligned, bout, st)); break;
-      default: TLRU_TRY(launch_s2<24>(tr, w.chunks + c, w.totals + c, w, aligned, bout, st)); break;
+      case 2: TLRU_TRY(launch_s2<2>(tr, w.chunks + c, w.totals + c, w, P, c, bins, aligned, bout, hist, st)); break;
+      case 4: TLRU_TRY(launch_s2<4>(tr, w.chunks + c, w.totals + c, w, P, c, bins, aligned, bout, hist, st)); break;
+      case 8: TLRU_TRY(launch_s2<8>(tr, w.chunks + c, w.totals + c, w, P, c, bins, aligned, bout, hist, st)); break;
+      case 12: TLRU_TRY(launch_s2<12>(tr, w.chunks + c, w.totals + c, w, P, c, bins, aligned, bout, hist, st)); break;
+      case 16: TLRU_TRY(launch_s2<16>(tr, w.chunks + c, w.totals + c, w, P, c, bins, aligned, bout, hist, st)); break;
+      case 20: TLRU_TRY(launch_s2<20>(tr, w.chunks + c, w.totals + c, w, P, c, bins, aligned, bout, hist, st)); break;
+      default: TLRU_TRY(launch_s2<24>(tr, w.chunks + c, w.totals + c, w, P, c, bins, aligned, bout, hist, st)); break;
     }
     *nkernels += 4;
   }
-  // K3 over b, then the eviction counters from the telescoped identities
+  // K3 (fused into s2_out unless the histograms are too wide), then the eviction counters from
+  // the telescoped identities
+  if (!P.gi) TLRU_TRY(launch_hist(bout, segs_dev, ni, bins, hist, clamped, st));
   if (ev_mid) TLRU_CUDA(cudaEventRecord(ev_mid, st));
-  TLRU_TRY(launch_hist(bout, segs_dev, ni, bins, hist, clamped, st));
   TLRU_TRY(launch_finalize(segs_dev, ni, bins, hist, clamped, 1.0, nullptr, results, st));
   if (!P.insts.empty()) {
     s3_results_kernel<<<grid_for(P.insts.size(), 128), 128, 0, st>>>(w.insts, static_cast<uint32_t>(P.insts.size()),
