@@ -46,7 +46,10 @@ constexpr int SND = 24;         // D values per chunk
 constexpr int S_THREADS = 256;  // events per s2 block
 constexpr uint32_t IT = 512;    // instance-table tile staged in shared memory by s2
 constexpr uint32_t WCH_MAX = 64;
-constexpr uint32_t GI_MAX = 64;  // instances per s2_out group
+constexpr uint32_t GI_MAX = 64;                     // instances per s2_out group
+constexpr uint32_t OUT_SMEM = 54u * 1024u;          // s2_out dynamic smem budget: 4 CTAs per SM
+constexpr uint32_t OUT_RANGE_MAX = 31u * 1024u;     // events per s2_out CTA (16-bit counters)
+constexpr uint32_t TAB_MAX = 8192;                  // s2_out count table covers capacities < TAB_MAX
 
 struct ChunkDev {
   uint32_t D[SND];
@@ -574,11 +577,17 @@ __global__ void __launch_bounds__(256) s2_out_kernel(const ChunkDev* __restrict_
                                                      const ChunkTotals* __restrict__ totals,
                                                      const AT* __restrict__ A, uint32_t Astride,
                                                      const uint32_t* __restrict__ LbJ, uint32_t E, uint32_t range_len,
-                                                     uint32_t bins, bool aligned, uint16_t* __restrict__ bout,
-                                                     uint32_t* __restrict__ hist) {
-  extern __shared__ int hd[];  // [group size + 1][bins] difference rows
-  __shared__ uint32_t C2_s[GI_MAX], C_s[GI_MAX], inst_s[GI_MAX];
+                                                     uint32_t bins, uint32_t rows, uint32_t tcap, bool aligned,
+                                                     uint16_t* __restrict__ bout, uint32_t* __restrict__ hist) {
+  // [rows >= group size + 1][hb2] difference rows, two 16-bit counters per word (bins 2v, 2v+1).  The
+  // counters wrap into each other, but a word's final value is lo + 65536 * hi (mod 2^32) and
+  // decodes exactly while |lo|, |hi| <= 32767, which range_len <= OUT_RANGE_MAX guarantees.
+  extern __shared__ uint32_t hw[];
+  const uint32_t hb2 = (bins + 1) >> 1;
+  __shared__ uint32_t C2_s[GI_MAX], C_s[GI_MAX], inst_s[GI_MAX], run_s[GI_MAX];
   __shared__ uint64_t off_s[GI_MAX];
+  // cnt[v] = #{i : C_i <= v} for v < tcap, after the histogram rows (used when C_{n-1} < tcap)
+  uint8_t* cnt = reinterpret_cast<uint8_t*>(hw + rows * hb2);
   const GroupDev g = groups[blockIdx.y];
   const uint32_t t = threadIdx.x, n = g.n;
   const uint32_t D = chunk->D[g.d], nsat = totals->nsat[g.d], inst0 = chunk->inst0;
@@ -593,12 +602,31 @@ __global__ void __launch_bounds__(256) s2_out_kernel(const ChunkDev* __restrict_
       C_s[t] = 0xFFFFFFFFu;  // sentinel: the branch-free searches below never count it
     }
   }
-  for (uint32_t k = t; k < (n + 1) * bins; k += blockDim.x) hd[k] = 0;
+  for (uint32_t k = t; k < (n + 1) * hb2; k += blockDim.x) hw[k] = 0;
   __syncthreads();
   const bool packed_all = C_s[n - 1] <= 65535u;  // capacities are sorted
+  const bool use_cnt = C_s[n - 1] < tcap;
+  auto count_le = [&](uint32_t v) {  // #{C_i <= v}: branch-free search over the sentinel-padded C_s
+    uint32_t k = 0;
+#pragma unroll
+    for (uint32_t step = GI_MAX / 2; step > 0; step >>= 1)
+      if (C_s[k + step - 1] <= v) k += step;
+    return k + (C_s[k] <= v);  // the steps sum to GI_MAX - 1: one last compare reaches GI_MAX
+  };
+  if (t < n) {  // run_s[i]: end of the run of instances with capacity C_i (equal b on every event)
+    uint32_t j = t + 1;
+    while (j < n && C_s[j] == C_s[t]) ++j;
+    run_s[t] = j;
+  }
+  if (use_cnt)
+    for (uint32_t v = t; v < tcap; v += blockDim.x) cnt[v] = static_cast<uint8_t>(count_le(v));
+  __syncthreads();
+  auto hadd = [&](uint32_t i, uint32_t v, int delta) {  // row i, bin v += delta
+    atomicAdd(&hw[i * hb2 + (v >> 1)], static_cast<uint32_t>(delta) << ((v & 1u) << 4));
+  };
   auto point = [&](uint32_t i, uint32_t v) {  // +1 at hist[i][v]
-    atomicAdd(&hd[i * bins + v], 1);
-    atomicAdd(&hd[(i + 1) * bins + v], -1);
+    hadd(i, v, 1);
+    hadd(i + 1, v, -1);
   };
   const AT* Ad = A + uint64_t(g.d) * Astride;
   const uint32_t e_begin = blockIdx.x * range_len, e_end = min(E, e_begin + range_len);
@@ -632,10 +660,15 @@ __global__ void __launch_bounds__(256) s2_out_kernel(const ChunkDev* __restrict_
     const bool full = nv == 4;
     const bool vec = full && aligned;
     const bool warm = (e / S_THREADS) < nsat;  // the 4 events share a 256-event block
-    if (warm) {  // b written by s2_warm: histogram only
-      for (uint32_t i = 0; i < n; ++i) {
+    if (warm) {  // b written by s2_warm: histogram only, one range update per run of equal C
+      for (uint32_t i = 0; i < n;) {
         const uint16_t* row = bout + off_s[i] + e;
-        for (uint32_t u = 0; u < nv; ++u) point(i, row[u]);
+        const uint32_t j = run_s[i];
+        for (uint32_t u = 0; u < nv; ++u) {
+          hadd(i, row[u], 1);
+          hadd(j, row[u], -1);
+        }
+        i = j;
       }
       continue;
     }
@@ -647,20 +680,21 @@ __global__ void __launch_bounds__(256) s2_out_kernel(const ChunkDev* __restrict_
       N[u] = nf_of(l4[u] & 0xFFFFu, D);  // first turns have L_before = 0 -> NF = 0
     }
     // ---- histograms: per event, prefix (b = J), middle (individual), suffix (b = J - N).
-    // k1 = #{C_i <= a}, k2 = #{C_i < a + N}: branch-free searches, the 4 events interleaved
-    uint32_t k1[4] = {0, 0, 0, 0}, k2[4] = {0, 0, 0, 0};
-#pragma unroll
-    for (uint32_t step = GI_MAX / 2; step > 0; step >>= 1) {
+    // k1 = #{C_i <= a}, k2 = #{C_i < a + N} = #{C_i <= a + N - 1}: table lookups, else
+    // branch-free searches with the 4 events interleaved
+    uint32_t k1[4], k2[4];
+    if (use_cnt) {
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        if (C_s[k1[u] + step - 1] <= Av[u]) k1[u] += step;
-        if (C_s[k2[u] + step - 1] < Av[u] + N[u]) k2[u] += step;
+        k1[u] = cnt[min(Av[u], tcap - 1)];
+        k2[u] = Av[u] + N[u] ? cnt[min(Av[u] + N[u] - 1, tcap - 1)] : 0u;
       }
-    }
+    } else {
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {  // the steps sum to GI_MAX - 1: one last compare reaches GI_MAX
-      k1[u] += C_s[k1[u]] <= Av[u];
-      k2[u] += C_s[k2[u]] < Av[u] + N[u];
+      for (int u = 0; u < 4; ++u) {
+        k1[u] = count_le(Av[u]);
+        k2[u] = Av[u] + N[u] ? count_le(Av[u] + N[u] - 1) : 0u;
+      }
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
@@ -668,13 +702,18 @@ __global__ void __launch_bounds__(256) s2_out_kernel(const ChunkDev* __restrict_
       const uint32_t a = Av[u], b0 = J[u], b1 = J[u] - N[u];
       const uint32_t lo = k1[u], hi = max(k2[u], k1[u]);
       if (lo > 0) {
-        atomicAdd(&hd[b0], 1);
-        atomicAdd(&hd[lo * bins + b0], -1);
+        hadd(0, b0, 1);
+        hadd(lo, b0, -1);
       }
-      for (uint32_t i = lo; i < hi; ++i) point(i, b0 - (C_s[i] - a));
+      for (uint32_t i = lo; i < hi;) {  // runs of equal C lie entirely inside [lo, hi)
+        const uint32_t j = run_s[i], v = b0 - (C_s[i] - a);
+        hadd(i, v, 1);
+        hadd(j, v, -1);
+        i = j;
+      }
       if (hi < n) {
-        atomicAdd(&hd[hi * bins + b1], 1);
-        atomicAdd(&hd[n * bins + b1], -1);
+        hadd(hi, b1, 1);
+        hadd(n, b1, -1);
       }
     }
     // ---- b for every instance of the group
@@ -700,11 +739,17 @@ __global__ void __launch_bounds__(256) s2_out_kernel(const ChunkDev* __restrict_
     }
   }
   __syncthreads();
-  for (uint32_t v = t; v < bins; v += blockDim.x) {  // prefix over the instance axis -> histograms
-    int run = 0;
+  for (uint32_t v2 = t; v2 < hb2; v2 += blockDim.x) {  // prefix over the instance axis -> histograms
+    int run0 = 0, run1 = 0;
+    const uint32_t v = 2 * v2;
     for (uint32_t i = 0; i < n; ++i) {
-      run += hd[i * bins + v];
-      if (run) atomicAdd(&hist[uint64_t(inst_s[i]) * bins + v], static_cast<uint32_t>(run));
+      const uint32_t w = hw[i * hb2 + v2];
+      const int lo = static_cast<int16_t>(w & 0xFFFFu);
+      run0 += lo;
+      run1 += static_cast<int>(w - static_cast<uint32_t>(lo)) >> 16;
+      uint32_t* h = hist + uint64_t(inst_s[i]) * bins + v;
+      if (run0) atomicAdd(h, static_cast<uint32_t>(run0));
+      if (run1) atomicAdd(h + 1, static_cast<uint32_t>(run1));  // run1 != 0 implies v + 1 < bins
     }
   }
 }
@@ -747,6 +792,7 @@ struct StackPlan {
   uint64_t Emax = 0;
   uint32_t maxbins = 1;
   uint32_t gi = 0;                     // instances per s2_out group (0 = unfused path)
+  uint32_t tcap = 1;                   // s2_out count table entries (capacities < tcap)
   bool any_big = false;                // some capacity > 65535 -> u32 window sums
 };
 
@@ -809,8 +855,13 @@ static void make_stack_plan(const tlru_trace* traces, uint32_t nt, const tlru_in
       P->chunks.push_back(ch);
     }
   }
-  // s2_out groups: the shared-memory histograms of a group hold gi x bins u32 counters
-  P->gi = P->maxbins <= 384 ? 64u : P->maxbins <= 768 ? 32u : P->maxbins <= 1536 ? 15u : 0u;
+  // s2_out groups: the shared-memory histograms of a group hold (gi + 1) x ceil(bins / 2) words
+  uint32_t cmax = 0;
+  for (const StackInstDev& in : P->insts) cmax = std::max(cmax, in.C);
+  P->tcap = std::min(cmax, TAB_MAX - 1u) + 1u;
+  const uint32_t hb2 = (P->maxbins + 1) / 2;  // maxbins == the batch's histogram bins
+  const uint32_t gfit = (OUT_SMEM - ((P->tcap + 3u) & ~3u)) / (4u * hb2);
+  P->gi = gfit >= 9u ? std::min(GI_MAX, gfit - 1u) : 0u;
   for (const StackPlan::Chunk& ch : P->chunks) {
     P->group0.push_back(static_cast<uint32_t>(P->groups.size()));
     if (!P->gi) continue;
@@ -889,9 +940,9 @@ static tlru_status launch_s2(const tlru_trace& tr, const ChunkDev* ch, const Chu
   const uint32_t target = 148u * 8u;  // CTAs for s2_out
   const uint32_t nr = std::max<uint32_t>(1u, (target + ng - 1) / std::max<uint32_t>(ng, 1u));
   uint32_t rl = (E + nr - 1) / nr;
-  rl = (rl + 1023u) & ~1023u;
+  rl = std::min(OUT_RANGE_MAX, (rl + 1023u) & ~1023u);
   const uint32_t nranges = (E + rl - 1) / rl;
-  const size_t out_smem = size_t(P.gi + 1) * bins * sizeof(uint32_t);
+  const size_t out_smem = size_t(P.gi + 1) * ((bins + 1) / 2) * sizeof(uint32_t) + ((P.tcap + 3) & ~3u);
   if (P.any_big) {
     s2_win_kernel<ND, uint32_t><<<nb, S_THREADS, 0, st>>>(tr.sim, w.scanrec, E, ch, tot, wch, maxL, w.A, w.Astride,
                                                           w.LbJ);
@@ -899,7 +950,7 @@ static tlru_status launch_s2(const tlru_trace& tr, const ChunkDev* ch, const Chu
     TLRU_CUDA(cudaFuncSetAttribute(s2_out_kernel<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(out_smem)));
     if (ng) s2_out_kernel<uint32_t><<<dim3(nranges, ng), 256, out_smem, st>>>(
-        ch, w.insts, w.groups + g0, tot, w.A, w.Astride, w.LbJ, E, rl, bins, aligned, bout, hist);
+        ch, w.insts, w.groups + g0, tot, w.A, w.Astride, w.LbJ, E, rl, bins, P.gi + 1, P.tcap, aligned, bout, hist);
   } else {
     uint16_t* A16 = reinterpret_cast<uint16_t*>(w.A);
     s2_win_kernel<ND, uint16_t><<<nb, S_THREADS, 0, st>>>(tr.sim, w.scanrec, E, ch, tot, wch, maxL, A16, w.Astride,
@@ -908,7 +959,7 @@ static tlru_status launch_s2(const tlru_trace& tr, const ChunkDev* ch, const Chu
     TLRU_CUDA(cudaFuncSetAttribute(s2_out_kernel<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(out_smem)));
     if (ng) s2_out_kernel<uint16_t><<<dim3(nranges, ng), 256, out_smem, st>>>(
-        ch, w.insts, w.groups + g0, tot, A16, w.Astride, w.LbJ, E, rl, bins, aligned, bout, hist);
+        ch, w.insts, w.groups + g0, tot, A16, w.Astride, w.LbJ, E, rl, bins, P.gi + 1, P.tcap, aligned, bout, hist);
   }
   TLRU_CHECK_LAUNCH();
   return TLRU_OK;
