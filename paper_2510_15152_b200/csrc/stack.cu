@@ -571,13 +571,13 @@ struct GroupDev {  // <= group-size instances of one chunk sharing D[d]: [inst0 
 // histograms are kept as a difference array along the instance axis (row i holds
 // hist[i] - hist[i-1]), a few shared-memory atomics per event instead of one per instance.
 template <typename AT>
-__global__ void __launch_bounds__(256) s2_out_kernel(const ChunkDev* __restrict__ chunk,
+__global__ void __launch_bounds__(256, 4) s2_out_kernel(const ChunkDev* __restrict__ chunk,
                                                      const StackInstDev* __restrict__ insts,
                                                      const GroupDev* __restrict__ groups,
                                                      const ChunkTotals* __restrict__ totals,
                                                      const AT* __restrict__ A, uint32_t Astride,
                                                      const uint32_t* __restrict__ LbJ, uint32_t E, uint32_t range_len,
-                                                     uint32_t bins, uint32_t rows, uint32_t tcap, bool aligned,
+                                                     uint32_t bins, uint32_t rows, uint32_t tcap, bool aligned16,
                                                      uint16_t* __restrict__ bout, uint32_t* __restrict__ hist) {
   // [rows >= group size + 1][hb2] difference rows, two 16-bit counters per word (bins 2v, 2v+1).  The
   // counters wrap into each other, but a word's final value is lo + 65536 * hi (mod 2^32) and
@@ -630,36 +630,43 @@ __global__ void __launch_bounds__(256) s2_out_kernel(const ChunkDev* __restrict_
   };
   const AT* Ad = A + uint64_t(g.d) * Astride;
   const uint32_t e_begin = blockIdx.x * range_len, e_end = min(E, e_begin + range_len);
-  const uint32_t stride = 4 * blockDim.x;
-  // software pipeline: the next tile's (L_before | J) and A_nf are loaded one iteration ahead
-  uint4 lj_n = make_uint4(0, 0, 0, 0);
-  uint32_t av_n[4] = {0, 0, 0, 0};
-  auto load = [&](uint32_t e, uint4& lj, uint32_t* av) {
-    if (e + 3 < e_end) {
-      lj = *reinterpret_cast<const uint4*>(LbJ + e);
-#pragma unroll
-      for (int u = 0; u < 4; ++u) av[u] = static_cast<uint32_t>(Ad[e + u]);
-    } else if (e < e_end) {
-      uint32_t l[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        l[u] = e + u < e_end ? LbJ[e + u] : 0u;
-        av[u] = e + u < e_end ? static_cast<uint32_t>(Ad[e + u]) : 0u;
+  constexpr uint32_t EV = 8;  // events per thread per tile: one 16-byte store per instance
+  const uint32_t stride = EV * blockDim.x;
+  const uint32_t D2 = min(D, 65535u) * 0x10001u;  // NF(L) = max(L, D) - D per 16-bit half (L <= 65535)
+  auto pk = [](uint32_t x, uint32_t y) { return min(x, 65535u) | (min(y, 65535u) << 16); };
+  // software pipeline: the next tile's (L_before | J) words and packed A_nf pairs (clamped to
+  // 65535, exact for C <= 65535) are loaded one iteration ahead
+  uint4 l0n = make_uint4(0, 0, 0, 0), l1n = l0n, an = l0n;
+  auto load = [&](uint32_t e, uint4& l0, uint4& l1, uint4& ap) {
+    if (e + EV <= e_end) {
+      l0 = *reinterpret_cast<const uint4*>(LbJ + e);
+      l1 = *reinterpret_cast<const uint4*>(LbJ + e + 4);
+      if constexpr (sizeof(AT) == 2) {
+        ap = *reinterpret_cast<const uint4*>(Ad + e);
+      } else {
+        const uint4 x = *reinterpret_cast<const uint4*>(Ad + e), y = *reinterpret_cast<const uint4*>(Ad + e + 4);
+        ap = make_uint4(pk(x.x, x.y), pk(x.z, x.w), pk(y.x, y.y), pk(y.z, y.w));
       }
-      lj = make_uint4(l[0], l[1], l[2], l[3]);
+    } else if (e < e_end) {
+      uint32_t l[EV], a[EV];
+#pragma unroll
+      for (uint32_t u = 0; u < EV; ++u) {
+        l[u] = e + u < e_end ? LbJ[e + u] : 0u;
+        a[u] = e + u < e_end ? static_cast<uint32_t>(Ad[e + u]) : 0u;
+      }
+      l0 = make_uint4(l[0], l[1], l[2], l[3]);
+      l1 = make_uint4(l[4], l[5], l[6], l[7]);
+      ap = make_uint4(pk(a[0], a[1]), pk(a[2], a[3]), pk(a[4], a[5]), pk(a[6], a[7]));
     }
   };
-  load(e_begin + 4 * t, lj_n, av_n);
+  load(e_begin + EV * t, l0n, l1n, an);
   for (uint32_t base = e_begin; base < e_end; base += stride) {
-    const uint32_t e = base + 4 * t;
-    const uint4 lj = lj_n;
-    uint32_t Av[4] = {av_n[0], av_n[1], av_n[2], av_n[3]};
-    if (base + stride < e_end) load(e + stride, lj_n, av_n);
+    const uint32_t e = base + EV * t;
+    const uint4 l0 = l0n, l1 = l1n, ap = an;
+    if (base + stride < e_end) load(e + stride, l0n, l1n, an);
     if (e >= e_end) continue;
-    const uint32_t nv = min(4u, e_end - e);
-    const bool full = nv == 4;
-    const bool vec = full && aligned;
-    const bool warm = (e / S_THREADS) < nsat;  // the 4 events share a 256-event block
+    const uint32_t nv = min(EV, e_end - e);
+    const bool warm = (e / S_THREADS) < nsat;  // the 8 events share a 256-event block
     if (warm) {  // b written by s2_warm: histogram only, one range update per run of equal C
       for (uint32_t i = 0; i < n;) {
         const uint16_t* row = bout + off_s[i] + e;
@@ -672,35 +679,37 @@ __global__ void __launch_bounds__(256) s2_out_kernel(const ChunkDev* __restrict_
       }
       continue;
     }
-    const uint32_t l4[4] = {lj.x, lj.y, lj.z, lj.w};
-    uint32_t J[4], N[4];
+    // packed pairs of events (2k, 2k + 1): J, N = NF(L_before) (first turns: L_before = 0), A_nf
+    const uint32_t lw[EV] = {l0.x, l0.y, l0.z, l0.w, l1.x, l1.y, l1.z, l1.w};
+    const uint32_t A2[4] = {ap.x, ap.y, ap.z, ap.w};
+    uint32_t J2[4], N2[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      J[u] = l4[u] >> 16;
-      N[u] = nf_of(l4[u] & 0xFFFFu, D);  // first turns have L_before = 0 -> NF = 0
+    for (int k = 0; k < 4; ++k) {
+      J2[k] = __byte_perm(lw[2 * k], lw[2 * k + 1], 0x7632);
+      N2[k] = __vsub2(__vmaxu2(__byte_perm(lw[2 * k], lw[2 * k + 1], 0x5410), D2), D2);
     }
+    auto half = [](const uint32_t* v2, int u) { return (v2[u >> 1] >> ((u & 1) * 16)) & 0xFFFFu; };
+    auto a_of = [&](int u) -> uint32_t {  // exact A_nf of event e + u
+      if constexpr (sizeof(AT) == 2) return half(A2, u);
+      else return static_cast<uint32_t>(Ad[e + u]);
+    };
     // ---- histograms: per event, prefix (b = J), middle (individual), suffix (b = J - N).
-    // k1 = #{C_i <= a}, k2 = #{C_i < a + N} = #{C_i <= a + N - 1}: table lookups, else
-    // branch-free searches with the 4 events interleaved
-    uint32_t k1[4], k2[4];
-    if (use_cnt) {
+    // k1 = #{C_i <= a}, k2 = #{C_i < a + N} = #{C_i <= a + N - 1}: table lookups (all 8 events
+    // before the first atomic), else branch-free searches
+    uint32_t kk[EV];  // k1 | k2 << 8
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        k1[u] = cnt[min(Av[u], tcap - 1)];
-        k2[u] = Av[u] + N[u] ? cnt[min(Av[u] + N[u] - 1, tcap - 1)] : 0u;
-      }
-    } else {
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        k1[u] = count_le(Av[u]);
-        k2[u] = Av[u] + N[u] ? count_le(Av[u] + N[u] - 1) : 0u;
-      }
+    for (int u = 0; u < static_cast<int>(EV); ++u) {
+      const uint32_t a = u < static_cast<int>(nv) ? a_of(u) : 0u, top = a + half(N2, u);
+      if (use_cnt)
+        kk[u] = cnt[min(a, tcap - 1)] | (top ? uint32_t(cnt[min(top - 1, tcap - 1)]) << 8 : 0u);
+      else
+        kk[u] = count_le(a) | (top ? count_le(top - 1) << 8 : 0u);
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      if (static_cast<uint32_t>(u) >= nv) break;
-      const uint32_t a = Av[u], b0 = J[u], b1 = J[u] - N[u];
-      const uint32_t lo = k1[u], hi = max(k2[u], k1[u]);
+    for (int u = 0; u < static_cast<int>(EV); ++u) {
+      if (u >= static_cast<int>(nv)) break;
+      const uint32_t a = a_of(u), b0 = half(J2, u), b1 = b0 - half(N2, u);
+      const uint32_t lo = kk[u] & 0xFFu, hi = max(kk[u] >> 8, lo);
       if (lo > 0) {
         hadd(0, b0, 1);
         hadd(lo, b0, -1);
@@ -716,25 +725,25 @@ __global__ void __launch_bounds__(256) s2_out_kernel(const ChunkDev* __restrict_
         hadd(n, b1, -1);
       }
     }
-    // ---- b for every instance of the group
-    const uint32_t J01 = J[0] | (J[1] << 16), J23 = J[2] | (J[3] << 16);
-    const uint32_t N01 = N[0] | (N[1] << 16), N23 = N[2] | (N[3] << 16);
-    if (packed_all && vec) {
-      const uint32_t A01 = min(Av[0], 65535u) | (min(Av[1], 65535u) << 16);
-      const uint32_t A23 = min(Av[2], 65535u) | (min(Av[3], 65535u) << 16);
-#pragma unroll 4
+    // ---- b for every instance of the group: b = J - min(N, (C - A)^+)
+    if (packed_all && aligned16 && nv == EV) {
+#pragma unroll 2
       for (uint32_t i = 0; i < n; ++i) {
         const uint32_t C2 = C2_s[i];
-        const uint32_t w01 = __vsub2(J01, __vminu2(N01, __vsub2(__vmaxu2(C2, A01), A01)));
-        const uint32_t w23 = __vsub2(J23, __vminu2(N23, __vsub2(__vmaxu2(C2, A23), A23)));
-        *reinterpret_cast<uint2*>(bout + off_s[i] + e) = make_uint2(w01, w23);
+        uint32_t w[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) w[k] = __vsub2(J2[k], __vminu2(N2[k], __vsub2(__vmaxu2(C2, A2[k]), A2[k])));
+        *reinterpret_cast<uint4*>(bout + off_s[i] + e) = make_uint4(w[0], w[1], w[2], w[3]);
       }
     } else {
       for (uint32_t i = 0; i < n; ++i) {
-        uint32_t b[4];
+        uint32_t b[EV];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) b[u] = J[u] - min(N[u], sat_sub(C_s[i], Av[u]));
-        store4(bout + off_s[i] + e, vec, b[0] | (b[1] << 16), b[2] | (b[3] << 16), e, e_end);
+        for (int u = 0; u < static_cast<int>(EV); ++u)
+          b[u] = u < static_cast<int>(nv) ? half(J2, u) - min(half(N2, u), sat_sub(C_s[i], a_of(u))) : 0u;
+        uint16_t* row = bout + off_s[i] + e;
+        store4(row, e + 4 <= e_end, b[0] | (b[1] << 16), b[2] | (b[3] << 16), e, e_end);
+        if (e + 4 < e_end) store4(row + 4, nv == EV, b[4] | (b[5] << 16), b[6] | (b[7] << 16), e + 4, e_end);
       }
     }
   }
@@ -918,7 +927,7 @@ tlru_status stack_workspace(const tlru_trace* traces, uint32_t nt, const tlru_in
 
 template <int ND>
 static tlru_status launch_s2(const tlru_trace& tr, const ChunkDev* ch, const ChunkTotals* tot, const StackWs& w,
-                             const StackPlan& P, uint32_t c, uint32_t bins, bool aligned, uint16_t* bout,
+                             const StackPlan& P, uint32_t c, uint32_t bins, bool aligned, bool aligned16, uint16_t* bout,
                              uint32_t* hist, cudaStream_t st) {
   const uint32_t E = static_cast<uint32_t>(tr.num_events);
   const uint32_t nb = (E + S_THREADS - 1) / S_THREADS;
@@ -950,7 +959,7 @@ static tlru_status launch_s2(const tlru_trace& tr, const ChunkDev* ch, const Chu
     TLRU_CUDA(cudaFuncSetAttribute(s2_out_kernel<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(out_smem)));
     if (ng) s2_out_kernel<uint32_t><<<dim3(nranges, ng), 256, out_smem, st>>>(
-        ch, w.insts, w.groups + g0, tot, w.A, w.Astride, w.LbJ, E, rl, bins, P.gi + 1, P.tcap, aligned, bout, hist);
+        ch, w.insts, w.groups + g0, tot, w.A, w.Astride, w.LbJ, E, rl, bins, P.gi + 1, P.tcap, aligned16, bout, hist);
   } else {
     uint16_t* A16 = reinterpret_cast<uint16_t*>(w.A);
     s2_win_kernel<ND, uint16_t><<<nb, S_THREADS, 0, st>>>(tr.sim, w.scanrec, E, ch, tot, wch, maxL, A16, w.Astride,
@@ -959,7 +968,7 @@ static tlru_status launch_s2(const tlru_trace& tr, const ChunkDev* ch, const Chu
     TLRU_CUDA(cudaFuncSetAttribute(s2_out_kernel<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(out_smem)));
     if (ng) s2_out_kernel<uint16_t><<<dim3(nranges, ng), 256, out_smem, st>>>(
-        ch, w.insts, w.groups + g0, tot, A16, w.Astride, w.LbJ, E, rl, bins, P.gi + 1, P.tcap, aligned, bout, hist);
+        ch, w.insts, w.groups + g0, tot, A16, w.Astride, w.LbJ, E, rl, bins, P.gi + 1, P.tcap, aligned16, bout, hist);
   }
   TLRU_CHECK_LAUNCH();
   return TLRU_OK;
@@ -993,6 +1002,8 @@ tlru_status stack_simulate(const tlru_trace* traces, uint32_t nt, const tlru_ins
   // 8-byte b stores need every instance row to start at a multiple of 4 requests (16-byte base)
   bool aligned = (reinterpret_cast<uintptr_t>(bout) & 7u) == 0;
   for (const StackInstDev& in : P.insts) aligned &= (in.boff & 3u) == 0;
+  bool aligned16 = (reinterpret_cast<uintptr_t>(bout) & 15u) == 0;  // s2_out: 16-byte stores of 8 requests
+  for (const StackInstDev& in : P.insts) aligned16 &= (in.boff & 7u) == 0;
   for (size_t c = 0; c < nc; ++c) {
     const tlru_trace& tr = traces[P.chunks[c].trace];
     const uint32_t E = static_cast<uint32_t>(tr.num_events);
@@ -1006,13 +1017,13 @@ tlru_status stack_simulate(const tlru_trace* traces, uint32_t nt, const tlru_ins
     s1_totals_kernel<<<1, T_THREADS, 0, st>>>(w.chunks + c, hb, w.hist, w.hist + hb, w.blockagg, nb, w.totals + c);
     TLRU_CHECK_LAUNCH();
     switch (P.chunks[c].ndk) {
-      case 2: TLRU_TRY(launch_s2<2>(tr, w.chunks + c, w.totals + c, w, P, c, bins, aligned, bout, hist, st)); break;
-      case 4: TLRU_TRY(launch_s2<4>(tr, w.chunks + c, w.totals + c, w, P, c, bins, aligned, bout, hist, st)); break;
-      case 8: TLRU_TRY(launch_s2<8>(tr, w.chunks + c, w.totals + c, w, P, c, bins, aligned, bout, hist, st)); break;
-      case 12: TLRU_TRY(launch_s2<12>(tr, w.chunks + c, w.totals + c, w, P, c, bins, aligned, bout, hist, st)); break;
-      case 16: TLRU_TRY(launch_s2<16>(tr, w.chunks + c, w.totals + c, w, P, c, bins, aligned, bout, hist, st)); break;
-      case 20: TLRU_TRY(launch_s2<20>(tr, w.chunks + c, w.totals + c, w, P, c, bins, aligned, bout, hist, st)); break;
-      default: TLRU_TRY(launch_s2<24>(tr, w.chunks + c, w.totals + c, w, P, c, bins, aligned, bout, hist, st)); break;
+      case 2: TLRU_TRY(launch_s2<2>(tr, w.chunks + c, w.totals + c, w, P, c, bins, aligned, aligned16, bout, hist, st)); break;
+      case 4: TLRU_TRY(launch_s2<4>(tr, w.chunks + c, w.totals + c, w, P, c, bins, aligned, aligned16, bout, hist, st)); break;
+      case 8: TLRU_TRY(launch_s2<8>(tr, w.chunks + c, w.totals + c, w, P, c, bins, aligned, aligned16, bout, hist, st)); break;
+      case 12: TLRU_TRY(launch_s2<12>(tr, w.chunks + c, w.totals + c, w, P, c, bins, aligned, aligned16, bout, hist, st)); break;
+      case 16: TLRU_TRY(launch_s2<16>(tr, w.chunks + c, w.totals + c, w, P, c, bins, aligned, aligned16, bout, hist, st)); break;
+      case 20: TLRU_TRY(launch_s2<20>(tr, w.chunks + c, w.totals + c, w, P, c, bins, aligned, aligned16, bout, hist, st)); break;
+      default: TLRU_TRY(launch_s2<24>(tr, w.chunks + c, w.totals + c, w, P, c, bins, aligned, aligned16, bout, hist, st)); break;
     }
     *nkernels += 4;
   }
