@@ -35,6 +35,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <type_traits>
 #include <vector>
 
 #include "metrics.cuh"
@@ -46,7 +47,12 @@ constexpr int SND = 24;         // D values per chunk
 constexpr int S_THREADS = 256;  // events per s2 block
 constexpr uint32_t IT = 512;    // instance-table tile staged in shared memory by s2
 constexpr uint32_t WCH_MAX = 64;
-constexpr uint32_t GI_MAX = 64;                     // instances per s2_out group
+constexpr uint32_t GI_MAX = 64;                     // instances per s2_out group (hard limit)
+// Measured on B200 (config-5 sweep): groups of 13..24 instances are fastest.  Each CTA writes
+// one 16-byte store per instance row per 8 events, and the write stream loses DRAM efficiency
+// as the number of rows a CTA interleaves grows (tools/write_bw.cu: 7.4 TB/s with one row per
+// CTA, 5.9-6.9 with 8, 4.9 with 35); smaller groups re-read the per-event inputs more often.
+constexpr uint32_t GI_CAP = 16;
 constexpr uint32_t OUT_SMEM = 54u * 1024u;          // s2_out dynamic smem budget: 4 CTAs per SM
 constexpr uint32_t OUT_RANGE_MAX = 31u * 1024u;     // events per s2_out CTA (16-bit counters)
 constexpr uint32_t TAB_MAX = 8192;                  // s2_out count table covers capacities < TAB_MAX
@@ -578,8 +584,9 @@ __global__ void __launch_bounds__(256, 4) s2_out_kernel(const ChunkDev* __restri
                                                      const AT* __restrict__ A, uint32_t Astride,
                                                      const uint32_t* __restrict__ LbJ, uint32_t E, uint32_t range_len,
                                                      uint32_t bins, uint32_t rows, uint32_t tcap, bool aligned16,
-                                                     uint16_t* __restrict__ bout, uint32_t* __restrict__ hist) {
-  // [rows >= group size + 1][hb2] difference rows, two 16-bit counters per word (bins 2v, 2v+1).  The
+                                                     uint16_t* __restrict__ bout, uint32_t* __restrict__ hist,
+                                                     uint32_t range0) {
+  // [rows >= group size][hb2] difference rows, two 16-bit counters per word (bins 2v, 2v+1).  The
   // counters wrap into each other, but a word's final value is lo + 65536 * hi (mod 2^32) and
   // decodes exactly while |lo|, |hi| <= 32767, which range_len <= OUT_RANGE_MAX guarantees.
   extern __shared__ uint32_t hw[];
@@ -588,7 +595,10 @@ __global__ void __launch_bounds__(256, 4) s2_out_kernel(const ChunkDev* __restri
   __shared__ uint64_t off_s[GI_MAX];
   // cnt[v] = #{i : C_i <= v} for v < tcap, after the histogram rows (used when C_{n-1} < tcap)
   uint8_t* cnt = reinterpret_cast<uint8_t*>(hw + rows * hb2);
-  const GroupDev g = groups[blockIdx.y];
+  // grid (groups, ranges): groups fastest, so the CTAs resident at one time share event ranges
+  // (the per-event inputs LbJ / A_nf are read once from DRAM and then hit in L2)
+  const GroupDev g = groups[blockIdx.x];
+  const uint32_t rid = range0 + blockIdx.y;
   const uint32_t t = threadIdx.x, n = g.n;
   const uint32_t D = chunk->D[g.d], nsat = totals->nsat[g.d], inst0 = chunk->inst0;
   if (t < GI_MAX) {
@@ -602,7 +612,7 @@ __global__ void __launch_bounds__(256, 4) s2_out_kernel(const ChunkDev* __restri
       C_s[t] = 0xFFFFFFFFu;  // sentinel: the branch-free searches below never count it
     }
   }
-  for (uint32_t k = t; k < (n + 1) * hb2; k += blockDim.x) hw[k] = 0;
+  for (uint32_t k = t; k < n * hb2; k += blockDim.x) hw[k] = 0;  // row n (never read) is not kept
   __syncthreads();
   const bool packed_all = C_s[n - 1] <= 65535u;  // capacities are sorted
   const bool use_cnt = C_s[n - 1] < tcap;
@@ -618,18 +628,24 @@ __global__ void __launch_bounds__(256, 4) s2_out_kernel(const ChunkDev* __restri
     while (j < n && C_s[j] == C_s[t]) ++j;
     run_s[t] = j;
   }
-  if (use_cnt)
-    for (uint32_t v = t; v < tcap; v += blockDim.x) cnt[v] = static_cast<uint8_t>(count_le(v));
+  if (use_cnt)  // four independent searches in flight per thread
+    for (uint32_t v0 = t; v0 < tcap; v0 += 4 * blockDim.x) {
+      uint32_t c[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) c[q] = count_le(v0 + q * blockDim.x);
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (v0 + q * blockDim.x < tcap) cnt[v0 + q * blockDim.x] = static_cast<uint8_t>(c[q]);
+    }
   __syncthreads();
   auto hadd = [&](uint32_t i, uint32_t v, int delta) {  // row i, bin v += delta
     atomicAdd(&hw[i * hb2 + (v >> 1)], static_cast<uint32_t>(delta) << ((v & 1u) << 4));
   };
-  auto point = [&](uint32_t i, uint32_t v) {  // +1 at hist[i][v]
-    hadd(i, v, 1);
-    hadd(i + 1, v, -1);
+  auto hsub = [&](uint32_t j, uint32_t v) {  // -1 at row j: row n is never read
+    if (j < n) hadd(j, v, -1);
   };
   const AT* Ad = A + uint64_t(g.d) * Astride;
-  const uint32_t e_begin = blockIdx.x * range_len, e_end = min(E, e_begin + range_len);
+  const uint32_t e_begin = rid * range_len, e_end = min(E, e_begin + range_len);
   constexpr uint32_t EV = 8;  // events per thread per tile: one 16-byte store per instance
   const uint32_t stride = EV * blockDim.x;
   const uint32_t D2 = min(D, 65535u) * 0x10001u;  // NF(L) = max(L, D) - D per 16-bit half (L <= 65535)
@@ -673,7 +689,7 @@ __global__ void __launch_bounds__(256, 4) s2_out_kernel(const ChunkDev* __restri
         const uint32_t j = run_s[i];
         for (uint32_t u = 0; u < nv; ++u) {
           hadd(i, row[u], 1);
-          hadd(j, row[u], -1);
+          hsub(j, row[u]);
         }
         i = j;
       }
@@ -712,18 +728,15 @@ __global__ void __launch_bounds__(256, 4) s2_out_kernel(const ChunkDev* __restri
       const uint32_t lo = kk[u] & 0xFFu, hi = max(kk[u] >> 8, lo);
       if (lo > 0) {
         hadd(0, b0, 1);
-        hadd(lo, b0, -1);
+        hsub(lo, b0);
       }
       for (uint32_t i = lo; i < hi;) {  // runs of equal C lie entirely inside [lo, hi)
         const uint32_t j = run_s[i], v = b0 - (C_s[i] - a);
         hadd(i, v, 1);
-        hadd(j, v, -1);
+        hsub(j, v);
         i = j;
       }
-      if (hi < n) {
-        hadd(hi, b1, 1);
-        hadd(n, b1, -1);
-      }
+      if (hi < n) hadd(hi, b1, 1);
     }
     // ---- b for every instance of the group: b = J - min(N, (C - A)^+)
     if (packed_all && aligned16 && nv == EV) {
@@ -870,13 +883,18 @@ static void make_stack_plan(const tlru_trace* traces, uint32_t nt, const tlru_in
   P->tcap = std::min(cmax, TAB_MAX - 1u) + 1u;
   const uint32_t hb2 = (P->maxbins + 1) / 2;  // maxbins == the batch's histogram bins
   const uint32_t gfit = (OUT_SMEM - ((P->tcap + 3u) & ~3u)) / (4u * hb2);
-  P->gi = gfit >= 9u ? std::min(GI_MAX, gfit - 1u) : 0u;
+  P->gi = gfit >= 8u ? std::min(GI_CAP, gfit) : 0u;
   for (const StackPlan::Chunk& ch : P->chunks) {
     P->group0.push_back(static_cast<uint32_t>(P->groups.size()));
     if (!P->gi) continue;
-    for (uint32_t d = 0; d < ch.dev.nd; ++d)
-      for (uint32_t k = ch.dev.dbeg[d]; k < ch.dev.dbeg[d + 1]; k += P->gi)
-        P->groups.push_back(GroupDev{d, k, std::min(P->gi, ch.dev.dbeg[d + 1] - k), 0u});
+    for (uint32_t d = 0; d < ch.dev.nd; ++d) {  // near-equal groups of <= gi instances
+      const uint32_t m = ch.dev.dbeg[d + 1] - ch.dev.dbeg[d], ngd = (m + P->gi - 1) / P->gi;
+      for (uint32_t q = 0, k = ch.dev.dbeg[d]; q < ngd; ++q) {
+        const uint32_t sz = m / ngd + (q < m % ngd ? 1u : 0u);
+        P->groups.push_back(GroupDev{d, k, sz, 0u});
+        k += sz;
+      }
+    }
   }
   P->group0.push_back(static_cast<uint32_t>(P->groups.size()));
 }
@@ -951,27 +969,23 @@ static tlru_status launch_s2(const tlru_trace& tr, const ChunkDev* ch, const Chu
   uint32_t rl = (E + nr - 1) / nr;
   rl = std::min(OUT_RANGE_MAX, (rl + 1023u) & ~1023u);
   const uint32_t nranges = (E + rl - 1) / rl;
-  const size_t out_smem = size_t(P.gi + 1) * ((bins + 1) / 2) * sizeof(uint32_t) + ((P.tcap + 3) & ~3u);
-  if (P.any_big) {
-    s2_win_kernel<ND, uint32_t><<<nb, S_THREADS, 0, st>>>(tr.sim, w.scanrec, E, ch, tot, wch, maxL, w.A, w.Astride,
-                                                          w.LbJ);
+  const size_t out_smem = size_t(P.gi) * ((bins + 1) / 2) * sizeof(uint32_t) + ((P.tcap + 3) & ~3u);
+  auto out = [&](auto* Aptr) -> tlru_status {
+    using AT = std::remove_const_t<std::remove_pointer_t<decltype(Aptr)>>;
+    s2_win_kernel<ND, AT><<<nb, S_THREADS, 0, st>>>(tr.sim, w.scanrec, E, ch, tot, wch, maxL, Aptr, w.Astride, w.LbJ);
     TLRU_CHECK_LAUNCH();
-    TLRU_CUDA(cudaFuncSetAttribute(s2_out_kernel<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    TLRU_CUDA(cudaFuncSetAttribute(s2_out_kernel<AT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(out_smem)));
-    if (ng) s2_out_kernel<uint32_t><<<dim3(nranges, ng), 256, out_smem, st>>>(
-        ch, w.insts, w.groups + g0, tot, w.A, w.Astride, w.LbJ, E, rl, bins, P.gi + 1, P.tcap, aligned16, bout, hist);
-  } else {
-    uint16_t* A16 = reinterpret_cast<uint16_t*>(w.A);
-    s2_win_kernel<ND, uint16_t><<<nb, S_THREADS, 0, st>>>(tr.sim, w.scanrec, E, ch, tot, wch, maxL, A16, w.Astride,
-                                                          w.LbJ);
-    TLRU_CHECK_LAUNCH();
-    TLRU_CUDA(cudaFuncSetAttribute(s2_out_kernel<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   static_cast<int>(out_smem)));
-    if (ng) s2_out_kernel<uint16_t><<<dim3(nranges, ng), 256, out_smem, st>>>(
-        ch, w.insts, w.groups + g0, tot, A16, w.Astride, w.LbJ, E, rl, bins, P.gi + 1, P.tcap, aligned16, bout, hist);
-  }
-  TLRU_CHECK_LAUNCH();
-  return TLRU_OK;
+    for (uint32_t r0 = 0; ng && r0 < nranges; r0 += 65535u) {  // grid.y <= 65535
+      s2_out_kernel<AT><<<dim3(ng, std::min(65535u, nranges - r0)), 256, out_smem, st>>>(
+          ch, w.insts, w.groups + g0, tot, Aptr, w.Astride, w.LbJ, E, rl, bins, P.gi, P.tcap, aligned16, bout, hist,
+          r0);
+      TLRU_CHECK_LAUNCH();
+    }
+    return TLRU_OK;
+  };
+  if (P.any_big) return out(w.A);
+  return out(reinterpret_cast<uint16_t*>(w.A));
 }
 
 tlru_status stack_simulate(const tlru_trace* traces, uint32_t nt, const tlru_instance* inst, uint32_t ni,
