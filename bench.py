@@ -207,7 +207,10 @@ def run_ours(args, rank, world, local_rank):
         gws.append(torch.empty(max(sz.value, 1), dtype=torch.uint8, device=dev))
     tstructs = [tr.struct() for tr in traces]
     gathered = torch.empty(world * results_all.numel(), dtype=torch.uint8, device=dev) if world > 1 else None
-    sA, sB = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
+    # generation (compute-bound) on a higher-priority stream: its CTAs take SM slots as the
+    # memory-bound simulation kernels' CTAs retire
+    prio = int(os.environ.get("BENCH_GEN_PRIO", "-1"))
+    sA, sB = torch.cuda.Stream(device=dev, priority=prio), torch.cuda.Stream(device=dev)
 
     def gen_one(t, st):  # a1-a3: K1 re-generates trace t in place (host waits on `st` only)
         _abi.check(_abi.lib.tlru_generate_traces(ctypes.byref(gstructs[t]), 1, ctypes.byref(tstructs[t]),
