@@ -210,7 +210,9 @@ def run_ours(args, rank, world, local_rank):
     # generation (compute-bound) on a higher-priority stream: its CTAs take SM slots as the
     # memory-bound simulation kernels' CTAs retire
     prio = int(os.environ.get("BENCH_GEN_PRIO", "-1"))
-    sA, sB = torch.cuda.Stream(device=dev, priority=prio), torch.cuda.Stream(device=dev)
+    sA = torch.cuda.Stream(device=dev, priority=prio)
+    nsim = int(os.environ.get("BENCH_SIM_STREAMS", "2"))
+    sBs = [torch.cuda.Stream(device=dev) for _ in range(nsim)]
 
     def gen_one(t, st):  # a1-a3: K1 re-generates trace t in place (host waits on `st` only)
         _abi.check(_abi.lib.tlru_generate_traces(ctypes.byref(gstructs[t]), 1, ctypes.byref(tstructs[t]),
@@ -235,12 +237,16 @@ def run_ours(args, rank, world, local_rank):
         return k2, k3
 
     def step():
-        """Pipelined: trace t+1 is generated on stream A while trace t is simulated on stream B."""
+        """Pipelined: trace t+1 is generated on stream A while traces are simulated on the
+        simulation streams (alternating, so one trace's compute-bound phase overlaps the
+        previous trace's memory-bound output phase; every batch has its own workspace)."""
         ev0 = torch.cuda.Event()
         ev0.record(stream)
         sA.wait_event(ev0)
-        sB.wait_event(ev0)
+        for sB in sBs:
+            sB.wait_event(ev0)
         for t, bt in enumerate(batches):
+            sB = sBs[t % len(sBs)]
             gen_one(t, sA)
             ev = torch.cuda.Event()
             ev.record(sA)
@@ -249,7 +255,8 @@ def run_ours(args, rank, world, local_rank):
             with torch.cuda.stream(sB):
                 results_all[slices[t]].copy_(bt.results)
         stream.wait_stream(sA)
-        stream.wait_stream(sB)
+        for sB in sBs:
+            stream.wait_stream(sB)
         gather()
 
     def barrier():
@@ -326,9 +333,11 @@ def run_ours(args, rank, world, local_rank):
         ev0 = torch.cuda.Event()
         ev0.record(stream)
         sA.wait_event(ev0)
-        sB.wait_event(ev0)
+        for sB in sBs:
+            sB.wait_event(ev0)
         for t, ((hc, hq, ha), (dc, dq, da), tr, ts, w, bt) in enumerate(
                 zip(host_turns, dev_turns, traces, tstructs, up_ws, batches)):
+            sB = sBs[t % len(sBs)]
             with torch.cuda.stream(sA):
                 dc.copy_(hc, non_blocking=True)
                 dq.copy_(hq, non_blocking=True)
@@ -342,7 +351,8 @@ def run_ours(args, rank, world, local_rank):
             with torch.cuda.stream(sB):
                 results_all[slices[t]].copy_(bt.results)
         stream.wait_stream(sA)
-        stream.wait_stream(sB)
+        for sB in sBs:
+            stream.wait_stream(sB)
         host_results.copy_(results_all, non_blocking=True)
         stream.synchronize()
 
