@@ -24,7 +24,6 @@ import json
 import os
 import statistics
 import sys
-import threading
 import time
 
 import numpy as np
@@ -39,6 +38,11 @@ sys.path.insert(0, ROOT)
 ALGO_BYTES_PER_REQUEST = 10
 STACK_B_BYTES = 2
 STACK_PASS_BYTES_PER_EVENT = 20
+#  * s2_out (the dominant kernel): 2-byte b written per request; 4-byte (L_before | J) read per event and
+#    one 2-byte A_nf per (event, distinct D) read, shared by the instances of a group.
+OUT_B_BYTES = 2
+OUT_EVENT_BYTES = 4
+OUT_ROW_BYTES = 2
 SEEDS_PER_RANK = 4
 
 
@@ -56,50 +60,59 @@ def peaks():
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+def _clock_sampler_proc(index, go, stop, out):
+    """Child process (no CUDA): polls NVML every 5 ms between `go` and `stop`."""
+    res = {"sm": [], "mx": 0, "reasons": 0, "error": None}
+    try:
+        import pynvml as nv
+        nv.nvmlInit()
+        h = nv.nvmlDeviceGetHandleByIndex(index)
+        res["mx"] = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        go.wait()
+        while not stop.is_set():
+            res["sm"].append(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
+            res["reasons"] |= int(nv.nvmlDeviceGetCurrentClocksEventReasons(h))
+            time.sleep(0.005)
+    except Exception as ex:  # noqa: BLE001 -- report, never fail the bench
+        res["error"] = repr(ex)
+    out.put(res)
+
+
 class ClockSampler:
     """SM clocks and throttle reasons sampled through NVML (the library nvidia-smi reads)
-    every 10 ms in a background thread while the timed region runs."""
+    every 5 ms while the timed region runs.  The sampler is a forked child process, so it
+    keeps sampling while this process blocks in CUDA calls holding the GIL."""
 
     REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20, "sw_power_cap": 0x4}
 
     def __init__(self, index: int):
-        self.index = index
-        self.sm, self.mx, self.reasons = [], 0, set()
-        self.stop = threading.Event()
-        self.h = None
-        try:  # NVML init before the timed region (it can take longer than a short region)
-            import pynvml
-            pynvml.nvmlInit()
-            self.nv = pynvml
-            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
-            self.mx = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
-        except Exception as ex:  # noqa: BLE001 -- report, never fail the bench
-            self.error = repr(ex)
-
-    def _run(self):
-        if self.h is None:
-            return
-        nv = self.nv
-        while not self.stop.is_set():
-            self.sm.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
-            r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
-            for n, bit in self.REASONS.items():
-                if r & bit:
-                    self.reasons.add(n)
-            time.sleep(0.005)
+        import multiprocessing as mp
+        ctx = mp.get_context("fork")
+        self.go, self.stop, self.q = ctx.Event(), ctx.Event(), ctx.Queue()
+        self.p = ctx.Process(target=_clock_sampler_proc, args=(index, self.go, self.stop, self.q), daemon=True)
+        self.p.start()  # NVML init happens before the timed region
+        self.res = None
 
     def __enter__(self):
-        self.t = threading.Thread(target=self._run, daemon=True)
-        self.t.start()
+        self.go.set()
         return self
 
     def __exit__(self, *a):
         self.stop.set()
-        self.t.join(timeout=5)
+        try:
+            self.res = self.q.get(timeout=10)
+        except Exception as ex:  # noqa: BLE001
+            self.res = {"sm": [], "mx": 0, "reasons": 0, "error": repr(ex)}
+        self.p.join(timeout=5)
 
     def summary(self):
-        return {"sm_mhz": statistics.median(self.sm) if self.sm else None, "sm_max_mhz": self.mx or None,
-                "reasons": sorted(self.reasons), "samples": len(self.sm)}
+        r = self.res or {"sm": [], "mx": 0, "reasons": 0}
+        out = {"sm_mhz": statistics.median(r["sm"]) if r["sm"] else None, "sm_max_mhz": r["mx"] or None,
+               "reasons": sorted(n for n, bit in self.REASONS.items() if r["reasons"] & bit),
+               "samples": len(r["sm"])}
+        if r.get("error"):
+            out["error"] = r["error"]
+        return out
 
 
 # ----------------------------------------------------------------------------- reference (CPU oracle)
@@ -226,15 +239,18 @@ def run_ours(args, rank, world, local_rank):
         """One stream, no overlap; returns the summed engine / K3 device times of the step."""
         for t in range(nt):
             gen_one(t, stream)
-        k2 = k3 = 0.0
+        k2 = k3 = out_ms = 0.0
+        out_n = 0
         for t, bt in enumerate(batches):
             bt.run(stream)  # a4-a9: simulation engine + K3
             st = T.last_sim_stats()
             k2 += st["k2_ms"]
             k3 += st["k3_ms"]
+            out_ms += st["out_ms"]
+            out_n += st["out_launches"]
             results_all[slices[t]].copy_(bt.results)
         gather()
-        return k2, k3
+        return k2, k3, out_ms, out_n
 
     def step():
         """Pipelined: trace t+1 is generated on stream A while traces are simulated on the
@@ -265,13 +281,14 @@ def run_ours(args, rank, world, local_rank):
         torch.cuda.synchronize()
 
     def timed(fn, steps: int, warmup: int):
+        clk = ClockSampler(local_rank)  # sampler process + NVML init before the timed region
         for _ in range(warmup):
             fn()
         barrier()
         l0 = _abi.lib.tlru_launch_count()
         out = []
         t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        with ClockSampler(local_rank) as clk:
+        with clk:
             barrier()
             t0.record(stream)
             for _ in range(steps):
@@ -287,6 +304,8 @@ def run_ours(args, rank, world, local_rank):
     seq = timed(step_seq, max(2, args.steps // 2), 1)
     main["k2"] = statistics.mean(o[0] for o in seq["out"])
     main["k3"] = statistics.mean(o[1] for o in seq["out"])
+    main["out_ms"] = statistics.mean(o[2] for o in seq["out"])
+    main["out_n"] = seq["out"][-1][3]
     stats = T.last_sim_stats()
     assert stats["failed_chains"] == 0
     res = results_all.cpu().numpy().view(_abi.RESULT_DTYPE)
@@ -361,10 +380,10 @@ def run_ours(args, rank, world, local_rank):
 
     # ---- max over ranks
     loc = torch.tensor([main["ms"], e2e["ms"], main["k2"], main["k3"], rep["ms"] if rep else 0.0,
-                        rep["k2"] if rep else 0.0, seq["ms"]], dtype=torch.float64, device=dev)
+                        rep["k2"] if rep else 0.0, seq["ms"], main["out_ms"]], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(loc, op=dist.ReduceOp.MAX)
-    ms, e2e_ms, k2, k3, rep_ms, rep_k2, seq_ms = [float(x) for x in loc.tolist()]
+    ms, e2e_ms, k2, k3, rep_ms, rep_k2, seq_ms, out_ms = [float(x) for x in loc.tolist()]
     if rank != 0:
         return
     req_all = E_tot * world
@@ -374,16 +393,21 @@ def run_ours(args, rank, world, local_rank):
     for r in rows:
         D = (r[3] - r[4]) if (r[1] == 1 and r[3] > r[4]) else 0
         nd_per_trace.setdefault(r[0], set()).add(D)
-    passes = sum((len(v) + 7) // 8 for v in nd_per_trace.values())  # D chunks of <= 8 values per trace
-    stack_bytes = STACK_B_BYTES * E_tot + STACK_PASS_BYTES_PER_EVENT * sum(
-        traces[t].num_events * ((len(v) + 7) // 8) for t, v in nd_per_trace.items())
-    achieved = stack_bytes / (k2 / 1000.0) / 1e9  # GB/s per GPU over the simulation phase
+    ev_tot = sum(traces[t].num_events for t in nd_per_trace)
+    ev_rows = sum(traces[t].num_events * len(v) for t, v in nd_per_trace.items())  # (event, D) pairs
+    # dominant kernel s2_out: writes b (2 B/request) and reads, once per event, the packed
+    # (L_before | J) word and one 2-byte A_nf per (event, D)
+    out_bytes = OUT_B_BYTES * E_tot + OUT_EVENT_BYTES * ev_tot + OUT_ROW_BYTES * ev_rows
+    out_n = max(int(main["out_n"]), 1)  # s2_out launches per step (one per trace here)
+    achieved = (out_bytes / out_n) / (out_ms / out_n / 1000.0) / 1e9 if out_ms > 0 else None
+    # whole engine (all simulation kernels of the step, sequential stream)
+    eng_bytes = STACK_B_BYTES * E_tot + STACK_PASS_BYTES_PER_EVENT * ev_tot
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
         t = json.load(open(tpath))
-        if "s2_dram_bytes_per_request" in t:
-            traffic = float(t["s2_dram_bytes_per_request"]) * E_tot
+        if "s2_out_dram_bytes_per_request" in t:
+            traffic = float(t["s2_out_dram_bytes_per_request"]) * E_tot / out_n
     line = {
         "metric": "simulated requests/sec", "value": value, "unit": "requests/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
@@ -396,16 +420,24 @@ def run_ours(args, rank, world, local_rank):
             "engine": "stack (closed form of Alg. 1 from the stack property, all capacities of a trace per pass; "
                       "bit-identical to the replay engine and the oracle); no dedup of identical instances",
             "engine_ms": k2, "k3_ms": k3, "sequential_ms_per_step": seq_ms,
-            "pipelining": "trace t+1 generated on stream A while trace t is simulated on stream B; "
-                          "engine_ms / k3_ms from the sequential (single-stream) step",
+            "pipelining": "traces generated on a high-priority stream A while earlier traces are simulated on "
+                          "two alternating streams; engine_ms / k3_ms / roofline.launch_ms from the sequential "
+                          "(single-stream) step",
         },
         "e2e": {"value": req_all / (e2e_ms / 1000.0), "unit": "requests/s", "h2d_bytes_per_step": h2d_bytes,
                 "d2h_bytes_per_step": d2h_bytes, "ms_per_step": e2e_ms},
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "kernel": "stack engine (s1 + s2_main, all launches of a step)",
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak if achieved else None, "traffic": traffic,
+                     "kernel": "s2_out_kernel (b output + per-group histograms), per launch",
+                     "launch_ms": out_ms / out_n, "launches_per_step": out_n,
+                     "algorithmic_bytes_per_launch": out_bytes / out_n,
+                     "algorithmic_bytes": f"{OUT_B_BYTES} B/request (b written) + {OUT_EVENT_BYTES} B/event + "
+                                          f"{OUT_ROW_BYTES} B/(event, D) read",
                      "peak_source": peak_src,
-                     "algorithmic_bytes": f"{STACK_B_BYTES} B/request (b) + {STACK_PASS_BYTES_PER_EVENT} B/event "
-                                          f"per trace pass ({passes} passes)",
+                     "engine": {"achieved": eng_bytes / (k2 / 1000.0) / 1e9,
+                                "frac": eng_bytes / (k2 / 1000.0) / 1e9 / peak, "ms": k2,
+                                "algorithmic_bytes": f"{STACK_B_BYTES} B/request + "
+                                                     f"{STACK_PASS_BYTES_PER_EVENT} B/event"},
                      "survey_model_frac": ALGO_BYTES_PER_REQUEST * E_tot / (k2 / 1000.0) / 1e9 / peak},
         "gpu_launches": int(main["launches"] // max(args.steps, 1)),
         "clocks": main["clocks"],

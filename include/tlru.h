@@ -231,6 +231,9 @@ typedef struct {
   uint32_t reserved;
   float k2_ms;              /* device time of the simulation kernels (K2 + spill, or the stack engine) */
   float k3_ms;              /* device time of the tail-metric kernels (K3) */
+  float out_ms;             /* stack engine, fused path: device time from the first to the last
+                               s2_out launch (b output + histograms, the dominant kernel); else 0 */
+  uint32_t out_launches;    /* s2_out launches in that interval */
 } tlru_sim_stats;
 tlru_status tlru_last_sim_stats(tlru_sim_stats* out /*host*/);
 

@@ -77,7 +77,7 @@ class SimStats(ctypes.Structure):
     _fields_ = [("chains", ctypes.c_uint64), ("segment_events", ctypes.c_uint64), ("spilled_chains", ctypes.c_uint64),
                 ("failed_chains", ctypes.c_uint64), ("kernels", ctypes.c_uint32), ("state_entries", ctypes.c_uint32),
                 ("engine", ctypes.c_uint32), ("reserved", ctypes.c_uint32), ("k2_ms", ctypes.c_float),
-                ("k3_ms", ctypes.c_float)]
+                ("k3_ms", ctypes.c_float), ("out_ms", ctypes.c_float), ("out_launches", ctypes.c_uint32)]
 
 
 EXPORTS = (

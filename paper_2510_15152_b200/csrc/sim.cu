@@ -351,7 +351,8 @@ static void carve_sim(Carver& cv, const Plan& P, uint32_t ni, SimWs* w) {
 
 static thread_local tlru_sim_stats g_stats;
 static thread_local unsigned int* g_counters = nullptr;
-static thread_local cudaEvent_t g_ev[3] = {nullptr, nullptr, nullptr};
+static thread_local cudaEvent_t g_ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+static thread_local OutTiming g_out;  // s2_out interval (g_ev[3], g_ev[4])
 static thread_local bool g_ev_recorded = false;
 
 static tlru_status record(int k, cudaStream_t st) {
@@ -403,6 +404,7 @@ extern "C" tlru_status tlru_simulate_batch(const tlru_trace* traces, uint32_t nt
   g_stats = tlru_sim_stats{};
   g_counters = nullptr;
   g_ev_recorded = false;
+  g_out.launches = 0;
   if (ni == 0) return TLRU_OK;
   if (!results) TLRU_FAIL(TLRU_EINVAL, "results is NULL");
   Plan P;
@@ -425,9 +427,11 @@ extern "C" tlru_status tlru_simulate_batch(const tlru_trace* traces, uint32_t nt
     TLRU_CUDA(cudaMemsetAsync(clamped, 0, ni * sizeof(unsigned long long), st));
     unsigned nk = 0;
     TLRU_TRY(record(0, st));
-    if (!g_ev[1]) TLRU_CUDA(cudaEventCreate(&g_ev[1]));
+    for (int k = 1; k < 5; ++k)
+      if (!g_ev[k]) TLRU_CUDA(cudaEventCreate(&g_ev[k]));
+    g_out = OutTiming{g_ev[3], g_ev[4], 0u};
     TLRU_TRY(stack_simulate(traces, nt, inst, ni, boffs.data(), uncached, results, cv, segs, P.bins, hist, clamped,
-                            ws_bytes, st, &nk, g_ev[1]));  // records g_ev[1] between the engine and K3
+                            ws_bytes, st, &nk, g_ev[1], &g_out));  // records g_ev[1] between the engine and K3
     TLRU_TRY(record(2, st));
     g_ev_recorded = true;
     g_stats.kernels = nk;
@@ -532,6 +536,9 @@ extern "C" tlru_status tlru_last_sim_stats(tlru_sim_stats* out) {
     TLRU_CUDA(cudaEventSynchronize(g_ev[2]));
     TLRU_CUDA(cudaEventElapsedTime(&out->k2_ms, g_ev[0], g_ev[1]));
     TLRU_CUDA(cudaEventElapsedTime(&out->k3_ms, g_ev[1], g_ev[2]));
+    out->out_ms = 0.0f;
+    out->out_launches = g_out.launches;
+    if (g_out.launches) TLRU_CUDA(cudaEventElapsedTime(&out->out_ms, g_out.first, g_out.last));
   }
   return TLRU_OK;
 }

@@ -576,6 +576,28 @@ struct GroupDev {  // <= group-size instances of one chunk sharing D[d]: [inst0 
 // of instances (C_i <= A), J - N on a suffix (C_i >= A + N) and individual only in between: the
 // histograms are kept as a difference array along the instance axis (row i holds
 // hist[i] - hist[i-1]), a few shared-memory atomics per event instead of one per instance.
+// cnt[g][v] = #{i in group g : C_i <= v} for v < tcap (rows padded to 16 bytes), for the
+// groups whose capacities are all < tcap.  One CTA per group.
+__global__ void __launch_bounds__(256) s2_cnt_kernel(const ChunkDev* __restrict__ chunk,
+                                                     const StackInstDev* __restrict__ insts,
+                                                     const GroupDev* __restrict__ groups, uint32_t tcap,
+                                                     uint8_t* __restrict__ cnt_g) {
+  __shared__ uint32_t C_s[GI_MAX];
+  const GroupDev g = groups[blockIdx.x];
+  const uint32_t t = threadIdx.x;
+  if (t < GI_MAX) C_s[t] = t < g.n ? insts[chunk->inst0 + g.k0 + t].C : 0xFFFFFFFFu;
+  __syncthreads();
+  if (C_s[g.n - 1] >= tcap) return;
+  uint8_t* row = cnt_g + uint64_t(blockIdx.x) * ((tcap + 15u) & ~15u);
+  for (uint32_t v = t; v < tcap; v += blockDim.x) {
+    uint32_t k = 0;
+#pragma unroll
+    for (uint32_t step = GI_MAX / 2; step > 0; step >>= 1)
+      if (C_s[k + step - 1] <= v) k += step;
+    row[v] = static_cast<uint8_t>(k + (C_s[k] <= v));
+  }
+}
+
 template <typename AT>
 __global__ void __launch_bounds__(256, 4) s2_out_kernel(const ChunkDev* __restrict__ chunk,
                                                      const StackInstDev* __restrict__ insts,
@@ -585,7 +607,7 @@ __global__ void __launch_bounds__(256, 4) s2_out_kernel(const ChunkDev* __restri
                                                      const uint32_t* __restrict__ LbJ, uint32_t E, uint32_t range_len,
                                                      uint32_t bins, uint32_t rows, uint32_t tcap, bool aligned16,
                                                      uint16_t* __restrict__ bout, uint32_t* __restrict__ hist,
-                                                     uint32_t range0) {
+                                                     const uint4* __restrict__ cnt_g, uint32_t range0) {
   // [rows >= group size][hb2] difference rows, two 16-bit counters per word (bins 2v, 2v+1).  The
   // counters wrap into each other, but a word's final value is lo + 65536 * hi (mod 2^32) and
   // decodes exactly while |lo|, |hi| <= 32767, which range_len <= OUT_RANGE_MAX guarantees.
@@ -594,7 +616,7 @@ __global__ void __launch_bounds__(256, 4) s2_out_kernel(const ChunkDev* __restri
   __shared__ uint32_t C2_s[GI_MAX], C_s[GI_MAX], inst_s[GI_MAX], run_s[GI_MAX];
   __shared__ uint64_t off_s[GI_MAX];
   // cnt[v] = #{i : C_i <= v} for v < tcap, after the histogram rows (used when C_{n-1} < tcap)
-  uint8_t* cnt = reinterpret_cast<uint8_t*>(hw + rows * hb2);
+  uint8_t* cnt = reinterpret_cast<uint8_t*>(hw + ((rows * hb2 + 3u) & ~3u));  // 16-byte aligned
   // grid (groups, ranges): groups fastest, so the CTAs resident at one time share event ranges
   // (the per-event inputs LbJ / A_nf are read once from DRAM and then hit in L2)
   const GroupDev g = groups[blockIdx.x];
@@ -628,15 +650,10 @@ __global__ void __launch_bounds__(256, 4) s2_out_kernel(const ChunkDev* __restri
     while (j < n && C_s[j] == C_s[t]) ++j;
     run_s[t] = j;
   }
-  if (use_cnt)  // four independent searches in flight per thread
-    for (uint32_t v0 = t; v0 < tcap; v0 += 4 * blockDim.x) {
-      uint32_t c[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) c[q] = count_le(v0 + q * blockDim.x);
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-        if (v0 + q * blockDim.x < tcap) cnt[v0 + q * blockDim.x] = static_cast<uint8_t>(c[q]);
-    }
+  if (use_cnt) {  // the group's table, built once by s2_cnt_kernel
+    const uint4* src = cnt_g + uint64_t(blockIdx.x) * ((tcap + 15u) >> 4);
+    for (uint32_t k = t; k < (tcap + 15u) >> 4; k += blockDim.x) reinterpret_cast<uint4*>(cnt)[k] = src[k];
+  }
   __syncthreads();
   auto hadd = [&](uint32_t i, uint32_t v, int delta) {  // row i, bin v += delta
     atomicAdd(&hw[i * hb2 + (v >> 1)], static_cast<uint32_t>(delta) << ((v & 1u) << 4));
@@ -882,7 +899,7 @@ static void make_stack_plan(const tlru_trace* traces, uint32_t nt, const tlru_in
   for (const StackInstDev& in : P->insts) cmax = std::max(cmax, in.C);
   P->tcap = std::min(cmax, TAB_MAX - 1u) + 1u;
   const uint32_t hb2 = (P->maxbins + 1) / 2;  // maxbins == the batch's histogram bins
-  const uint32_t gfit = (OUT_SMEM - ((P->tcap + 3u) & ~3u)) / (4u * hb2);
+  const uint32_t gfit = (OUT_SMEM - 16u - ((P->tcap + 15u) & ~15u)) / (4u * hb2);
   P->gi = gfit >= 8u ? std::min(GI_CAP, gfit) : 0u;
   for (const StackPlan::Chunk& ch : P->chunks) {
     P->group0.push_back(static_cast<uint32_t>(P->groups.size()));
@@ -911,6 +928,7 @@ struct StackWs {
   GroupDev* groups;    // s2_out groups of every chunk
   uint32_t* A;         // [SND][Astride] window sums A_nf (u16 or u32), reused per chunk
   uint32_t* LbJ;       // [event] L_before | J << 16
+  uint8_t* cnt;        // [group][tcap rounded to 16] s2_out count tables
   uint32_t Astride;
 };
 
@@ -929,6 +947,7 @@ static void carve_stack(Carver& cv, const StackPlan& P, uint32_t ni, StackWs* w)
   const size_t abytes = P.gi ? size_t(SND) * w->Astride * (P.any_big ? 4 : 2) : 4;
   w->A = cv.take<uint32_t>((abytes + 3) / 4);
   w->LbJ = cv.take<uint32_t>(P.gi ? P.Emax + 8 : 1);
+  w->cnt = cv.take<uint8_t>(P.gi ? P.groups.size() * ((P.tcap + 15u) & ~size_t(15)) : 16);
 }
 
 tlru_status stack_workspace(const tlru_trace* traces, uint32_t nt, const tlru_instance* inst, uint32_t ni,
@@ -946,7 +965,7 @@ tlru_status stack_workspace(const tlru_trace* traces, uint32_t nt, const tlru_in
 template <int ND>
 static tlru_status launch_s2(const tlru_trace& tr, const ChunkDev* ch, const ChunkTotals* tot, const StackWs& w,
                              const StackPlan& P, uint32_t c, uint32_t bins, bool aligned, bool aligned16, uint16_t* bout,
-                             uint32_t* hist, cudaStream_t st) {
+                             uint32_t* hist, cudaStream_t st, OutTiming* ot) {
   const uint32_t E = static_cast<uint32_t>(tr.num_events);
   const uint32_t nb = (E + S_THREADS - 1) / S_THREADS;
   // 16x2 partial sums of max(L, min(D, maxL)) stay exact while wch * maxL < 2^16
@@ -969,18 +988,29 @@ static tlru_status launch_s2(const tlru_trace& tr, const ChunkDev* ch, const Chu
   uint32_t rl = (E + nr - 1) / nr;
   rl = std::min(OUT_RANGE_MAX, (rl + 1023u) & ~1023u);
   const uint32_t nranges = (E + rl - 1) / rl;
-  const size_t out_smem = size_t(P.gi) * ((bins + 1) / 2) * sizeof(uint32_t) + ((P.tcap + 3) & ~3u);
+  const size_t out_smem = ((size_t(P.gi) * ((bins + 1) / 2) + 3) & ~size_t(3)) * sizeof(uint32_t) +
+                          ((P.tcap + 15) & ~15u);
+  uint8_t* cnt_g = w.cnt + size_t(g0) * ((P.tcap + 15u) & ~15u);
   auto out = [&](auto* Aptr) -> tlru_status {
     using AT = std::remove_const_t<std::remove_pointer_t<decltype(Aptr)>>;
     s2_win_kernel<ND, AT><<<nb, S_THREADS, 0, st>>>(tr.sim, w.scanrec, E, ch, tot, wch, maxL, Aptr, w.Astride, w.LbJ);
     TLRU_CHECK_LAUNCH();
     TLRU_CUDA(cudaFuncSetAttribute(s2_out_kernel<AT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(out_smem)));
+    if (ng) {
+      s2_cnt_kernel<<<ng, 256, 0, st>>>(ch, w.insts, w.groups + g0, P.tcap, cnt_g);
+      TLRU_CHECK_LAUNCH();
+    }
     for (uint32_t r0 = 0; ng && r0 < nranges; r0 += 65535u) {  // grid.y <= 65535
+      if (ot && ot->first && ot->launches == 0) TLRU_CUDA(cudaEventRecord(ot->first, st));
       s2_out_kernel<AT><<<dim3(ng, std::min(65535u, nranges - r0)), 256, out_smem, st>>>(
           ch, w.insts, w.groups + g0, tot, Aptr, w.Astride, w.LbJ, E, rl, bins, P.gi, P.tcap, aligned16, bout, hist,
-          r0);
+          reinterpret_cast<const uint4*>(cnt_g), r0);
       TLRU_CHECK_LAUNCH();
+      if (ot && ot->last) {
+        TLRU_CUDA(cudaEventRecord(ot->last, st));
+        ++ot->launches;
+      }
     }
     return TLRU_OK;
   };
@@ -991,7 +1021,8 @@ static tlru_status launch_s2(const tlru_trace& tr, const ChunkDev* ch, const Chu
 tlru_status stack_simulate(const tlru_trace* traces, uint32_t nt, const tlru_instance* inst, uint32_t ni,
                            const uint64_t* boffs, uint16_t* bout, tlru_result* results, Carver& cv,
                            const SegDev* segs_dev, uint32_t bins, uint32_t* hist, unsigned long long* clamped,
-                           size_t ws_bytes, cudaStream_t st, unsigned* nkernels, cudaEvent_t ev_mid) {
+                           size_t ws_bytes, cudaStream_t st, unsigned* nkernels, cudaEvent_t ev_mid,
+                           OutTiming* out_timing) {
   StackPlan P;
   make_stack_plan(traces, nt, inst, ni, boffs, &P);
   StackWs w;
@@ -1031,13 +1062,13 @@ tlru_status stack_simulate(const tlru_trace* traces, uint32_t nt, const tlru_ins
     s1_totals_kernel<<<1, T_THREADS, 0, st>>>(w.chunks + c, hb, w.hist, w.hist + hb, w.blockagg, nb, w.totals + c);
     TLRU_CHECK_LAUNCH();
     switch (P.chunks[c].ndk) {
-      case 2: TLRU_TRY(launch_s2<2>(tr, w.chunks + c, w.totals + c, w, P, c, bins, aligned, aligned16, bout, hist, st)); break;
-      case 4: TLRU_TRY(launch_s2<4>(tr, w.chunks + c, w.totals + c, w, P, c, bins, aligned, aligned16, bout, hist, st)); break;
-      case 8: TLRU_TRY(launch_s2<8>(tr, w.chunks + c, w.totals + c, w, P, c, bins, aligned, aligned16, bout, hist, st)); break;
-      case 12: TLRU_TRY(launch_s2<12>(tr, w.chunks + c, w.totals + c, w, P, c, bins, aligned, aligned16, bout, hist, st)); break;
-      case 16: TLRU_TRY(launch_s2<16>(tr, w.chunks + c, w.totals + c, w, P, c, bins, aligned, aligned16, bout, hist, st)); break;
-      case 20: TLRU_TRY(launch_s2<20>(tr, w.chunks + c, w.totals + c, w, P, c, bins, aligned, aligned16, bout, hist, st)); break;
-      default: TLRU_TRY(launch_s2<24>(tr, w.chunks + c, w.totals + c, w, P, c, bins, aligned, aligned16, bout, hist, st)); break;
+      case 2: TLRU_TRY(launch_s2<2>(tr, w.chunks + c, w.totals + c, w, P, c, bins, aligned, aligned16, bout, hist, st, out_timing)); break;
+      case 4: TLRU_TRY(launch_s2<4>(tr, w.chunks + c, w.totals + c, w, P, c, bins, aligned, aligned16, bout, hist, st, out_timing)); break;
+      case 8: TLRU_TRY(launch_s2<8>(tr, w.chunks + c, w.totals + c, w, P, c, bins, aligned, aligned16, bout, hist, st, out_timing)); break;
+      case 12: TLRU_TRY(launch_s2<12>(tr, w.chunks + c, w.totals + c, w, P, c, bins, aligned, aligned16, bout, hist, st, out_timing)); break;
+      case 16: TLRU_TRY(launch_s2<16>(tr, w.chunks + c, w.totals + c, w, P, c, bins, aligned, aligned16, bout, hist, st, out_timing)); break;
+      case 20: TLRU_TRY(launch_s2<20>(tr, w.chunks + c, w.totals + c, w, P, c, bins, aligned, aligned16, bout, hist, st, out_timing)); break;
+      default: TLRU_TRY(launch_s2<24>(tr, w.chunks + c, w.totals + c, w, P, c, bins, aligned, aligned16, bout, hist, st, out_timing)); break;
     }
     *nkernels += 4;
   }
