@@ -311,6 +311,43 @@ def test_config5_bench_launch_sampled(T):
                 assert all(a >= b for a, b in zip(sums, sums[1:]))
 
 
+def test_config5_stratified(T):
+    """SURVEY 8(d) full-sweep parity: a stratified sample with >= 1 instance per (C, policy)
+    and per (xi, policy) of the config-5 grid, checked element by element against the oracle
+    (seed 0, all 1000 of its instances in the bench's one-trace launch; 50 oracle replays on
+    host threads -- the oracle's ctypes calls release the GIL)."""
+    import os
+    from concurrent.futures import ThreadPoolExecutor
+    T.set_sim_engine(T.ENGINE_STACK)
+    p = preset("wildchat", 0, 1_000_000)
+    g = T.generate_traces([p], exports=False)[0]
+    o = O.generate(p)
+    assert g.num_events == o.E
+    rows = [(0,) + tuple(r[1:]) for r in config5_rows(1)]
+    bt = T.simulate_batch([g], rows)
+    res = bt.results_numpy()
+    key = {r: i for i, r in enumerate(rows)}
+    picks = [key[(0, pol, C, XI_CONFIG5[(k + 7 * pol) % len(XI_CONFIG5)], Q_HAT, SLO_BLOCKS)]
+             for pol in (0, 1) for k, C in enumerate(CAPS_CONFIG5)]
+    assert {(rows[i][1], rows[i][3]) for i in picks} == {(pol, xi) for pol in (0, 1) for xi in XI_CONFIG5}
+
+    def one(i):
+        _, pol, C, xi, qh, slo = rows[i]
+        return i, O.replay(o.conv, o.q, o.a, pol, C, xi, qh)
+
+    with ThreadPoolExecutor(max_workers=max(1, min(len(picks), os.cpu_count() or 1))) as ex:
+        for i, r in ex.map(one, picks):
+            _, pol, C, xi, qh, slo = rows[i]
+            assert np.array_equal(bt.b(i).astype(np.uint64), r.b), rows[i]
+            tl = O.tail(r.b, xi, ALPHA_MS * xi, slo, ALPHA_MS)
+            got = res[i]
+            assert (got["sum_uncached"], got["tel_blocks"], got["slo_violations"]) == \
+                (tl.sum_b, tl.tel_blocks, tl.slo_violations), rows[i]
+            assert (got["p50"], got["p90"], got["p95"], got["p99"]) == (tl.p50, tl.p90, tl.p95, tl.p99), rows[i]
+            assert (got["evicted_trim"], got["evicted_lru"], got["max_occupancy"]) == \
+                (r.evicted_trim, r.evicted_lru, r.max_occupancy), rows[i]
+
+
 # ----------------------------------------------------------------------------- tail metrics
 def test_tail_metrics_against_oracle(T):
     rng = np.random.default_rng(4)
