@@ -155,11 +155,16 @@ tlru_status tlru_trace_from_turns(const uint32_t* conv, const uint16_t* q, const
  *   Phase 2: evict from the least recently used conversation,
  *     partially, tail blocks first (Reading #10).
  * LRU = Phase 2 only.  xi and Q_hat are in blocks (xi = xi_s / alpha).
+ * Threshold-LRU (the paper's baseline): LRU that caches a
+ *   conversation's history only once its length reaches `threshold` blocks
+ *   (L_after >= threshold, Reading #23): below it nothing is cached (b = J),
+ *   at or above it the whole history is cached and evicted by plain LRU.
  * ------------------------------------------------------------------------ */
 enum {
   TLRU_POLICY_LRU = 0,
-  TLRU_POLICY_TLRU = 1
-  /* 2..5 reserved: THRESHOLD_LRU, END_AWARE, LENGTH_AWARE, TAIL_BELADY -> TLRU_EUNSUPPORTED */
+  TLRU_POLICY_TLRU = 1,
+  TLRU_POLICY_THRESHOLD = 2
+  /* 3..5 reserved: END_AWARE, LENGTH_AWARE, TAIL_BELADY -> TLRU_EUNSUPPORTED */
 };
 
 typedef struct {
@@ -169,6 +174,8 @@ typedef struct {
   uint32_t xi;       /* xi in blocks: T-LRU threshold and TEL threshold (Eq. 3) */
   uint32_t q_hat;    /* Q_hat in blocks, next-prompt estimate */
   uint32_t slo;      /* SLO violation iff b > slo (strict); 16 = 200 ms at 12.5 ms/block */
+  uint32_t threshold; /* TLRU_POLICY_THRESHOLD: admission threshold in blocks (1024 tokens = 8 blocks
+                         of 128); ignored by the other policies */
 } tlru_instance;
 
 typedef struct { /* 72 B, all exact integers */

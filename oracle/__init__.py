@@ -65,7 +65,7 @@ def lib():
         L.oracle_derive.argtypes = [u32p, u32p, u32p, ctypes.c_uint64, u32p, u64p, u64p, u32p]
         L.oracle_derive.restype = ctypes.c_int
         L.oracle_replay.argtypes = [u32p, u32p, u32p, ctypes.c_uint64, ctypes.c_int, ctypes.c_uint64,
-                                    ctypes.c_uint64, ctypes.c_uint64, u64p, u64p]
+                                    ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, u64p, u64p]
         L.oracle_replay.restype = ctypes.c_int
         L.oracle_tail.argtypes = [u64p, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_double, ctypes.c_uint64,
                                   ctypes.c_double, u64p, ctypes.POINTER(ctypes.c_double)]
@@ -187,6 +187,7 @@ def derive(conv, q, a) -> Derived:
 
 LRU = 0
 TLRU = 1
+THRESHOLD = 2
 
 
 @dataclass
@@ -197,8 +198,9 @@ class Replay:
     max_occupancy: int
 
 
-def replay(conv, q, a, policy: int, C: int, xi: int = 0, q_hat: int = 0) -> Replay:
-    """Alg. 1 replay of one instance; LRU = Phase 2 only."""
+def replay(conv, q, a, policy: int, C: int, xi: int = 0, q_hat: int = 0, threshold: int = 0) -> Replay:
+    """Alg. 1 replay of one instance; LRU = Phase 2 only; policy 2 =
+    Threshold-LRU with admission threshold `threshold` blocks."""
     conv = np.ascontiguousarray(conv, dtype=np.uint32)
     q = np.ascontiguousarray(q, dtype=np.uint32)
     a = np.ascontiguousarray(a, dtype=np.uint32)
@@ -206,7 +208,7 @@ def replay(conv, q, a, policy: int, C: int, xi: int = 0, q_hat: int = 0) -> Repl
     b = np.zeros(E, np.uint64)
     cnt = np.zeros(3, np.uint64)
     rc = lib().oracle_replay(_p(conv, ctypes.c_uint32), _p(q, ctypes.c_uint32), _p(a, ctypes.c_uint32), E,
-                             int(policy), int(C), int(xi), int(q_hat), _p(b, ctypes.c_uint64),
+                             int(policy), int(C), int(xi), int(q_hat), int(threshold), _p(b, ctypes.c_uint64),
                              _p(cnt, ctypes.c_uint64))
     if rc != 0:
         raise MemoryError("oracle_replay")

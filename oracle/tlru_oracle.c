@@ -371,11 +371,13 @@ static void list_push_tail(conv_state* s, list_ends* l, int which, int64_t i) {
     l->tail = i;
 }
 
-/* policy: 0 = LRU, 1 = T-LRU.  b_out[E] receives the uncached blocks of each
-   request (u64).  counters_out[3] = {evicted_trim, evicted_lru, max_occupancy}.
-   Returns 0, or -1 on allocation failure. */
+/* policy: 0 = LRU, 1 = T-LRU, 2 = Threshold-LRU (LRU that caches a
+   conversation's history only when its length reaches `threshold` blocks; below it
+   nothing is cached -- Reading #23: L_after >= threshold).  b_out[E] receives the
+   uncached blocks of each request (u64).  counters_out[3] = {evicted_trim,
+   evicted_lru, max_occupancy}.  Returns 0, or -1 on allocation failure. */
 int oracle_replay(const uint32_t* conv, const uint32_t* q, const uint32_t* a, uint64_t E,
-                  int policy, uint64_t C, uint64_t xi, uint64_t q_hat,
+                  int policy, uint64_t C, uint64_t xi, uint64_t q_hat, uint64_t threshold,
                   uint64_t* b_out, uint64_t* counters_out) {
     uint32_t* dense = (uint32_t*)malloc((E ? E : 1) * 4);
     if (!dense) return -1;
@@ -398,6 +400,12 @@ int oracle_replay(const uint32_t* conv, const uint32_t* q, const uint32_t* a, ui
         /* Alg. 1 line 1: L_theta <- L', X_theta <- L_theta, tau_theta <- now.
            Optional caching caches the whole history incl. the response (Reading #7). */
         uint64_t L_after = J + a[t];
+        if (policy == 2 && L_after < threshold) {
+            /* Threshold-LRU below the threshold: the history is not cached at all.  L
+               never decreases, so this conversation was never admitted: X = 0, b = J. */
+            s[c].L = L_after;
+            continue;
+        }
         used = used - s[c].X + L_after;
         s[c].X = L_after;
         s[c].L = L_after;

@@ -67,7 +67,7 @@ class Trace(ctypes.Structure):
 
 
 class Instance(ctypes.Structure):
-    _fields_ = [(n, ctypes.c_uint32) for n in ("trace", "policy", "capacity", "xi", "q_hat", "slo")]
+    _fields_ = [(n, ctypes.c_uint32) for n in ("trace", "policy", "capacity", "xi", "q_hat", "slo", "threshold")]
 
 
 from .abi_types import RESULT_DTYPE, TAIL_DTYPE  # noqa: E402  (pure-python mirrors of the header)

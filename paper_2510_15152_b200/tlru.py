@@ -141,11 +141,11 @@ def trace_from_turns(conv: torch.Tensor, q: torch.Tensor, a: torch.Tensor, expor
 
 
 def instances_array(rows) -> "ctypes.Array":
-    """rows: iterable of (trace, policy, capacity, xi, q_hat, slo)."""
+    """rows: iterable of (trace, policy, capacity, xi, q_hat, slo[, threshold])."""
     rows = list(rows)
     arr = (Instance * max(len(rows), 1))()
     for i, r in enumerate(rows):
-        for k, v in zip(("trace", "policy", "capacity", "xi", "q_hat", "slo"), r):
+        for k, v in zip(("trace", "policy", "capacity", "xi", "q_hat", "slo", "threshold"), r):
             setattr(arr[i], k, int(v))
     return arr
 

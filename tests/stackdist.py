@@ -37,3 +37,23 @@ def topc_replay(conv, q, a, C: int, D: int):
         L[c] = L.get(c, 0) + qq + aa
         tau[c] = t
     return out
+
+
+def topc_replay_threshold(conv, q, a, C: int, T: int):
+    """Threshold-LRU in the same closed form: LRU over the admitted blocks,
+    i.e. conversation weights w_j = L_j if L_j >= T else 0 (Reading #23), so
+    X_theta = min(w_theta, (C - sum of w_j over conversations used after theta's
+    previous turn)^+).  T = 0 is the LRU closed form above."""
+    L: dict[int, int] = {}
+    tau: dict[int, int] = {}
+    out = []
+    w = lambda v: v if v >= T else 0  # noqa: E731
+    for t, (c, qq, aa) in enumerate(zip(conv.tolist(), q.tolist(), a.tolist())):
+        X = 0
+        if c in L:
+            s = sum(w(L[j]) for j in L if j != c and tau[j] > tau[c])
+            X = min(w(L[c]), max(C - s, 0))
+        out.append(L.get(c, 0) + qq - X)
+        L[c] = L.get(c, 0) + qq + aa
+        tau[c] = t
+    return out
