@@ -16,6 +16,7 @@ LIB_PATH = os.path.join(HERE, "libtlru.so")
 TLRU_NONE = 0xFFFFFFFF
 POLICY_LRU = 0
 POLICY_TLRU = 1
+POLICY_THRESHOLD = 2
 ENGINE_REPLAY = 0
 ENGINE_STACK = 1
 

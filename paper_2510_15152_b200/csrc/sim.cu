@@ -26,7 +26,7 @@ namespace tlru {
 struct LaneDev {
   uint32_t inst;  // instance index, 0xFFFFFFFF = idle lane
   uint32_t C, D;
-  uint32_t pad;
+  uint32_t T;     // Threshold-LRU admission threshold (0: LRU / T-LRU)
   uint64_t boff;  // offset of the instance's b array in `uncached`
 };
 
@@ -91,7 +91,7 @@ __global__ void __launch_bounds__(32) sim_kernel(const ItemDev* __restrict__ ite
   bool active = lp.inst != 0xFFFFFFFFu;
   SmemState st{tau_s, X_s, lane};
   ChainRegs c;
-  chain_init(c, lp.C, lp.D, W, active && s > 0);
+  chain_init(c, lp.C, lp.D, lp.T, W, active && s > 0);
 
   // ---- rebuild the exact state at s (sim.cuh "Segment start")
   for (int pass = 0; pass < 2; ++pass) {
@@ -166,7 +166,7 @@ __global__ void sim_spill_kernel(const GroupDev* __restrict__ groups, const Lane
     const uint64_t slot = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
     GlobalState st{tau_pool + slot * W_big, X_pool + slot * W_big};
     ChainRegs c;
-    chain_init(c, lp.C, lp.D, W_big, s > 0);
+    chain_init(c, lp.C, lp.D, lp.T, W_big, s > 0);
     for (int pass = 0; pass < 2; ++pass) {
       for (int64_t e = int64_t(s) - 1; e >= 0 && c.walking; --e) {
         if (tr.next[e] >= s) chain_walk_step(c, st, static_cast<uint32_t>(e), sim_La(tr.sim[e]));
@@ -253,8 +253,11 @@ static tlru_status make_plan(const tlru_trace* traces, uint32_t nt, const tlru_i
   for (uint32_t i = 0; i < ni; ++i) {
     const tlru_instance& in = inst[i];
     if (in.trace >= nt) TLRU_FAIL(TLRU_EINVAL, "instance %u: trace index %u out of range", i, in.trace);
-    if (in.policy != TLRU_POLICY_LRU && in.policy != TLRU_POLICY_TLRU)
-      TLRU_FAIL(TLRU_EUNSUPPORTED, "instance %u: policy %u is not built (LRU = 0, T-LRU = 1)", i, in.policy);
+    if (in.policy != TLRU_POLICY_LRU && in.policy != TLRU_POLICY_TLRU && in.policy != TLRU_POLICY_THRESHOLD)
+      TLRU_FAIL(TLRU_EUNSUPPORTED, "instance %u: policy %u is not built (LRU = 0, T-LRU = 1, Threshold-LRU = 2)", i,
+                in.policy);
+    if (in.policy == TLRU_POLICY_THRESHOLD && in.threshold > 65535)
+      TLRU_FAIL(TLRU_ERANGE, "instance %u: threshold %u > 65535 (histories are u16)", i, in.threshold);
     order[i] = i;
     const uint32_t C = std::min<uint32_t>(in.capacity, 0x7FFF0000u);
     wc[i] = g_opt_w >= 0 ? g_opt_w : w_class(C, traces[in.trace].num_conversations);
@@ -279,7 +282,7 @@ static tlru_status make_plan(const tlru_trace* traces, uint32_t nt, const tlru_i
       l.inst = order[k];
       l.C = std::min<uint32_t>(in.capacity, 0x7FFF0000u);
       l.D = (in.policy == TLRU_POLICY_TLRU && in.xi > in.q_hat) ? in.xi - in.q_hat : 0u;  // free tail
-      l.pad = 0;
+      l.T = in.policy == TLRU_POLICY_THRESHOLD ? in.threshold : 0u;  // admission (Reading #23)
       l.boff = P->segs[order[k]].begin;
       P->lanes.push_back(l);
       ++g.nlanes;

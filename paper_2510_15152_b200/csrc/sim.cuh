@@ -23,6 +23,8 @@
 // max(L - D, 0) most-recent-first until C is reached; only if the whole prefix
 // holds fewer than C non-free blocks are free blocks min(L, D) granted too
 // (second walk, most-recent-first).
+// Threshold-LRU (D = 0): only admitted histories (L >= T) hold blocks, so the walk grants
+// L [L >= T] per conversation (the same top-C argument over the admitted universe).
 #pragma once
 
 #include <stdint.h>
@@ -51,16 +53,18 @@ struct GlobalState {
 
 struct ChainRegs {
   uint32_t head, tail, fh, frem;
-  uint32_t used, C, D, W;
+  uint32_t used, C, D, T, W;  // T: Threshold-LRU admission threshold (0 for LRU / T-LRU)
   uint32_t ev_trim, ev_lru, max_occ;
   // warm-start bookkeeping
   uint32_t r, cum_nf, cum_f, nf_target, free_budget, fh_pos, fh_rem;
   bool walking, overflow;
 };
 
-__device__ __forceinline__ void chain_init(ChainRegs& c, uint32_t C, uint32_t D, uint32_t W, bool has_prefix) {
+__device__ __forceinline__ void chain_init(ChainRegs& c, uint32_t C, uint32_t D, uint32_t T, uint32_t W,
+                                           bool has_prefix) {
   c.C = C;
   c.D = D;
+  c.T = T;
   c.W = W;
   c.head = c.tail = W;
   c.fh = W;
@@ -80,7 +84,7 @@ __device__ __forceinline__ void chain_init(ChainRegs& c, uint32_t C, uint32_t D,
 // next[e'] >= s (the last turn of its conversation before s) and L_after = la.
 template <class St>
 __device__ __forceinline__ void chain_walk_step(ChainRegs& c, const St& st, uint32_t e_prime, uint32_t la) {
-  uint32_t nf = la > c.D ? la - c.D : 0u;  // non-free blocks max(L - D, 0)
+  uint32_t nf = (la >= c.T && la > c.D) ? la - c.D : 0u;  // non-free blocks max(L - D, 0), admitted only
   uint32_t f = la < c.D ? la : c.D;        // free blocks min(L, D)
   uint32_t x = min(nf, c.nf_target - c.cum_nf);
   uint32_t y = min(f, c.free_budget - c.cum_f);
@@ -186,6 +190,9 @@ __device__ __forceinline__ uint32_t chain_request(ChainRegs& c, const St& st, ui
     }
   }
   const uint32_t b = J - x_old;
+  // Threshold-LRU: a history below the threshold is not cached (L never
+  // decreases, so theta had no entry either: x_old = 0)
+  if (La < c.T) return b;
   if (c.tail == c.W) {
     if (!chain_compact(c, st)) {
       c.overflow = true;

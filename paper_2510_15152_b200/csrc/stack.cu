@@ -62,7 +62,9 @@ struct ChunkDev {
   uint32_t Cmax[SND];      // largest capacity among the chunk's instances with this D
   uint32_t dbeg[SND + 1];  // instances of D[d]: [inst0 + dbeg[d], inst0 + dbeg[d+1]), sorted by C
   uint32_t dbig[SND];      // first instance of D[d] with C > 65535 (packed 16x2 path before it)
-  uint32_t nd;             // real D values (the rest pad with D[0] and own no instances)
+  uint32_t T[SND];         // Threshold-LRU admission threshold of the row (0: LRU / T-LRU row)
+  uint32_t nd;             // real rows (the rest pad with row 0 and own no instances)
+  uint32_t anyT;           // some row has T > 0
   uint32_t inst0, ninst;   // instances [inst0, inst0 + ninst) of the StackInstDev table
 };
 
@@ -76,12 +78,17 @@ struct ChunkTotals {  // per chunk: exact trace totals
   unsigned long long nfE[SND];   // NF_all(E): non-free blocks of the final universe
   unsigned long long fE[SND];    // F_all(E)
   unsigned long long suma;       // sum_e a_e
+  unsigned long long suma_adm[SND];  // T rows: sum of a over admitted events (L_after >= T)
+  unsigned long long sumJ_na[SND];   // T rows: sum of J over the other events (b = J there)
   uint32_t nsat[SND];            // first 256-event block where NF_all(D[d]) >= Cmax[d]
   uint32_t nsat_min, nsat_max;   // over the real D values
 };
 
 __device__ __forceinline__ uint32_t nf_of(uint32_t L, uint32_t D) { return L > D ? L - D : 0u; }
 __device__ __forceinline__ uint32_t f_of(uint32_t L, uint32_t D) { return L < D ? L : D; }
+// Cached-by-recency weight of a history of length L in a row (D, T): NF(L) = max(L - D, 0), and
+// for Threshold-LRU rows (D = 0, T > 0) only admitted histories count: L [L >= T] (Reading #23).
+__device__ __forceinline__ uint32_t nft(uint32_t L, uint32_t D, uint32_t T) { return L >= T ? nf_of(L, D) : 0u; }
 __device__ __forceinline__ uint32_t sat_sub(uint32_t a, uint32_t b) { return a > b ? a - b : 0u; }
 
 __device__ __forceinline__ uint32_t L_before(const uint64_t* sim, uint64_t s) {
@@ -101,23 +108,30 @@ __global__ void __launch_bounds__(S_THREADS) s1_block_kernel(const uint64_t* __r
                                                              ChunkTotals* totals) {
   extern __shared__ uint32_t sh[];  // [2 * bins] when bins fit, else unused
   __shared__ uint32_t wsum[S_THREADS / 32][SND];
-  __shared__ uint32_t Ds[SND];
+  __shared__ uint32_t Ds[SND], Ts[SND];
+  __shared__ unsigned long long acc_a[SND], acc_j[SND];  // T rows: admitted a, non-admitted J
   const bool smem_hist = bins <= 8192;
   uint32_t* ha = smem_hist ? sh : hist_all;
   uint32_t* hl = smem_hist ? sh + bins : hist_last;
   if (smem_hist)
     for (uint32_t k = threadIdx.x; k < 2 * bins; k += S_THREADS) sh[k] = 0;
-  if (threadIdx.x < SND) Ds[threadIdx.x] = chunk->D[threadIdx.x];
+  if (threadIdx.x < SND) {
+    Ds[threadIdx.x] = chunk->D[threadIdx.x];
+    Ts[threadIdx.x] = chunk->T[threadIdx.x];
+    acc_a[threadIdx.x] = acc_j[threadIdx.x] = 0ull;
+  }
   const uint32_t nd = chunk->nd;
+  const bool anyT = chunk->anyT != 0;
   __syncthreads();
   unsigned long long sa = 0;
   const uint32_t nblocks = (E + S_THREADS - 1) / S_THREADS;
   const uint32_t warp = threadIdx.x / 32, lane = threadIdx.x & 31;
   for (uint32_t blk = blockIdx.x; blk < nblocks; blk += gridDim.x) {
     const uint32_t e = blk * S_THREADS + threadIdx.x;
-    uint32_t La = 0, Lb = 0;
+    uint32_t La = 0, Lb = 0, Jv = 0;
     if (e < E) {
       const uint64_t s = __ldg(sim + e);
+      Jv = sim_J(s);
       const uint32_t nx = __ldg(next + e);
       La = sim_La(s);
       Lb = L_before(sim, s);
@@ -126,10 +140,21 @@ __global__ void __launch_bounds__(S_THREADS) s1_block_kernel(const uint64_t* __r
       atomicAdd(&ha[La], 1u);
       if (nx == TLRU_NONE) atomicAdd(&hl[La], 1u);
     }
-    for (uint32_t d = 0; d < nd; ++d) {  // growth of NF_all for D[d]; <= 256 * 65535: no overflow
-      const uint32_t v = __reduce_add_sync(0xFFFFFFFFu, nf_of(La, Ds[d]) - nf_of(Lb, Ds[d]));
+    for (uint32_t d = 0; d < nd; ++d) {  // growth of NF_all for row d; <= 256 * 65535: no overflow
+      const uint32_t v = __reduce_add_sync(0xFFFFFFFFu, nft(La, Ds[d], Ts[d]) - nft(Lb, Ds[d], Ts[d]));
       if (lane == 0) wsum[warp][d] = v;
     }
+    if (anyT)
+      for (uint32_t d = 0; d < nd; ++d) {  // Threshold-LRU rows: inputs of the eviction identity
+        if (Ts[d] == 0) continue;
+        const bool adm = La >= Ts[d];
+        const uint32_t va = __reduce_add_sync(0xFFFFFFFFu, (e < E && adm) ? La - Jv : 0u);
+        const uint32_t vj = __reduce_add_sync(0xFFFFFFFFu, (e < E && !adm) ? Jv : 0u);
+        if (lane == 0) {
+          if (va) atomicAdd(&acc_a[d], static_cast<unsigned long long>(va));
+          if (vj) atomicAdd(&acc_j[d], static_cast<unsigned long long>(vj));
+        }
+      }
     __syncthreads();
     if (threadIdx.x < nd) {
       uint32_t v = 0;
@@ -148,6 +173,13 @@ __global__ void __launch_bounds__(S_THREADS) s1_block_kernel(const uint64_t* __r
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) sa += __shfl_xor_sync(0xFFFFFFFFu, sa, o);
   if (lane == 0 && sa) atomicAdd(&totals->suma, sa);
+  if (anyT) {
+    __syncthreads();
+    if (threadIdx.x < nd && Ts[threadIdx.x]) {
+      if (acc_a[threadIdx.x]) atomicAdd(&totals->suma_adm[threadIdx.x], acc_a[threadIdx.x]);
+      if (acc_j[threadIdx.x]) atomicAdd(&totals->sumJ_na[threadIdx.x], acc_j[threadIdx.x]);
+    }
+  }
 }
 
 // One CTA: exact totals per D from the L_after histograms; then, one warp per D, the block
@@ -165,12 +197,12 @@ __global__ void __launch_bounds__(T_THREADS) s1_totals_kernel(const ChunkDev* __
   __shared__ uint32_t ns_s[SND];
   const ChunkDev& ch = *chunk;
   for (int d = 0; d < SND; ++d) {
-    const uint32_t D = ch.D[d];
+    const uint32_t D = ch.D[d], Tt = ch.T[d];
     unsigned long long sF = 0, nE = 0, fE = 0;
     for (uint32_t L = threadIdx.x; L < bins; L += T_THREADS) {
       const unsigned long long a = hist_all[L], l = hist_last[L];
       sF += a * f_of(L, D);
-      nE += l * nf_of(L, D);
+      nE += l * nft(L, D, Tt);
       fE += l * f_of(L, D);
     }
     sF = BR(red).Sum(sF);
@@ -229,15 +261,20 @@ __global__ void __launch_bounds__(T_THREADS) s1_totals_kernel(const ChunkDev* __
 // ----------------------------------------------------------------------------- s2 common
 // Phase B of both s2 kernels: each thread takes window chunks `it` of the block and
 // accumulates, branch-free, sum L and sum max(L, Deff) per D pair over the chunk.
-template <int ND, bool WITH_F>
+// HT: the chunk has Threshold-LRU rows; element L then counts only where L >= T (T = 0 on the
+// other rows), and those rows (D = 0) have no free blocks.
+template <int ND, bool WITH_F, bool HT>
 __device__ __forceinline__ void window_phase(const uint64_t* __restrict__ scanrec, uint32_t e0, uint32_t wch,
                                              const uint32_t* p_s, const uint32_t* cbeg_s, uint32_t ntot,
-                                             const uint32_t* Deff, uint32_t (*anf_s)[S_THREADS],
-                                             uint32_t (*af_s)[S_THREADS]) {
+                                             const uint32_t* Deff, const uint32_t* Tr,
+                                             uint32_t (*anf_s)[S_THREADS], uint32_t (*af_s)[S_THREADS]) {
   constexpr int NP = (ND + 1) / 2;
-  uint32_t Dpk[NP];
+  uint32_t Dpk[NP], Tpk[NP];
 #pragma unroll
-  for (int q = 0; q < NP; ++q) Dpk[q] = Deff[2 * q] | (Deff[min(2 * q + 1, ND - 1)] << 16);
+  for (int q = 0; q < NP; ++q) {
+    Dpk[q] = Deff[2 * q] | (Deff[min(2 * q + 1, ND - 1)] << 16);
+    Tpk[q] = HT ? (Tr[2 * q] | (Tr[min(2 * q + 1, ND - 1)] << 16)) : 0u;  // T <= 65535 (validated)
+  }
   for (uint32_t it = threadIdx.x; it < ntot; it += S_THREADS) {
     uint32_t lo = 0, hi = S_THREADS;  // owner event: last j with cbeg_s[j] <= it
     while (hi - lo > 1) {
@@ -258,7 +295,10 @@ __device__ __forceinline__ void window_phase(const uint64_t* __restrict__ scanre
       if (WITH_F) sumL += L;
       const uint32_t L2 = L * 0x10001u;  // L in both 16-bit halves
 #pragma unroll
-      for (int q = 0; q < NP; ++q) mx2[q] = __vadd2(mx2[q], __vmaxu2(L2, Dpk[q]));
+      for (int q = 0; q < NP; ++q) {
+        if (HT) mx2[q] = __vadd2(mx2[q], __vmaxu2(L2, Dpk[q]) & __vcmpgeu2(L2, Tpk[q]));
+        else mx2[q] = __vadd2(mx2[q], __vmaxu2(L2, Dpk[q]));
+      }
     }
     const uint32_t n = top + 1 - bot;
 #pragma unroll
@@ -270,7 +310,7 @@ __device__ __forceinline__ void window_phase(const uint64_t* __restrict__ scanre
           const uint32_t smax = h ? (mx2[q] >> 16) : (mx2[q] & 0xFFFFu);
           const uint32_t nD = n * Deff[d];
           atomicAdd(&anf_s[d][j], smax - nD);
-          if (WITH_F) atomicAdd(&af_s[d][j], sumL + nD - smax);
+          if (WITH_F && !(HT && Tr[d] > 0)) atomicAdd(&af_s[d][j], sumL + nD - smax);
         }
       }
     }
@@ -326,7 +366,7 @@ struct InstTileW {
 };
 
 // ----------------------------------------------------------------------------- s2_sat
-template <int ND>
+template <int ND, bool HT>
 __global__ void __launch_bounds__(S_THREADS, 4) s2_sat_kernel(const uint64_t* __restrict__ sim,
                                                               const uint64_t* __restrict__ scanrec, uint32_t E,
                                                               const ChunkDev* __restrict__ chunk,
@@ -359,7 +399,7 @@ __global__ void __launch_bounds__(S_THREADS, 4) s2_sat_kernel(const uint64_t* __
   uint32_t Deff[ND];
 #pragma unroll
   for (int d = 0; d < ND; ++d) Deff[d] = min(ch.D[d], maxL);
-  window_phase<ND, false>(scanrec, e0, wch, p_s, cbeg_s, ntot, Deff, anf_s, nullptr);
+  window_phase<ND, false, HT>(scanrec, e0, wch, p_s, cbeg_s, ntot, Deff, ch.T, anf_s, nullptr);
   // ---- C: per-instance b; X = min(NF(Lb), (C - A_nf)^+) (no free block is cached here)
   const uint32_t quad = t & 63, lane4 = t >> 6;
   const uint32_t j0 = quad * 4;
@@ -388,7 +428,7 @@ __global__ void __launch_bounds__(S_THREADS, 4) s2_sat_kernel(const uint64_t* __
       uint32_t nfb[4], anf[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        nfb[u] = p_s[j0 + u] != TLRU_NONE ? nf_of(Lb_s[j0 + u], ch.D[d]) : 0u;
+        nfb[u] = p_s[j0 + u] != TLRU_NONE ? nft(Lb_s[j0 + u], ch.D[d], ch.T[d]) : 0u;
         anf[u] = anf_s[d][j0 + u];
       }
       // packed 16x2: X = min(nfb, max(C, A) - A), A clamped to 65535 (exact for C <= 65535)
@@ -427,7 +467,7 @@ __global__ void __launch_bounds__(S_THREADS, 4) s2_sat_kernel(const uint64_t* __
 // ----------------------------------------------------------------------------- s2_warm
 // Blocks before nsat: exact NF_all(e) per D (sum of the universe deltas of every earlier event)
 // and the free-block term.  Few blocks, so this kernel favours simplicity; dynamic shared memory.
-template <int ND>
+template <int ND, bool HT>
 __global__ void __launch_bounds__(S_THREADS) s2_warm_kernel(const uint64_t* __restrict__ sim,
                                                             const uint64_t* __restrict__ scanrec, uint32_t E,
                                                             const ChunkDev* __restrict__ chunk,
@@ -463,7 +503,7 @@ __global__ void __launch_bounds__(S_THREADS) s2_warm_kernel(const uint64_t* __re
 #pragma unroll 1
     for (int d = 0; d < ND; ++d) {
       if (blk >= nsat_s[d] || d >= static_cast<int>(ch.nd)) continue;  // uniform across the block
-      const uint32_t delta = (e0 + t < E) ? nf_of(La_t, ch.D[d]) - nf_of(Lb, ch.D[d]) : 0u;
+      const uint32_t delta = (e0 + t < E) ? nft(La_t, ch.D[d], ch.T[d]) - nft(Lb, ch.D[d], ch.T[d]) : 0u;
       uint32_t ex;
       BSu(scan).ExclusiveSum(delta, ex);
       nfall_s[d][t] = blockpre[uint64_t(blk) * SND + d] + ex;  // < Cmax[d] + 256 * 65535
@@ -472,7 +512,7 @@ __global__ void __launch_bounds__(S_THREADS) s2_warm_kernel(const uint64_t* __re
     uint32_t Deff[ND];
 #pragma unroll
     for (int d = 0; d < ND; ++d) Deff[d] = min(ch.D[d], maxL);
-    window_phase<ND, true>(scanrec, e0, wch, p_s, cbeg_s, ntot, Deff, anf_s, af_s);
+    window_phase<ND, true, HT>(scanrec, e0, wch, p_s, cbeg_s, ntot, Deff, ch.T, anf_s, af_s);
     __syncthreads();
     // phase C for the D values still in warm-up: 4 events per thread, instance stride 4, the
     // instance table staged in shared memory (as in s2_sat), general formula with free blocks
@@ -496,7 +536,7 @@ __global__ void __launch_bounds__(S_THREADS) s2_warm_kernel(const uint64_t* __re
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const bool hit = p_s[j0 + u] != TLRU_NONE;
-          nfb[u] = hit ? nf_of(Lb_s[j0 + u], ch.D[d]) : 0u;
+          nfb[u] = hit ? nft(Lb_s[j0 + u], ch.D[d], ch.T[d]) : 0u;
           fb[u] = hit ? f_of(Lb_s[j0 + u], ch.D[d]) : 0u;
           anf[u] = anf_s[d][j0 + u];
           af[u] = af_s[d][j0 + u];
@@ -530,7 +570,7 @@ __global__ void __launch_bounds__(S_THREADS) s2_warm_kernel(const uint64_t* __re
 // s2_win: phases A and B of s2_sat for every block from nsat_min on, writing the window sums
 // A_nf (clamped to AT's range; AT = u16 when every capacity of the chunk is <= 65535) and
 // (L_before | J << 16) per event, so the per-instance work can run instance-group-major.
-template <int ND, typename AT>
+template <int ND, typename AT, bool HT>
 __global__ void __launch_bounds__(S_THREADS, 4) s2_win_kernel(const uint64_t* __restrict__ sim,
                                                               const uint64_t* __restrict__ scanrec, uint32_t E,
                                                               const ChunkDev* __restrict__ chunk,
@@ -555,7 +595,7 @@ __global__ void __launch_bounds__(S_THREADS, 4) s2_win_kernel(const uint64_t* __
   uint32_t Deff[ND];
 #pragma unroll
   for (int d = 0; d < ND; ++d) Deff[d] = min(ch.D[d], maxL);
-  window_phase<ND, false>(scanrec, e0, wch, p_s, cbeg_s, ntot, Deff, anf_s, nullptr);
+  window_phase<ND, false, HT>(scanrec, e0, wch, p_s, cbeg_s, ntot, Deff, ch.T, anf_s, nullptr);
   __syncthreads();
   const uint32_t e = e0 + t;
   if (e >= E) return;
@@ -598,7 +638,7 @@ __global__ void __launch_bounds__(256) s2_cnt_kernel(const ChunkDev* __restrict_
   }
 }
 
-template <typename AT>
+template <typename AT, bool HT>
 __global__ void __launch_bounds__(256, 4) s2_out_kernel(const ChunkDev* __restrict__ chunk,
                                                      const StackInstDev* __restrict__ insts,
                                                      const GroupDev* __restrict__ groups,
@@ -666,6 +706,7 @@ __global__ void __launch_bounds__(256, 4) s2_out_kernel(const ChunkDev* __restri
   constexpr uint32_t EV = 8;  // events per thread per tile: one 16-byte store per instance
   const uint32_t stride = EV * blockDim.x;
   const uint32_t D2 = min(D, 65535u) * 0x10001u;  // NF(L) = max(L, D) - D per 16-bit half (L <= 65535)
+  const uint32_t T2 = HT ? chunk->T[g.d] * 0x10001u : 0u;  // Threshold-LRU rows: NF(L) = L [L >= T]
   auto pk = [](uint32_t x, uint32_t y) { return min(x, 65535u) | (min(y, 65535u) << 16); };
   // software pipeline: the next tile's (L_before | J) words and packed A_nf pairs (clamped to
   // 65535, exact for C <= 65535) are loaded one iteration ahead
@@ -719,7 +760,9 @@ __global__ void __launch_bounds__(256, 4) s2_out_kernel(const ChunkDev* __restri
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       J2[k] = __byte_perm(lw[2 * k], lw[2 * k + 1], 0x7632);
-      N2[k] = __vsub2(__vmaxu2(__byte_perm(lw[2 * k], lw[2 * k + 1], 0x5410), D2), D2);
+      const uint32_t L2 = __byte_perm(lw[2 * k], lw[2 * k + 1], 0x5410);
+      N2[k] = __vsub2(__vmaxu2(L2, D2), D2);
+      if (HT) N2[k] &= __vcmpgeu2(L2, T2);
     }
     auto half = [](const uint32_t* v2, int u) { return (v2[u >> 1] >> ((u & 1) * 16)) & 0xFFFFu; };
     auto a_of = [&](int u) -> uint32_t {  // exact A_nf of event e + u
@@ -795,8 +838,9 @@ __global__ void __launch_bounds__(256, 4) s2_out_kernel(const ChunkDev* __restri
 
 // ----------------------------------------------------------------------------- s3
 __global__ void s3_results_kernel(const StackInstDev* __restrict__ insts, uint32_t ninst,
-                                  const uint32_t* __restrict__ inst_chunk, const ChunkTotals* __restrict__ totals,
-                                  const unsigned long long* sumXf, tlru_result* results) {
+                                  const uint32_t* __restrict__ inst_chunk, const ChunkDev* __restrict__ chunks,
+                                  const ChunkTotals* __restrict__ totals, const unsigned long long* sumXf,
+                                  tlru_result* results) {
   for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < ninst; k += gridDim.x * blockDim.x) {
     const StackInstDev in = insts[k];
     const ChunkTotals& T = totals[inst_chunk[k]];
@@ -806,7 +850,11 @@ __global__ void s3_results_kernel(const StackInstDev* __restrict__ insts, uint32
     const unsigned long long room = C > nfE ? C - nfE : 0ull;
     const unsigned long long fc_final = fE < room ? fE : room;
     tlru_result& r = results[in.inst];
-    const unsigned long long total = T.suma + r.sum_uncached - used_final;  // telescoped evictions
+    // telescoped evictions: blocks inserted (a + b per cached request) - blocks still cached.
+    // Threshold-LRU rows insert only on admitted requests; the others have b = J.
+    const bool thr = chunks[inst_chunk[k]].T[in.d] > 0;
+    const unsigned long long total = thr ? T.suma_adm[in.d] + (r.sum_uncached - T.sumJ_na[in.d]) - used_final
+                                         : T.suma + r.sum_uncached - used_final;
     const unsigned long long trim = T.sumF[in.d] - sumXf[in.inst] - fc_final;
     r.evicted_trim = trim;
     r.evicted_lru = total - trim;
@@ -843,13 +891,16 @@ static void make_stack_plan(const tlru_trace* traces, uint32_t nt, const tlru_in
   }
   std::vector<std::vector<uint32_t>> by_trace(nt);
   for (uint32_t i = 0; i < ni; ++i) by_trace[inst[i].trace].push_back(i);
-  auto Dof = [&](uint32_t i) {
+  // row key (T << 32 | D): T-LRU rows D = max(xi - Q_hat, 0), T = 0; LRU rows D = T = 0;
+  // Threshold-LRU rows D = 0, T = the admission threshold (T = 0 is plain LRU)
+  auto Dof = [&](uint32_t i) -> uint64_t {
+    if (inst[i].policy == TLRU_POLICY_THRESHOLD) return uint64_t(inst[i].threshold) << 32;
     return (inst[i].policy == TLRU_POLICY_TLRU && inst[i].xi > inst[i].q_hat) ? inst[i].xi - inst[i].q_hat : 0u;
   };
   for (uint32_t t = 0; t < nt; ++t) {
     const std::vector<uint32_t>& ids = by_trace[t];
     if (ids.empty() || traces[t].num_events == 0) continue;
-    std::vector<uint32_t> Ds;
+    std::vector<uint64_t> Ds;
     for (uint32_t i : ids) Ds.push_back(Dof(i));
     std::sort(Ds.begin(), Ds.end());
     Ds.erase(std::unique(Ds.begin(), Ds.end()), Ds.end());
@@ -864,13 +915,18 @@ static void make_stack_plan(const tlru_trace* traces, uint32_t nt, const tlru_in
           ch.ndk = k;
           break;
         }
-      for (uint32_t d = 0; d < SND; ++d) ch.dev.D[d] = d < ch.dev.nd ? Ds[c0 + d] : Ds[c0];
+      for (uint32_t d = 0; d < SND; ++d) {
+        const uint64_t key = d < ch.dev.nd ? Ds[c0 + d] : Ds[c0];
+        ch.dev.D[d] = static_cast<uint32_t>(key);
+        ch.dev.T[d] = static_cast<uint32_t>(key >> 32);
+        ch.dev.anyT |= ch.dev.T[d] > 0 ? 1u : 0u;
+      }
       ch.dev.inst0 = static_cast<uint32_t>(P->insts.size());
       for (uint32_t d = 0; d < ch.dev.nd; ++d) {
         ch.dev.dbeg[d] = static_cast<uint32_t>(P->insts.size()) - ch.dev.inst0;
         std::vector<uint32_t> mine;
         for (uint32_t i : ids)
-          if (Dof(i) == ch.dev.D[d]) mine.push_back(i);
+          if (Dof(i) == Ds[c0 + d]) mine.push_back(i);
         std::stable_sort(mine.begin(), mine.end(), [&](uint32_t a, uint32_t b) {
           return std::min<uint32_t>(inst[a].capacity, 0x7FFF0000u) < std::min<uint32_t>(inst[b].capacity, 0x7FFF0000u);
         });
@@ -962,7 +1018,7 @@ tlru_status stack_workspace(const tlru_trace* traces, uint32_t nt, const tlru_in
   return TLRU_OK;
 }
 
-template <int ND>
+template <int ND, bool HT>
 static tlru_status launch_s2(const tlru_trace& tr, const ChunkDev* ch, const ChunkTotals* tot, const StackWs& w,
                              const StackPlan& P, uint32_t c, uint32_t bins, bool aligned, bool aligned16, uint16_t* bout,
                              uint32_t* hist, cudaStream_t st, OutTiming* ot) {
@@ -972,13 +1028,13 @@ static tlru_status launch_s2(const tlru_trace& tr, const ChunkDev* ch, const Chu
   const uint32_t maxL = std::max<uint32_t>(tr.max_history, 1u);
   const uint32_t wch = std::max<uint32_t>(1u, std::min<uint32_t>(WCH_MAX, 65535u / maxL));
   const size_t warm_smem = size_t(3) * ND * S_THREADS * sizeof(uint32_t);
-  TLRU_CUDA(cudaFuncSetAttribute(s2_warm_kernel<ND>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  TLRU_CUDA(cudaFuncSetAttribute(s2_warm_kernel<ND, HT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(warm_smem)));
-  s2_warm_kernel<ND><<<std::min<uint32_t>(nb ? nb : 1, 2u * 148u), S_THREADS, warm_smem, st>>>(
+  s2_warm_kernel<ND, HT><<<std::min<uint32_t>(nb ? nb : 1, 2u * 148u), S_THREADS, warm_smem, st>>>(
       tr.sim, w.scanrec, E, ch, w.insts, tot, w.blockagg, wch, maxL, bout, w.sumXf);
   TLRU_CHECK_LAUNCH();
   if (!P.gi) {  // unfused: b written by s2_sat, histograms by the generic K3 afterwards
-    s2_sat_kernel<ND><<<nb, S_THREADS, 0, st>>>(tr.sim, w.scanrec, E, ch, w.insts, tot, wch, maxL, aligned, bout);
+    s2_sat_kernel<ND, HT><<<nb, S_THREADS, 0, st>>>(tr.sim, w.scanrec, E, ch, w.insts, tot, wch, maxL, aligned, bout);
     TLRU_CHECK_LAUNCH();
     return TLRU_OK;
   }
@@ -993,9 +1049,9 @@ static tlru_status launch_s2(const tlru_trace& tr, const ChunkDev* ch, const Chu
   uint8_t* cnt_g = w.cnt + size_t(g0) * ((P.tcap + 15u) & ~15u);
   auto out = [&](auto* Aptr) -> tlru_status {
     using AT = std::remove_const_t<std::remove_pointer_t<decltype(Aptr)>>;
-    s2_win_kernel<ND, AT><<<nb, S_THREADS, 0, st>>>(tr.sim, w.scanrec, E, ch, tot, wch, maxL, Aptr, w.Astride, w.LbJ);
+    s2_win_kernel<ND, AT, HT><<<nb, S_THREADS, 0, st>>>(tr.sim, w.scanrec, E, ch, tot, wch, maxL, Aptr, w.Astride, w.LbJ);
     TLRU_CHECK_LAUNCH();
-    TLRU_CUDA(cudaFuncSetAttribute(s2_out_kernel<AT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    TLRU_CUDA(cudaFuncSetAttribute(s2_out_kernel<AT, HT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(out_smem)));
     if (ng) {
       s2_cnt_kernel<<<ng, 256, 0, st>>>(ch, w.insts, w.groups + g0, P.tcap, cnt_g);
@@ -1003,7 +1059,7 @@ static tlru_status launch_s2(const tlru_trace& tr, const ChunkDev* ch, const Chu
     }
     for (uint32_t r0 = 0; ng && r0 < nranges; r0 += 65535u) {  // grid.y <= 65535
       if (ot && ot->first && ot->launches == 0) TLRU_CUDA(cudaEventRecord(ot->first, st));
-      s2_out_kernel<AT><<<dim3(ng, std::min(65535u, nranges - r0)), 256, out_smem, st>>>(
+      s2_out_kernel<AT, HT><<<dim3(ng, std::min(65535u, nranges - r0)), 256, out_smem, st>>>(
           ch, w.insts, w.groups + g0, tot, Aptr, w.Astride, w.LbJ, E, rl, bins, P.gi, P.tcap, aligned16, bout, hist,
           reinterpret_cast<const uint4*>(cnt_g), r0);
       TLRU_CHECK_LAUNCH();
@@ -1061,14 +1117,17 @@ tlru_status stack_simulate(const tlru_trace* traces, uint32_t nt, const tlru_ins
     TLRU_CHECK_LAUNCH();
     s1_totals_kernel<<<1, T_THREADS, 0, st>>>(w.chunks + c, hb, w.hist, w.hist + hb, w.blockagg, nb, w.totals + c);
     TLRU_CHECK_LAUNCH();
-    switch (P.chunks[c].ndk) {
-      case 2: TLRU_TRY(launch_s2<2>(tr, w.chunks + c, w.totals + c, w, P, c, bins, aligned, aligned16, bout, hist, st, out_timing)); break;
-      case 4: TLRU_TRY(launch_s2<4>(tr, w.chunks + c, w.totals + c, w, P, c, bins, aligned, aligned16, bout, hist, st, out_timing)); break;
-      case 8: TLRU_TRY(launch_s2<8>(tr, w.chunks + c, w.totals + c, w, P, c, bins, aligned, aligned16, bout, hist, st, out_timing)); break;
-      case 12: TLRU_TRY(launch_s2<12>(tr, w.chunks + c, w.totals + c, w, P, c, bins, aligned, aligned16, bout, hist, st, out_timing)); break;
-      case 16: TLRU_TRY(launch_s2<16>(tr, w.chunks + c, w.totals + c, w, P, c, bins, aligned, aligned16, bout, hist, st, out_timing)); break;
-      case 20: TLRU_TRY(launch_s2<20>(tr, w.chunks + c, w.totals + c, w, P, c, bins, aligned, aligned16, bout, hist, st, out_timing)); break;
-      default: TLRU_TRY(launch_s2<24>(tr, w.chunks + c, w.totals + c, w, P, c, bins, aligned, aligned16, bout, hist, st, out_timing)); break;
+    if (P.chunks[c].dev.anyT) {  // chunks with Threshold-LRU rows: masked window sums (two widths)
+      if (P.chunks[c].ndk <= 8) TLRU_TRY((launch_s2<8, true>(tr, w.chunks + c, w.totals + c, w, P, c, bins, aligned, aligned16, bout, hist, st, out_timing)));
+      else TLRU_TRY((launch_s2<24, true>(tr, w.chunks + c, w.totals + c, w, P, c, bins, aligned, aligned16, bout, hist, st, out_timing)));
+    } else switch (P.chunks[c].ndk) {
+      case 2: TLRU_TRY((launch_s2<2, false>(tr, w.chunks + c, w.totals + c, w, P, c, bins, aligned, aligned16, bout, hist, st, out_timing))); break;
+      case 4: TLRU_TRY((launch_s2<4, false>(tr, w.chunks + c, w.totals + c, w, P, c, bins, aligned, aligned16, bout, hist, st, out_timing))); break;
+      case 8: TLRU_TRY((launch_s2<8, false>(tr, w.chunks + c, w.totals + c, w, P, c, bins, aligned, aligned16, bout, hist, st, out_timing))); break;
+      case 12: TLRU_TRY((launch_s2<12, false>(tr, w.chunks + c, w.totals + c, w, P, c, bins, aligned, aligned16, bout, hist, st, out_timing))); break;
+      case 16: TLRU_TRY((launch_s2<16, false>(tr, w.chunks + c, w.totals + c, w, P, c, bins, aligned, aligned16, bout, hist, st, out_timing))); break;
+      case 20: TLRU_TRY((launch_s2<20, false>(tr, w.chunks + c, w.totals + c, w, P, c, bins, aligned, aligned16, bout, hist, st, out_timing))); break;
+      default: TLRU_TRY((launch_s2<24, false>(tr, w.chunks + c, w.totals + c, w, P, c, bins, aligned, aligned16, bout, hist, st, out_timing))); break;
     }
     *nkernels += 4;
   }
@@ -1079,7 +1138,8 @@ tlru_status stack_simulate(const tlru_trace* traces, uint32_t nt, const tlru_ins
   TLRU_TRY(launch_finalize(segs_dev, ni, bins, hist, clamped, 1.0, nullptr, results, st));
   if (!P.insts.empty()) {
     s3_results_kernel<<<grid_for(P.insts.size(), 128), 128, 0, st>>>(w.insts, static_cast<uint32_t>(P.insts.size()),
-                                                                     w.inst_chunk, w.totals, w.sumXf, results);
+                                                                     w.inst_chunk, w.chunks, w.totals, w.sumXf,
+                                                                     results);
     TLRU_CHECK_LAUNCH();
   }
   *nkernels += 3;
