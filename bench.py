@@ -171,6 +171,11 @@ def workload(name: str, rank: int):
     """(seeds, rows, description) of one GPU's share.  Weak scaling: rank r takes the seeds
     after rank r-1's, so per-GPU work is fixed as N grows."""
     from paper_2510_15152_b200.inputs import SEEDS_CONFIG5, config5_rows
+    if name == "config5x3":
+        seeds = [SEEDS_CONFIG5 * rank + k for k in range(SEEDS_CONFIG5)]
+        return seeds, config5_rows(len(seeds), threshold_lru=True), (
+            "config5 sweep per GPU with the paper's three policies: 10 seeds x 10^6-conversation traces x 25 "
+            "capacities x 20 xi x {LRU, T-LRU, Threshold-LRU (1024 tokens = 8 blocks)} = 1.5x10^4 instances")
     if name == "config5":
         seeds = [SEEDS_CONFIG5 * rank + k for k in range(SEEDS_CONFIG5)]
         return seeds, config5_rows(len(seeds)), (
@@ -392,7 +397,8 @@ def run_ours(args, rank, world, local_rank):
     nd_per_trace = {}
     for r in rows:
         D = (r[3] - r[4]) if (r[1] == 1 and r[3] > r[4]) else 0
-        nd_per_trace.setdefault(r[0], set()).add(D)
+        Tk = r[6] if (r[1] == 2 and len(r) > 6) else 0  # Threshold-LRU rows: (D = 0, T)
+        nd_per_trace.setdefault(r[0], set()).add((D, Tk))
     ev_tot = sum(traces[t].num_events for t in nd_per_trace)
     ev_rows = sum(traces[t].num_events * len(v) for t, v in nd_per_trace.items())  # (event, D) pairs
     # dominant kernel s2_out: writes b (2 B/request) and reads, once per event, the packed
@@ -469,7 +475,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-replay", action="store_true", help="skip timing the replay engine")
     ap.add_argument("--replay-instances", type=int, default=0, help="limit the replay-engine sample (0 = all of seed 0)")
-    ap.add_argument("--config", choices=("config5", "config4"), default="config5")
+    ap.add_argument("--config", choices=("config5", "config5x3", "config4"), default="config5")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

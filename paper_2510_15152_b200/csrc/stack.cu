@@ -904,11 +904,15 @@ static void make_stack_plan(const tlru_trace* traces, uint32_t nt, const tlru_in
     for (uint32_t i : ids) Ds.push_back(Dof(i));
     std::sort(Ds.begin(), Ds.end());
     Ds.erase(std::unique(Ds.begin(), Ds.end()), Ds.end());
-    for (size_t c0 = 0; c0 < Ds.size(); c0 += SND) {
+    // Threshold-LRU rows (keys with T > 0, sorted last) get chunks of their own, so the D rows
+    // keep the unmasked window sums
+    const size_t nD = std::lower_bound(Ds.begin(), Ds.end(), uint64_t(1) << 32) - Ds.begin();
+    for (size_t c0 = 0; c0 < Ds.size();) {
+      const size_t cend = std::min(c0 + SND, c0 < nD ? nD : Ds.size());
       StackPlan::Chunk ch;
       ch.trace = t;
       memset(&ch.dev, 0, sizeof(ch.dev));
-      ch.dev.nd = static_cast<uint32_t>(std::min<size_t>(SND, Ds.size() - c0));
+      ch.dev.nd = static_cast<uint32_t>(cend - c0);
       ch.ndk = SND;
       for (int k : kNDs)
         if (static_cast<uint32_t>(k) >= ch.dev.nd) {
@@ -948,6 +952,7 @@ static void make_stack_plan(const tlru_trace* traces, uint32_t nt, const tlru_in
       ch.dev.ninst = static_cast<uint32_t>(P->insts.size()) - ch.dev.inst0;
       for (uint32_t d = 0; d < ch.dev.nd; ++d) P->any_big |= ch.dev.Cmax[d] > 65535u;
       P->chunks.push_back(ch);
+      c0 = cend;
     }
   }
   // s2_out groups: the shared-memory histograms of a group hold (gi + 1) x ceil(bins / 2) words
@@ -1117,8 +1122,9 @@ tlru_status stack_simulate(const tlru_trace* traces, uint32_t nt, const tlru_ins
     TLRU_CHECK_LAUNCH();
     s1_totals_kernel<<<1, T_THREADS, 0, st>>>(w.chunks + c, hb, w.hist, w.hist + hb, w.blockagg, nb, w.totals + c);
     TLRU_CHECK_LAUNCH();
-    if (P.chunks[c].dev.anyT) {  // chunks with Threshold-LRU rows: masked window sums (two widths)
-      if (P.chunks[c].ndk <= 8) TLRU_TRY((launch_s2<8, true>(tr, w.chunks + c, w.totals + c, w, P, c, bins, aligned, aligned16, bout, hist, st, out_timing)));
+    if (P.chunks[c].dev.anyT) {  // Threshold-LRU chunks: masked window sums (three widths)
+      if (P.chunks[c].ndk <= 2) TLRU_TRY((launch_s2<2, true>(tr, w.chunks + c, w.totals + c, w, P, c, bins, aligned, aligned16, bout, hist, st, out_timing)));
+      else if (P.chunks[c].ndk <= 8) TLRU_TRY((launch_s2<8, true>(tr, w.chunks + c, w.totals + c, w, P, c, bins, aligned, aligned16, bout, hist, st, out_timing)));
       else TLRU_TRY((launch_s2<24, true>(tr, w.chunks + c, w.totals + c, w, P, c, bins, aligned, aligned16, bout, hist, st, out_timing)));
     } else switch (P.chunks[c].ndk) {
       case 2: TLRU_TRY((launch_s2<2, false>(tr, w.chunks + c, w.totals + c, w, P, c, bins, aligned, aligned16, bout, hist, st, out_timing))); break;

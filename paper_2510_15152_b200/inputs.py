@@ -56,10 +56,20 @@ XI_CONFIG5 = tuple(range(2, 41, 2))
 SEEDS_CONFIG5 = 10
 
 
-def config5_rows(n_traces: int = SEEDS_CONFIG5):
-    """(trace, policy, C, xi, Q_hat, slo) for the config-5 sweep over n_traces seeds."""
-    return [(t, pol, C, xi, Q_HAT, SLO_BLOCKS) for t in range(n_traces) for pol in (0, 1) for C in CAPS_CONFIG5
-            for xi in XI_CONFIG5]
+# Threshold-LRU admission threshold: 1024 tokens (the OpenAI rule the paper follows) = 8 blocks
+THRESHOLD_BLOCKS = 8
+
+
+def config5_rows(n_traces: int = SEEDS_CONFIG5, threshold_lru: bool = False):
+    """(trace, policy, C, xi, Q_hat, slo[, threshold]) for the config-5 sweep over n_traces seeds;
+    with threshold_lru the paper's third policy (Threshold-LRU, T = 8 blocks) joins LRU and T-LRU."""
+    rows = []
+    for t in range(n_traces):
+        for pol in ((0, 1, 2) if threshold_lru else (0, 1)):
+            for C in CAPS_CONFIG5:
+                for xi in XI_CONFIG5:
+                    rows.append((t, pol, C, xi, Q_HAT, SLO_BLOCKS) + ((THRESHOLD_BLOCKS,) if pol == 2 else ()))
+    return rows
 
 # Figure 1 (P:37): events A, B, A with 100-block prompts, no responses, C = 100.
 FIG1 = dict(conv=[0, 1, 0], q=[100, 100, 100], a=[0, 0, 0], C=100, xi=150, q_hat=100)
