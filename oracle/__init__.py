@@ -188,6 +188,8 @@ def derive(conv, q, a) -> Derived:
 LRU = 0
 TLRU = 1
 THRESHOLD = 2
+END_AWARE = 3
+LENGTH_AWARE = 4
 
 
 @dataclass

@@ -373,9 +373,14 @@ static void list_push_tail(conv_state* s, list_ends* l, int which, int64_t i) {
 
 /* policy: 0 = LRU, 1 = T-LRU, 2 = Threshold-LRU (LRU that caches a
    conversation's history only when its length reaches `threshold` blocks; below it
-   nothing is cached -- Reading #23: L_after >= threshold).  b_out[E] receives the
+   nothing is cached -- Reading #23: L_after >= threshold), 3 = End-Aware T-LRU and
+   4 = Length-Aware T-LRU (with future knowledge taken from the trace itself:
+   a conversation's terminating turn releases all its blocks instead of caching its
+   history (Reading #24); Length-Aware also budgets with the true next prompt length,
+   surplus = min(L, max(xi - q_next, 0)) (Reading #25)).  b_out[E] receives the
    uncached blocks of each request (u64).  counters_out[3] = {evicted_trim,
-   evicted_lru, max_occupancy}.  Returns 0, or -1 on allocation failure. */
+   evicted_lru, max_occupancy}; released blocks are not evictions.  Returns 0, or -1
+   on allocation failure. */
 int oracle_replay(const uint32_t* conv, const uint32_t* q, const uint32_t* a, uint64_t E,
                   int policy, uint64_t C, uint64_t xi, uint64_t q_hat, uint64_t threshold,
                   uint64_t* b_out, uint64_t* counters_out) {
@@ -385,12 +390,22 @@ int oracle_replay(const uint32_t* conv, const uint32_t* q, const uint32_t* a, ui
     if (n < 0) { free(dense); return -1; }
     conv_state* s = (conv_state*)calloc((size_t)(n ? n : 1), sizeof(conv_state));
     if (!s) { free(dense); return -1; }
+    /* next turn of the same conversation (End-/Length-Aware knowledge, from the trace) */
+    uint64_t* nxt = (uint64_t*)malloc((E ? E : 1) * 8);
+    int64_t* seen = (int64_t*)malloc((size_t)(n ? n : 1) * 8);
+    if (!nxt || !seen) { free(dense); free(s); free(nxt); free(seen); return -1; }
+    for (int64_t i = 0; i < n; ++i) seen[i] = -1;
+    for (uint64_t t = E; t-- > 0;) {
+        nxt[t] = seen[dense[t]] < 0 ? (uint64_t)-1 : (uint64_t)seen[dense[t]];
+        seen[dense[t]] = (int64_t)t;
+    }
+    free(seen);
     list_ends res = {-1, -1}, fre = {-1, -1};
     /* Free tail per conversation D = max(xi - q_hat, 0): the blocks at the end
        of the history beyond the TEL-safe budget L + Q_hat - xi (P:56, P:62
        footnote; Readings #2, #4, #6).  LRU has no free blocks. */
     uint64_t D = 0;
-    if (policy == 1 && xi > q_hat) D = xi - q_hat;
+    if ((policy == 1 || policy == 3) && xi > q_hat) D = xi - q_hat;
     uint64_t used = 0, ev_trim = 0, ev_lru = 0, max_occ = 0;
     for (uint64_t t = 0; t < E; ++t) {
         int64_t c = dense[t];
@@ -406,11 +421,28 @@ int oracle_replay(const uint32_t* conv, const uint32_t* q, const uint32_t* a, ui
             s[c].L = L_after;
             continue;
         }
+        if ((policy == 3 || policy == 4) && nxt[t] == (uint64_t)-1) {
+            /* terminating turn (End-/Length-Aware): "evicts all blocks from
+               terminating conversations" -- the history is not cached and the blocks
+               theta held are released (Reading #24) */
+            used -= s[c].X;
+            s[c].X = 0;
+            s[c].surplus = 0;
+            s[c].L = L_after;
+            if (s[c].in_res) list_remove(s, &res, RES, c);
+            if (s[c].in_fre) list_remove(s, &fre, FRE, c);
+            continue;
+        }
+        uint64_t Dt = D;
+        if (policy == 4) {  /* budget with the true next prompt q_next (Reading #25) */
+            uint64_t qn = q[nxt[t]];
+            Dt = xi > qn ? xi - qn : 0;
+        }
         used = used - s[c].X + L_after;
         s[c].X = L_after;
         s[c].L = L_after;
         s[c].tau = t;
-        s[c].surplus = L_after < D ? L_after : D;
+        s[c].surplus = L_after < Dt ? L_after : Dt;
         if (s[c].in_res) list_remove(s, &res, RES, c);
         list_push_tail(s, &res, RES, c);
         if (s[c].in_fre) list_remove(s, &fre, FRE, c);
@@ -446,6 +478,7 @@ int oracle_replay(const uint32_t* conv, const uint32_t* q, const uint32_t* a, ui
     counters_out[2] = max_occ;
     free(s);
     free(dense);
+    free(nxt);
     return 0;
 }
 

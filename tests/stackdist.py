@@ -57,3 +57,42 @@ def topc_replay_threshold(conv, q, a, C: int, T: int):
         L[c] = L.get(c, 0) + qq + aa
         tau[c] = t
     return out
+
+
+
+def block_replay(conv, q, a, C: int, xi: int, q_hat: int, kind: str = "tlru"):
+    """Definitional brute force of Alg. 1 and its End-/Length-Aware variants (P:206-218,
+    P:389-395; Readings #1-#5, #24, #25), written as a priority cache of individual blocks:
+    every cached block has the key (class, tau of its conversation, -position) with class 0
+    for free blocks (the last min(L, D) of a history, "infinitely old") and 1 for the
+    rest; an overflow evicts the minimum-key block, one block at a time, until the cache
+    fits.  Within a conversation the cached blocks are then always a prefix of its history,
+    so a count X per conversation represents them.  No surplus bookkeeping or eviction lists
+    are shared with the oracle.  kind: "tlru", "end" (a terminating turn releases theta's
+    blocks) or "length" ("end" + D from the true next prompt)."""
+    conv, q, a = list(map(int, conv)), list(map(int, q)), list(map(int, a))
+    E = len(conv)
+    nxt, seen = [None] * E, {}
+    for t in range(E - 1, -1, -1):
+        nxt[t] = seen.get(conv[t])
+        seen[conv[t]] = t
+    X, L, F, tau = {}, {}, {}, {}
+    out = []
+    for e in range(E):
+        c = conv[e]
+        Lb = L.get(c, 0)
+        out.append(Lb + q[e] - X.get(c, 0))
+        La = Lb + q[e] + a[e]
+        L[c] = La
+        if kind in ("end", "length") and nxt[e] is None:
+            X[c] = 0  # released
+            continue
+        qn = q[nxt[e]] if (kind == "length" and nxt[e] is not None) else q_hat
+        X[c], F[c], tau[c] = La, min(La, max(xi - qn, 0)), e
+        while sum(X.values()) > C:
+            def key(j):
+                free_cached = X[j] - (L[j] - F[j])
+                return (0 if free_cached > 0 else 1, tau[j])
+            j = min((j for j in X if X[j] > 0), key=key)
+            X[j] -= 1
+    return out
