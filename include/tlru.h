@@ -159,12 +159,21 @@ tlru_status tlru_trace_from_turns(const uint32_t* conv, const uint16_t* q, const
  *   conversation's history only once its length reaches `threshold` blocks
  *   (L_after >= threshold, Reading #23): below it nothing is cached (b = J),
  *   at or above it the whole history is cached and evicted by plain LRU.
+ * End-Aware / Length-Aware T-LRU (Readings #24-#25): the trace
+ *   supplies the future knowledge -- a turn with no later turn of its
+ *   conversation releases theta's blocks (not counted as evictions) and caches
+ *   nothing; Length-Aware budgets each cached history with the true next prompt,
+ *   surplus = min(L_after, max(xi - q_next, 0)).  Their cache is not the top-C of
+ *   the universe, so they always run on the replay engine as whole-trace chains;
+ *   a batch that contains them runs entirely on the replay engine.
  * ------------------------------------------------------------------------ */
 enum {
   TLRU_POLICY_LRU = 0,
   TLRU_POLICY_TLRU = 1,
-  TLRU_POLICY_THRESHOLD = 2
-  /* 3..5 reserved: END_AWARE, LENGTH_AWARE, TAIL_BELADY -> TLRU_EUNSUPPORTED */
+  TLRU_POLICY_THRESHOLD = 2,
+  TLRU_POLICY_END_AWARE = 3,
+  TLRU_POLICY_LENGTH_AWARE = 4
+  /* 5 reserved: TAIL_BELADY -> TLRU_EUNSUPPORTED */
 };
 
 typedef struct {

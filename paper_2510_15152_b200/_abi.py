@@ -17,6 +17,8 @@ TLRU_NONE = 0xFFFFFFFF
 POLICY_LRU = 0
 POLICY_TLRU = 1
 POLICY_THRESHOLD = 2
+POLICY_END_AWARE = 3
+POLICY_LENGTH_AWARE = 4
 ENGINE_REPLAY = 0
 ENGINE_STACK = 1
 

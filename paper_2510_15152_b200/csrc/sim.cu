@@ -28,10 +28,12 @@ struct LaneDev {
   uint32_t C, D;
   uint32_t T;     // Threshold-LRU admission threshold (0: LRU / T-LRU)
   uint64_t boff;  // offset of the instance's b array in `uncached`
+  uint32_t policy, xi;  // End-/Length-Aware chains: the policy and xi (Length-Aware's D per turn)
 };
 
 struct GroupDev {
   uint32_t trace, lane0, nlanes, W;
+  uint32_t aware;  // End-/Length-Aware lanes: one whole-trace chain (no segment warm start)
 };
 
 struct ItemDev {
@@ -68,7 +70,9 @@ __device__ __forceinline__ void acc_commit(AccDev* acc, uint32_t inst, const Cha
 }
 
 // One warp per (lane group, segment).  W = state entries per lane (compile-time).
-template <int W>
+// AWARE: End-/Length-Aware groups: the segment is the whole trace (their cache is not the
+// top-C of the universe, so no exact warm start exists) and the state keeps per-entry surplus.
+template <int W, bool AWARE>
 __global__ void __launch_bounds__(32) sim_kernel(const ItemDev* __restrict__ items, const GroupDev* __restrict__ groups,
                                                  const LaneDev* __restrict__ lanes, const TraceDev* __restrict__ traces,
                                                  uint32_t seg_len, uint16_t* __restrict__ bout, AccDev* acc,
@@ -76,25 +80,27 @@ __global__ void __launch_bounds__(32) sim_kernel(const ItemDev* __restrict__ ite
   extern __shared__ __align__(16) unsigned char smem[];
   uint32_t* tau_s = reinterpret_cast<uint32_t*>(smem);
   uint16_t* X_s = reinterpret_cast<uint16_t*>(tau_s + W * 32);
-  uint16_t* bst = X_s + W * 32;
+  uint16_t* S_s = X_s + W * 32;
+  uint16_t* bst = AWARE ? S_s + W * 32 : S_s;
   const int lane = threadIdx.x;
   const ItemDev it = items[blockIdx.x];
   const GroupDev g = groups[it.group];
   const TraceDev tr = traces[g.trace];
-  const uint32_t s = it.seg * seg_len;
-  const uint32_t s_end = static_cast<uint32_t>(min(uint64_t(s) + seg_len, tr.E));
+  const uint32_t s = AWARE ? 0u : it.seg * seg_len;
+  const uint32_t s_end = AWARE ? static_cast<uint32_t>(tr.E) : static_cast<uint32_t>(min(uint64_t(s) + seg_len, tr.E));
   LaneDev lp;
   lp.inst = 0xFFFFFFFFu;
-  lp.C = lp.D = 0;
+  lp.C = lp.D = lp.T = 0;
   lp.boff = 0;
+  lp.policy = lp.xi = 0;
   if (lane < static_cast<int>(g.nlanes)) lp = lanes[g.lane0 + lane];
   bool active = lp.inst != 0xFFFFFFFFu;
-  SmemState st{tau_s, X_s, lane};
+  SmemState st{tau_s, X_s, S_s, lane};
   ChainRegs c;
   chain_init(c, lp.C, lp.D, lp.T, W, active && s > 0);
 
-  // ---- rebuild the exact state at s (sim.cuh "Segment start")
-  for (int pass = 0; pass < 2; ++pass) {
+  // ---- rebuild the exact state at s (sim.cuh "Segment start"); AWARE chains start at event 0
+  for (int pass = 0; pass < (AWARE ? 0 : 2); ++pass) {
     int64_t e0 = int64_t(s) - 1;
     while (e0 >= 0 && __any_sync(0xFFFFFFFFu, c.walking)) {
       const int64_t e = e0 - lane;
@@ -124,13 +130,31 @@ __global__ void __launch_bounds__(32) sim_kernel(const ItemDev* __restrict__ ite
     const uint64_t evc = evn;
     const uint32_t nk = min(32u, s_end - base);
     if (base + 32 + lane < s_end) evn = __ldg(tr.sim + base + 32 + lane);  // prefetch the next tile
+    uint32_t qnc = 0xFFFFFFFFu;  // AWARE: this lane's event's next prompt, or NONE on a terminating turn
+    if (AWARE && base + lane < s_end) {
+      const uint32_t nx = __ldg(tr.next + base + lane);
+      if (nx != TLRU_NONE) qnc = sim_J(__ldg(tr.sim + nx)) - sim_La(evc);  // q = J - L_before
+    }
     for (uint32_t k = 0; k < nk; ++k) {
       const uint64_t ev = shfl64(evc, k);
-      if (active) {
+      if (AWARE) {
+        const uint32_t qn = __shfl_sync(0xFFFFFFFFu, qnc, k);
+        if (active) {
+          const bool last = qn == 0xFFFFFFFFu;
+          const uint32_t Dcur = lp.policy == TLRU_POLICY_LENGTH_AWARE ? (lp.xi > qn ? lp.xi - qn : 0u) : lp.D;
+          const uint32_t b = chain_request_aware(c, st, base + k, sim_prev(ev), sim_J(ev), sim_La(ev), last, Dcur);
+          bst[lane * BST_STRIDE + k] = static_cast<uint16_t>(b);
+          if (c.overflow) active = false;
+        }
+      } else if (active) {
         const uint32_t b = chain_request(c, st, base + k, sim_prev(ev), sim_J(ev), sim_La(ev));
         bst[lane * BST_STRIDE + k] = static_cast<uint16_t>(b);
         if (c.overflow) active = false;
       }
+    }
+    if (AWARE && active && (c.ev_trim >= (1u << 30) || c.ev_lru >= (1u << 30))) {  // whole-trace chain: flush
+      acc_commit(acc, lp.inst, c);
+      c.ev_trim = c.ev_lru = 0;
     }
     __syncwarp();
     // coalesced write-out: row r = lane r's instance, 64 contiguous bytes
@@ -154,7 +178,7 @@ __global__ void __launch_bounds__(32) sim_kernel(const ItemDev* __restrict__ ite
 __global__ void sim_spill_kernel(const GroupDev* __restrict__ groups, const LaneDev* __restrict__ lanes,
                                  const TraceDev* __restrict__ traces, uint32_t seg_len, uint16_t* __restrict__ bout,
                                  AccDev* acc, const SpillDev* spill, const unsigned int* nspill, uint32_t* tau_pool,
-                                 uint16_t* X_pool, uint32_t W_big, unsigned int* nfail) {
+                                 uint16_t* X_pool, uint16_t* S_pool, uint32_t W_big, unsigned int* nfail) {
   const unsigned n = *nspill;
   for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const SpillDev sp = spill[i];
@@ -164,8 +188,26 @@ __global__ void sim_spill_kernel(const GroupDev* __restrict__ groups, const Lane
     const uint32_t s = sp.seg * seg_len;
     const uint32_t s_end = static_cast<uint32_t>(min(uint64_t(s) + seg_len, tr.E));
     const uint64_t slot = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
-    GlobalState st{tau_pool + slot * W_big, X_pool + slot * W_big};
+    GlobalState st{tau_pool + slot * W_big, X_pool + slot * W_big, S_pool + slot * W_big};
     ChainRegs c;
+    if (g.aware) {  // whole-trace End-/Length-Aware chain
+      chain_init(c, lp.C, lp.D, lp.T, W_big, false);
+      for (uint32_t e = 0; e < tr.E && !c.overflow; ++e) {
+        const uint64_t ev = tr.sim[e];
+        const uint32_t nx = tr.next[e];
+        const uint32_t qn = nx != TLRU_NONE ? sim_J(tr.sim[nx]) - sim_La(ev) : 0u;
+        const uint32_t Dcur = lp.policy == TLRU_POLICY_LENGTH_AWARE ? (lp.xi > qn ? lp.xi - qn : 0u) : lp.D;
+        bout[lp.boff + e] = static_cast<uint16_t>(
+            chain_request_aware(c, st, e, sim_prev(ev), sim_J(ev), sim_La(ev), nx == TLRU_NONE, Dcur));
+        if (c.ev_trim >= (1u << 30) || c.ev_lru >= (1u << 30)) {
+          acc_commit(acc, lp.inst, c);
+          c.ev_trim = c.ev_lru = 0;
+        }
+      }
+      if (c.overflow) atomicAdd(nfail, 1u);
+      else acc_commit(acc, lp.inst, c);
+      continue;
+    }
     chain_init(c, lp.C, lp.D, lp.T, W_big, s > 0);
     for (int pass = 0; pass < 2; ++pass) {
       for (int64_t e = int64_t(s) - 1; e >= 0 && c.walking; --e) {
@@ -215,10 +257,14 @@ static int w_class(uint32_t C, uint32_t nconv) {
   return kNumW - 1;
 }
 
+static bool is_aware(const tlru_instance& in) { return in.policy >= TLRU_POLICY_END_AWARE; }
+
 struct Plan {
   std::vector<LaneDev> lanes;
   std::vector<GroupDev> groups;
   std::vector<ItemDev> items[kNumW];
+  std::vector<ItemDev> items_aware[kNumW];  // whole-trace End-/Length-Aware chains
+  bool any_aware = false;
   std::vector<TraceDev> traces;
   std::vector<SegDev> segs;
   uint32_t seg_len = 0;
@@ -253,9 +299,10 @@ static tlru_status make_plan(const tlru_trace* traces, uint32_t nt, const tlru_i
   for (uint32_t i = 0; i < ni; ++i) {
     const tlru_instance& in = inst[i];
     if (in.trace >= nt) TLRU_FAIL(TLRU_EINVAL, "instance %u: trace index %u out of range", i, in.trace);
-    if (in.policy != TLRU_POLICY_LRU && in.policy != TLRU_POLICY_TLRU && in.policy != TLRU_POLICY_THRESHOLD)
-      TLRU_FAIL(TLRU_EUNSUPPORTED, "instance %u: policy %u is not built (LRU = 0, T-LRU = 1, Threshold-LRU = 2)", i,
-                in.policy);
+    if (in.policy > TLRU_POLICY_LENGTH_AWARE)
+      TLRU_FAIL(TLRU_EUNSUPPORTED, "instance %u: policy %u is not built (0..4: LRU, T-LRU, Threshold-LRU, "
+                "End-Aware, Length-Aware)", i, in.policy);
+    if (in.policy >= TLRU_POLICY_END_AWARE) P->any_aware = true;
     if (in.policy == TLRU_POLICY_THRESHOLD && in.threshold > 65535)
       TLRU_FAIL(TLRU_ERANGE, "instance %u: threshold %u > 65535 (histories are u16)", i, in.threshold);
     order[i] = i;
@@ -268,6 +315,7 @@ static tlru_status make_plan(const tlru_trace* traces, uint32_t nt, const tlru_i
   }
   std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) {
     if (inst[a].trace != inst[b].trace) return inst[a].trace < inst[b].trace;
+    if (is_aware(inst[a]) != is_aware(inst[b])) return is_aware(inst[b]);
     if (wc[a] != wc[b]) return wc[a] < wc[b];
     return inst[a].capacity < inst[b].capacity;
   });
@@ -275,13 +323,19 @@ static tlru_status make_plan(const tlru_trace* traces, uint32_t nt, const tlru_i
   for (uint32_t k = 0; k < ni;) {
     const uint32_t t = inst[order[k]].trace;
     const int w = wc[order[k]];
-    GroupDev g{t, static_cast<uint32_t>(P->lanes.size()), 0, static_cast<uint32_t>(w)};
-    while (k < ni && g.nlanes < 32 && inst[order[k]].trace == t && wc[order[k]] == w) {
+    const bool aw = is_aware(inst[order[k]]);
+    GroupDev g{t, static_cast<uint32_t>(P->lanes.size()), 0, static_cast<uint32_t>(w), aw ? 1u : 0u};
+    while (k < ni && g.nlanes < 32 && inst[order[k]].trace == t && wc[order[k]] == w &&
+           is_aware(inst[order[k]]) == aw) {
       const tlru_instance& in = inst[order[k]];
       LaneDev l;
       l.inst = order[k];
       l.C = std::min<uint32_t>(in.capacity, 0x7FFF0000u);
-      l.D = (in.policy == TLRU_POLICY_TLRU && in.xi > in.q_hat) ? in.xi - in.q_hat : 0u;  // free tail
+      l.D = ((in.policy == TLRU_POLICY_TLRU || in.policy == TLRU_POLICY_END_AWARE) && in.xi > in.q_hat)
+                ? in.xi - in.q_hat
+                : 0u;  // free tail
+      l.policy = in.policy;
+      l.xi = in.xi;
       l.T = in.policy == TLRU_POLICY_THRESHOLD ? in.threshold : 0u;  // admission (Reading #23)
       l.boff = P->segs[order[k]].begin;
       P->lanes.push_back(l);
@@ -304,6 +358,13 @@ static tlru_status make_plan(const tlru_trace* traces, uint32_t nt, const tlru_i
   for (uint32_t gi = 0; gi < P->groups.size(); ++gi) {
     const GroupDev& g = P->groups[gi];
     const uint64_t E = P->traces[g.trace].E;
+    if (g.aware) {  // one whole-trace chain per lane group
+      if (E > 0) {
+        P->items_aware[g.W].push_back(ItemDev{gi, 0u});
+        ++nitems;
+      }
+      continue;
+    }
     const uint64_t nseg = (E + seg - 1) / seg;
     for (uint64_t sgi = 0; sgi < nseg; ++sgi) P->items[g.W].push_back(ItemDev{gi, static_cast<uint32_t>(sgi)});
     nitems += nseg;
@@ -333,11 +394,12 @@ struct SimWs {
   unsigned long long* clamped;
   uint32_t* tau_pool;
   uint16_t* X_pool;
+  uint16_t* S_pool;
 };
 
 static void carve_sim(Carver& cv, const Plan& P, uint32_t ni, SimWs* w) {
   uint64_t nitems = 0;
-  for (int k = 0; k < kNumW; ++k) nitems += P.items[k].size();
+  for (int k = 0; k < kNumW; ++k) nitems += P.items[k].size() + P.items_aware[k].size();
   w->lanes = cv.take<LaneDev>(P.lanes.size() + 1);
   w->groups = cv.take<GroupDev>(P.groups.size() + 1);
   w->items = cv.take<ItemDev>(nitems + 1);
@@ -350,6 +412,7 @@ static void carve_sim(Carver& cv, const Plan& P, uint32_t ni, SimWs* w) {
   w->clamped = cv.take<unsigned long long>(ni + 1);
   w->tau_pool = cv.take<uint32_t>(uint64_t(kSpillSlots) * P.W_big);
   w->X_pool = cv.take<uint16_t>(uint64_t(kSpillSlots) * P.W_big);
+  w->S_pool = cv.take<uint16_t>(uint64_t(kSpillSlots) * P.W_big);
 }
 
 static thread_local tlru_sim_stats g_stats;
@@ -364,14 +427,17 @@ static tlru_status record(int k, cudaStream_t st) {
   return TLRU_OK;
 }
 
-template <int W>
+template <int W, bool AWARE>
 static tlru_status launch_w(const std::vector<ItemDev>& items, const ItemDev* d_items, const SimWs& w,
                             uint32_t seg_len, uint16_t* bout, cudaStream_t st) {
   if (items.empty()) return TLRU_OK;
-  const size_t smem = size_t(W) * 32 * (sizeof(uint32_t) + sizeof(uint16_t)) + 32 * BST_STRIDE * sizeof(uint16_t);
-  TLRU_CUDA(cudaFuncSetAttribute(sim_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-  sim_kernel<W><<<static_cast<unsigned>(items.size()), 32, smem, st>>>(d_items, w.groups, w.lanes, w.traces, seg_len,
-                                                                       bout, w.acc, w.spill, w.counters);
+  const size_t smem = size_t(W) * 32 * (sizeof(uint32_t) + (AWARE ? 2 : 1) * sizeof(uint16_t)) +
+                      32 * BST_STRIDE * sizeof(uint16_t);
+  TLRU_CUDA(cudaFuncSetAttribute(sim_kernel<W, AWARE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem)));
+  sim_kernel<W, AWARE><<<static_cast<unsigned>(items.size()), 32, smem, st>>>(d_items, w.groups, w.lanes, w.traces,
+                                                                              seg_len, bout, w.acc, w.spill,
+                                                                              w.counters);
   TLRU_CHECK_LAUNCH();
   ++g_stats.kernels;
   return TLRU_OK;
@@ -416,8 +482,9 @@ extern "C" tlru_status tlru_simulate_batch(const tlru_trace* traces, uint32_t nt
     for (uint32_t i = 0; i < ni; ++i)
       if (traces[inst[i].trace].num_events > 0) TLRU_FAIL(TLRU_EINVAL, "uncached is NULL");
   }
-  g_stats.engine = g_opt_engine;
-  if (g_opt_engine == TLRU_ENGINE_STACK) {
+  // End-/Length-Aware instances have no stack property: such a batch runs on the replay engine
+  g_stats.engine = P.any_aware ? TLRU_ENGINE_REPLAY : g_opt_engine;
+  if (g_stats.engine == TLRU_ENGINE_STACK) {
     Carver cv(ws);
     SegDev* segs = cv.take<SegDev>(ni + 1);
     uint32_t* hist = cv.take<uint32_t>(uint64_t(ni + 1) * P.bins);
@@ -447,12 +514,16 @@ extern "C" tlru_status tlru_simulate_batch(const tlru_trace* traces, uint32_t nt
   TLRU_TRY(check_ws(cv, ws, ws_bytes));
   // tables -> device (pageable copies complete before the call returns)
   std::vector<ItemDev> all_items;
-  size_t item_off[kNumW + 1];
+  size_t item_off[kNumW + 1], aware_off[kNumW];
   for (int k = 0; k < kNumW; ++k) {
     item_off[k] = all_items.size();
     all_items.insert(all_items.end(), P.items[k].begin(), P.items[k].end());
   }
   item_off[kNumW] = all_items.size();
+  for (int k = 0; k < kNumW; ++k) {
+    aware_off[k] = all_items.size();
+    all_items.insert(all_items.end(), P.items_aware[k].begin(), P.items_aware[k].end());
+  }
   TLRU_CUDA(cudaMemcpyAsync(w.lanes, P.lanes.data(), P.lanes.size() * sizeof(LaneDev), cudaMemcpyHostToDevice, st));
   TLRU_CUDA(cudaMemcpyAsync(w.groups, P.groups.data(), P.groups.size() * sizeof(GroupDev), cudaMemcpyHostToDevice, st));
   if (!all_items.empty())
@@ -467,18 +538,27 @@ extern "C" tlru_status tlru_simulate_batch(const tlru_trace* traces, uint32_t nt
   TLRU_TRY(record(0, st));
   for (int k = kNumW - 1; k >= 0; --k) {
     const ItemDev* d = w.items + item_off[k];
+    const ItemDev* da = w.items + aware_off[k];
+    const std::vector<ItemDev>& ia = P.items_aware[k];
     switch (k) {
-      case 0: TLRU_TRY(launch_w<32>(P.items[k], d, w, P.seg_len, uncached, st)); break;
-      case 1: TLRU_TRY(launch_w<64>(P.items[k], d, w, P.seg_len, uncached, st)); break;
-      case 2: TLRU_TRY(launch_w<128>(P.items[k], d, w, P.seg_len, uncached, st)); break;
-      case 3: TLRU_TRY(launch_w<256>(P.items[k], d, w, P.seg_len, uncached, st)); break;
-      case 4: TLRU_TRY(launch_w<512>(P.items[k], d, w, P.seg_len, uncached, st)); break;
-      case 5: TLRU_TRY(launch_w<1024>(P.items[k], d, w, P.seg_len, uncached, st)); break;
+      case 0: TLRU_TRY((launch_w<32, false>(P.items[k], d, w, P.seg_len, uncached, st)));
+              TLRU_TRY((launch_w<32, true>(ia, da, w, P.seg_len, uncached, st))); break;
+      case 1: TLRU_TRY((launch_w<64, false>(P.items[k], d, w, P.seg_len, uncached, st)));
+              TLRU_TRY((launch_w<64, true>(ia, da, w, P.seg_len, uncached, st))); break;
+      case 2: TLRU_TRY((launch_w<128, false>(P.items[k], d, w, P.seg_len, uncached, st)));
+              TLRU_TRY((launch_w<128, true>(ia, da, w, P.seg_len, uncached, st))); break;
+      case 3: TLRU_TRY((launch_w<256, false>(P.items[k], d, w, P.seg_len, uncached, st)));
+              TLRU_TRY((launch_w<256, true>(ia, da, w, P.seg_len, uncached, st))); break;
+      case 4: TLRU_TRY((launch_w<512, false>(P.items[k], d, w, P.seg_len, uncached, st)));
+              TLRU_TRY((launch_w<512, true>(ia, da, w, P.seg_len, uncached, st))); break;
+      case 5: TLRU_TRY((launch_w<1024, false>(P.items[k], d, w, P.seg_len, uncached, st)));
+              TLRU_TRY((launch_w<1024, true>(ia, da, w, P.seg_len, uncached, st))); break;
     }
   }
   // spill path: always launched; exits at once when the queue is empty (no host sync)
   sim_spill_kernel<<<kSpillSlots / 32, 32, 0, st>>>(w.groups, w.lanes, w.traces, P.seg_len, uncached, w.acc, w.spill,
-                                                    w.counters, w.tau_pool, w.X_pool, P.W_big, w.counters + 1);
+                                                    w.counters, w.tau_pool, w.X_pool, w.S_pool, P.W_big,
+                                                    w.counters + 1);
   TLRU_CHECK_LAUNCH();
   ++g_stats.kernels;
   TLRU_TRY(record(1, st));
@@ -491,10 +571,10 @@ extern "C" tlru_status tlru_simulate_batch(const tlru_trace* traces, uint32_t nt
   g_ev_recorded = true;
   g_stats.kernels += 3;
   g_stats.chains = 0;
-  for (int k = 0; k < kNumW; ++k) g_stats.chains += P.items[k].size() * 32;
+  for (int k = 0; k < kNumW; ++k) g_stats.chains += (P.items[k].size() + P.items_aware[k].size()) * 32;
   g_stats.segment_events = P.seg_len;
   for (int k = kNumW - 1; k >= 0; --k)
-    if (!P.items[k].empty()) {
+    if (!P.items[k].empty() || !P.items_aware[k].empty()) {
       g_stats.state_entries = kWClasses[k];
       break;
     }

@@ -38,17 +38,21 @@ namespace tlru {
 struct SmemState {
   uint32_t* tau;
   uint16_t* X;
+  uint16_t* S;  // End-/Length-Aware chains only: surplus of the entry at insertion
   int lane;
   __device__ __forceinline__ uint32_t& T(uint32_t k) const { return tau[k * 32u + lane]; }
   __device__ __forceinline__ uint16_t& Xr(uint32_t k) const { return X[k * 32u + lane]; }
+  __device__ __forceinline__ uint16_t& Sr(uint32_t k) const { return S[k * 32u + lane]; }
 };
 
 // Chain-contiguous global-memory state (spill path).
 struct GlobalState {
   uint32_t* tau;
   uint16_t* X;
+  uint16_t* S;
   __device__ __forceinline__ uint32_t& T(uint32_t k) const { return tau[k]; }
   __device__ __forceinline__ uint16_t& Xr(uint32_t k) const { return X[k]; }
+  __device__ __forceinline__ uint16_t& Sr(uint32_t k) const { return S[k]; }
 };
 
 struct ChainRegs {
@@ -139,7 +143,7 @@ __device__ __forceinline__ void chain_walk_finish(ChainRegs& c) {
   }
 }
 
-template <class St>
+template <bool AWARE = false, class St>
 __device__ __forceinline__ bool chain_compact(ChainRegs& c, const St& st) {
   uint32_t j = 0;
   uint32_t new_fh = 0xFFFFFFFFu;
@@ -151,13 +155,14 @@ __device__ __forceinline__ bool chain_compact(ChainRegs& c, const St& st) {
       uint32_t t = st.T(k);
       st.T(j) = t;
       st.Xr(j) = x;
+      if (AWARE) st.Sr(j) = st.Sr(k);
       ++j;
     }
   }
   if (c.fh >= c.tail) {
     new_fh = j;
   } else if (fh_dead) {  // fh was a tombstone: the next live entry is untouched since insertion
-    c.frem = (new_fh < j) ? min(static_cast<uint32_t>(st.Xr(new_fh)), c.D) : 0u;
+    c.frem = (new_fh < j) ? min(static_cast<uint32_t>(st.Xr(new_fh)), AWARE ? uint32_t(st.Sr(new_fh)) : c.D) : 0u;
   }
   c.head = 0;
   c.tail = j;
@@ -223,6 +228,81 @@ __device__ __forceinline__ uint32_t chain_request(ChainRegs& c, const St& st, ui
     }
     // Phase 2: LRU, partial, from the least recently used entry
     while (over > 0) {
+      uint32_t x = st.Xr(c.head);
+      uint32_t take = min(x, over);
+      st.Xr(c.head) = static_cast<uint16_t>(x - take);
+      over -= take;
+      c.ev_lru += take;
+      if (x == take) ++c.head;
+    }
+    c.used = c.C;
+  }
+  c.max_occ = max(c.max_occ, c.used);
+  return b;
+}
+
+// End-Aware / Length-Aware T-LRU (Readings #24-#25) on a whole-trace chain.
+// `last`: theta's conversation has no later turn -> its blocks are released and its history is
+// not cached; otherwise Alg. 1 with the surplus min(La, Dcur) stored per entry (Length-Aware's
+// Dcur = max(xi - q_next, 0) differs per turn, so entries with surplus 0 may follow fh; fh is
+// the oldest entry whose surplus may be > 0, and every entry after it is untouched since its
+// insertion, so its surplus is S).
+template <class St>
+__device__ __forceinline__ uint32_t chain_request_aware(ChainRegs& c, const St& st, uint32_t e, uint32_t prev,
+                                                        uint32_t J, uint32_t La, bool last, uint32_t Dcur) {
+  uint32_t x_old = 0;
+  if (prev != TLRU_NONE) {
+    uint32_t lo = c.head, n = c.tail - c.head;
+    while (n > 0) {
+      uint32_t half = n >> 1;
+      uint32_t m = lo + half;
+      if (st.T(m) < prev) {
+        lo = m + 1;
+        n -= half + 1;
+      } else {
+        n = half;
+      }
+    }
+    if (lo < c.tail && st.T(lo) == prev) {
+      x_old = st.Xr(lo);
+      st.Xr(lo) = 0;
+      if (lo == c.fh) c.frem = 0;
+    }
+  }
+  const uint32_t b = J - x_old;
+  if (last) {  // terminating turn: release, cache nothing
+    c.used -= x_old;
+    return b;
+  }
+  if (c.tail == c.W) {
+    if (!chain_compact<true>(c, st)) {
+      c.overflow = true;
+      return b;
+    }
+  }
+  const uint32_t s0 = min(La, Dcur);
+  st.T(c.tail) = e;
+  st.Xr(c.tail) = static_cast<uint16_t>(La);
+  st.Sr(c.tail) = static_cast<uint16_t>(s0);
+  if (c.fh == c.tail) c.frem = s0;
+  ++c.tail;
+  c.used += La - x_old;
+  if (c.used > c.C) {
+    uint32_t over = c.used - c.C;
+    while (over > 0 && c.fh < c.tail) {  // Phase 1, oldest surplus first, theta last
+      uint32_t take = min(c.frem, over);
+      if (take > 0) {
+        st.Xr(c.fh) = static_cast<uint16_t>(st.Xr(c.fh) - take);
+        c.frem -= take;
+        over -= take;
+        c.ev_trim += take;
+      }
+      if (c.frem == 0) {
+        ++c.fh;
+        c.frem = (c.fh < c.tail) ? min(static_cast<uint32_t>(st.Xr(c.fh)), static_cast<uint32_t>(st.Sr(c.fh))) : 0u;
+      }
+    }
+    while (over > 0) {  // Phase 2, LRU
       uint32_t x = st.Xr(c.head);
       uint32_t take = min(x, over);
       st.Xr(c.head) = static_cast<uint16_t>(x - take);
