@@ -171,6 +171,15 @@ def workload(name: str, rank: int):
     """(seeds, rows, description) of one GPU's share.  Weak scaling: rank r takes the seeds
     after rank r-1's, so per-GPU work is fixed as N grows."""
     from paper_2510_15152_b200.inputs import SEEDS_CONFIG5, config5_rows
+    if name == "spectrum":
+        from paper_2510_15152_b200.inputs import CAPS_CONFIG5, Q_HAT, SLO_BLOCKS
+        seeds = [SEEDS_CONFIG5 * rank + k for k in range(SEEDS_CONFIG5)]
+        rows = [(t, pol, C, xi, Q_HAT, SLO_BLOCKS) for t in range(len(seeds)) for pol in (3, 4)
+                for C in CAPS_CONFIG5 for xi in (4, 8, 16, 24)]
+        return seeds, rows, (
+            "predictability spectrum per GPU (P:389-395): 10 seeds x 10^6-conversation traces x 25 capacities x "
+            "xi in {4, 8, 16, 24} x {End-Aware, Length-Aware T-LRU} = 2000 instances (replay engine, whole-trace "
+            "chains)")
     if name == "config5x3":
         seeds = [SEEDS_CONFIG5 * rank + k for k in range(SEEDS_CONFIG5)]
         return seeds, config5_rows(len(seeds), threshold_lru=True), (
@@ -423,8 +432,10 @@ def run_ours(args, rank, world, local_rank):
             "conversations": args.conversations,
             "parallelism": f"dp{world} (instances sharded by seed, NCCL all_gather of results)",
             "l2": f"inputs larger than L2: {2 * E_tot / 1e9:.1f} GB of b written per GPU-step",
-            "engine": "stack (closed form of Alg. 1 from the stack property, all capacities of a trace per pass; "
-                      "bit-identical to the replay engine and the oracle); no dedup of identical instances",
+            "engine": ("stack (closed form of Alg. 1 from the stack property, all capacities of a trace per pass; "
+                       "bit-identical to the replay engine and the oracle); no dedup of identical instances")
+            if stats["engine"] == 1 else
+            "replay (Alg. 1 request by request, one lane per instance; End-/Length-Aware: whole-trace chains)",
             "engine_ms": k2, "k3_ms": k3, "sequential_ms_per_step": seq_ms,
             "pipelining": "traces generated on a high-priority stream A while earlier traces are simulated on "
                           "two alternating streams; engine_ms / k3_ms / roofline.launch_ms from the sequential "
@@ -475,7 +486,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-replay", action="store_true", help="skip timing the replay engine")
     ap.add_argument("--replay-instances", type=int, default=0, help="limit the replay-engine sample (0 = all of seed 0)")
-    ap.add_argument("--config", choices=("config5", "config5x3", "config4"), default="config5")
+    ap.add_argument("--config", choices=("config5", "config5x3", "spectrum", "config4"), default="config5")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

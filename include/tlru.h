@@ -239,7 +239,8 @@ tlru_status tlru_set_sim_engine(uint32_t engine);
 typedef struct {
   uint64_t chains;          /* instance x segment work units launched (32 lanes per warp) */
   uint64_t segment_events;  /* events per segment */
-  uint64_t spilled_chains;  /* chains re-run with global-memory state */
+  uint64_t spilled_chains;  /* chains re-run with global-memory state (incl. End-/Length-Aware
+                               segments re-run by the fix-up) */
   uint64_t failed_chains;   /* chains that overflowed even the global-memory state (must be 0) */
   uint32_t kernels;         /* kernel launches issued */
   uint32_t state_entries;   /* largest on-chip W used (replay engine) */

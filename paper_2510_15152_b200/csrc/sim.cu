@@ -29,7 +29,61 @@ struct LaneDev {
   uint32_t T;     // Threshold-LRU admission threshold (0: LRU / T-LRU)
   uint64_t boff;  // offset of the instance's b array in `uncached`
   uint32_t policy, xi;  // End-/Length-Aware chains: the policy and xi (Length-Aware's D per turn)
+  uint32_t aidx, pad;   // index among the End-/Length-Aware lanes (snapshot / counter slots)
 };
+
+// End-/Length-Aware time partitioning (their cache is not the top-C of the universe, so no
+// closed-form warm start exists).  Segment k of a chain starts `burn` events early from an
+// empty cache; its state at the segment start (G_k) and end (F_k) is saved.  Segment k is exact
+// iff k = 0 or G_k == F_{k-1} (the state determines the rest of the run); aware_fix_kernel
+// re-runs the others from the exact F_{k-1}, in order, so every output is exact.
+struct AwareDev {
+  uint32_t seg_len, burn, nseg_max, wsnap;
+  uint32_t* snap;            // [aware lane][seg][2] snapshots of 4 + 2 * wsnap words
+  unsigned long long* segc;  // [aware lane][seg][2] evicted_trim, evicted_lru of the segment
+  uint32_t* segm;            // [aware lane][seg] max occupancy in the segment
+  uint32_t* ovf;             // [aware lane][seg] 1 = the segment overflowed the on-chip state
+};
+
+__host__ __device__ __forceinline__ size_t snap_words(uint32_t wsnap) { return 4 + 2 * size_t(wsnap); }
+
+// Canonical state: live entries in tau order (tau, X | S << 16), S zeroed up to the first entry
+// with positive remaining surplus (fh) -- it is not used there; header {n, used, fh, frem}.
+template <class St>
+__device__ void snap_write(uint32_t* out, uint32_t wsnap, const ChainRegs& c, const St& st) {
+  uint32_t n = 0, fhn = 0xFFFFFFFFu, frem = 0;
+  uint32_t* tau = out + 4;
+  uint32_t* xs = tau + wsnap;
+  for (uint32_t k = c.head; k < c.tail; ++k) {
+    const uint32_t x = st.Xr(k);
+    if (x == 0) continue;
+    uint32_t s = st.Sr(k);
+    if (fhn == 0xFFFFFFFFu) {
+      const uint32_t eff = k < c.fh ? 0u : (k == c.fh ? c.frem : min(x, s));
+      if (eff > 0) {
+        fhn = n;
+        frem = eff;
+      }
+      s = 0;
+    }
+    if (n < wsnap) {
+      tau[n] = st.T(k);
+      xs[n] = x | (s << 16);
+    }
+    ++n;
+  }
+  out[0] = n <= wsnap ? n : 0xFFFFFFFFu;  // too large to save: never matches, the fix-up re-runs it
+  out[1] = c.used;
+  out[2] = fhn == 0xFFFFFFFFu ? n : fhn;
+  out[3] = frem;
+}
+
+__device__ bool snap_equal(const uint32_t* a, const uint32_t* b, uint32_t wsnap) {
+  if (a[0] == 0xFFFFFFFFu || a[0] != b[0] || a[1] != b[1] || a[2] != b[2] || a[3] != b[3]) return false;
+  for (uint32_t i = 0; i < a[0]; ++i)
+    if (a[4 + i] != b[4 + i] || a[4 + wsnap + i] != b[4 + wsnap + i]) return false;
+  return true;
+}
 
 struct GroupDev {
   uint32_t trace, lane0, nlanes, W;
@@ -76,7 +130,7 @@ template <int W, bool AWARE>
 __global__ void __launch_bounds__(32) sim_kernel(const ItemDev* __restrict__ items, const GroupDev* __restrict__ groups,
                                                  const LaneDev* __restrict__ lanes, const TraceDev* __restrict__ traces,
                                                  uint32_t seg_len, uint16_t* __restrict__ bout, AccDev* acc,
-                                                 SpillDev* spill, unsigned int* nspill) {
+                                                 SpillDev* spill, unsigned int* nspill, AwareDev aw) {
   extern __shared__ __align__(16) unsigned char smem[];
   uint32_t* tau_s = reinterpret_cast<uint32_t*>(smem);
   uint16_t* X_s = reinterpret_cast<uint16_t*>(tau_s + W * 32);
@@ -86,8 +140,10 @@ __global__ void __launch_bounds__(32) sim_kernel(const ItemDev* __restrict__ ite
   const ItemDev it = items[blockIdx.x];
   const GroupDev g = groups[it.group];
   const TraceDev tr = traces[g.trace];
-  const uint32_t s = AWARE ? 0u : it.seg * seg_len;
-  const uint32_t s_end = AWARE ? static_cast<uint32_t>(tr.E) : static_cast<uint32_t>(min(uint64_t(s) + seg_len, tr.E));
+  const uint32_t sl = AWARE ? aw.seg_len : seg_len;
+  const uint32_t s = it.seg * sl;
+  const uint32_t s_end = static_cast<uint32_t>(min(uint64_t(s) + sl, tr.E));
+  const uint32_t s0 = AWARE ? (s > aw.burn ? s - aw.burn : 0u) : s;  // aware: burn-in from an empty cache
   LaneDev lp;
   lp.inst = 0xFFFFFFFFu;
   lp.C = lp.D = lp.T = 0;
@@ -125,8 +181,15 @@ __global__ void __launch_bounds__(32) sim_kernel(const ItemDev* __restrict__ ite
 
   // ---- forward: Alg. 1 per request, events broadcast from a 32-event register tile
   uint64_t evn = 0;
-  if (s + lane < s_end) evn = __ldg(tr.sim + s + lane);
-  for (uint32_t base = s; base < s_end; base += 32) {
+  if (s0 + lane < s_end) evn = __ldg(tr.sim + s0 + lane);
+  const size_t sw = AWARE ? snap_words(aw.wsnap) : 0;
+  uint32_t* snapG = nullptr;
+  if (AWARE && lp.inst != 0xFFFFFFFFu) snapG = aw.snap + (size_t(lp.aidx) * aw.nseg_max + it.seg) * 2 * sw;
+  for (uint32_t base = s0; base < s_end; base += 32) {
+    if (AWARE && base == s) {  // segment start: save G_k, restart the segment's counters
+      if (active && it.seg > 0) snap_write(snapG, aw.wsnap, c, st);
+      c.ev_trim = c.ev_lru = c.max_occ = 0;
+    }
     const uint64_t evc = evn;
     const uint32_t nk = min(32u, s_end - base);
     if (base + 32 + lane < s_end) evn = __ldg(tr.sim + base + 32 + lane);  // prefetch the next tile
@@ -152,11 +215,11 @@ __global__ void __launch_bounds__(32) sim_kernel(const ItemDev* __restrict__ ite
         if (c.overflow) active = false;
       }
     }
-    if (AWARE && active && (c.ev_trim >= (1u << 30) || c.ev_lru >= (1u << 30))) {  // whole-trace chain: flush
-      acc_commit(acc, lp.inst, c);
-      c.ev_trim = c.ev_lru = 0;
-    }
     __syncwarp();
+    if (AWARE && base < s) {  // burn-in tile: no output
+      __syncwarp();
+      continue;
+    }
     // coalesced write-out: row r = lane r's instance, 64 contiguous bytes
     const unsigned act = __ballot_sync(0xFFFFFFFFu, active);
     for (int r = 0; r < 32; ++r) {
@@ -165,6 +228,17 @@ __global__ void __launch_bounds__(32) sim_kernel(const ItemDev* __restrict__ ite
         bout[off + base + lane] = bst[r * BST_STRIDE + lane];
     }
     __syncwarp();
+  }
+  if (AWARE) {  // F_k and the segment's counters; overflowed segments are re-run by the fix-up
+    if (lp.inst != 0xFFFFFFFFu) {
+      const size_t slot = size_t(lp.aidx) * aw.nseg_max + it.seg;
+      if (active) snap_write(snapG + sw, aw.wsnap, c, st);
+      aw.segc[2 * slot] = c.ev_trim;
+      aw.segc[2 * slot + 1] = c.ev_lru;
+      aw.segm[slot] = c.max_occ;
+      aw.ovf[slot] = active ? 0u : 1u;
+    }
+    return;
   }
   if (active) {
     acc_commit(acc, lp.inst, c);
@@ -190,24 +264,6 @@ __global__ void sim_spill_kernel(const GroupDev* __restrict__ groups, const Lane
     const uint64_t slot = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
     GlobalState st{tau_pool + slot * W_big, X_pool + slot * W_big, S_pool + slot * W_big};
     ChainRegs c;
-    if (g.aware) {  // whole-trace End-/Length-Aware chain
-      chain_init(c, lp.C, lp.D, lp.T, W_big, false);
-      for (uint32_t e = 0; e < tr.E && !c.overflow; ++e) {
-        const uint64_t ev = tr.sim[e];
-        const uint32_t nx = tr.next[e];
-        const uint32_t qn = nx != TLRU_NONE ? sim_J(tr.sim[nx]) - sim_La(ev) : 0u;
-        const uint32_t Dcur = lp.policy == TLRU_POLICY_LENGTH_AWARE ? (lp.xi > qn ? lp.xi - qn : 0u) : lp.D;
-        bout[lp.boff + e] = static_cast<uint16_t>(
-            chain_request_aware(c, st, e, sim_prev(ev), sim_J(ev), sim_La(ev), nx == TLRU_NONE, Dcur));
-        if (c.ev_trim >= (1u << 30) || c.ev_lru >= (1u << 30)) {
-          acc_commit(acc, lp.inst, c);
-          c.ev_trim = c.ev_lru = 0;
-        }
-      }
-      if (c.overflow) atomicAdd(nfail, 1u);
-      else acc_commit(acc, lp.inst, c);
-      continue;
-    }
     chain_init(c, lp.C, lp.D, lp.T, W_big, s > 0);
     for (int pass = 0; pass < 2; ++pass) {
       for (int64_t e = int64_t(s) - 1; e >= 0 && c.walking; --e) {
@@ -225,6 +281,94 @@ __global__ void sim_spill_kernel(const GroupDev* __restrict__ groups, const Lane
     } else {
       acc_commit(acc, lp.inst, c);
     }
+  }
+}
+
+// Fix-up of the End-/Length-Aware segments: one thread per aware lane walks its segments in
+// order; a segment that overflowed or whose start state G_k differs from the exact end state
+// F_{k-1} is re-run from F_{k-1} (from an empty cache for k = 0) with global-memory state, which
+// also rewrites F_k.  Then the segment counters are summed into the instance's accumulators.
+__global__ void aware_fix_kernel(const LaneDev* __restrict__ lanes, const uint32_t* __restrict__ alane,
+                                 const uint32_t* __restrict__ atrace, uint32_t nal,
+                                 const TraceDev* __restrict__ traces, uint16_t* __restrict__ bout, AccDev* acc,
+                                 AwareDev aw, uint32_t* tau_pool, uint16_t* X_pool, uint16_t* S_pool, uint32_t Wp,
+                                 unsigned int* nfail, unsigned int* nfixed) {
+  const size_t sw = snap_words(aw.wsnap);
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nal; i += gridDim.x * blockDim.x) {
+    const LaneDev lp = lanes[alane[i]];
+    const TraceDev tr = traces[atrace[i]];
+    const uint32_t nseg = static_cast<uint32_t>((tr.E + aw.seg_len - 1) / aw.seg_len);
+    GlobalState st{tau_pool + size_t(i) * Wp, X_pool + size_t(i) * Wp, S_pool + size_t(i) * Wp};
+    bool failed = false, carry = false;  // carry: the pool holds the exact state at the end of segment k - 1
+    ChainRegs c;
+    for (uint32_t k = 0; k < nseg && !failed; ++k) {
+      const size_t slot = size_t(i) * aw.nseg_max + k;
+      uint32_t* G = aw.snap + slot * 2 * sw;
+      uint32_t* F = G + sw;
+      const uint32_t* Fp = k > 0 ? aw.snap + (slot - 1) * 2 * sw + sw : nullptr;
+      if (!aw.ovf[slot] && (k == 0 || snap_equal(G, Fp, aw.wsnap))) {
+        carry = false;
+        continue;
+      }
+      if (!carry) {  // start from the exact state: empty (k = 0) or the saved F_{k-1}
+        chain_init(c, lp.C, lp.D, lp.T, Wp, false);
+        c.head = c.tail = c.fh = 0;
+        if (k > 0) {
+          if (Fp[0] == 0xFFFFFFFFu) {
+            failed = true;
+            break;
+          }
+          const uint32_t n = Fp[0];
+          for (uint32_t j = 0; j < n; ++j) {
+            const uint32_t xs = Fp[4 + aw.wsnap + j];
+            st.T(j) = Fp[4 + j];
+            st.Xr(j) = static_cast<uint16_t>(xs & 0xFFFFu);
+            st.Sr(j) = static_cast<uint16_t>(xs >> 16);
+          }
+          c.tail = n;
+          c.used = Fp[1];
+          c.fh = Fp[2];
+          c.frem = Fp[3];
+        }
+      }
+      c.ev_trim = c.ev_lru = c.max_occ = 0;
+      const uint32_t s = k * aw.seg_len;
+      const uint32_t s_end = static_cast<uint32_t>(min(uint64_t(s) + aw.seg_len, tr.E));
+      for (uint32_t e = s; e < s_end && !c.overflow; ++e) {
+        const uint64_t ev = tr.sim[e];
+        const uint32_t nx = tr.next[e];
+        const uint32_t qn = nx != TLRU_NONE ? sim_J(tr.sim[nx]) - sim_La(ev) : 0u;
+        const uint32_t Dcur = lp.policy == TLRU_POLICY_LENGTH_AWARE ? (lp.xi > qn ? lp.xi - qn : 0u) : lp.D;
+        bout[lp.boff + e] = static_cast<uint16_t>(
+            chain_request_aware(c, st, e, sim_prev(ev), sim_J(ev), sim_La(ev), nx == TLRU_NONE, Dcur));
+      }
+      if (c.overflow) {
+        failed = true;
+        break;
+      }
+      aw.segc[2 * slot] = c.ev_trim;
+      aw.segc[2 * slot + 1] = c.ev_lru;
+      aw.segm[slot] = c.max_occ;
+      aw.ovf[slot] = 0;
+      snap_write(F, aw.wsnap, c, st);
+      carry = true;
+      atomicAdd(nfixed, 1u);
+    }
+    if (failed) {
+      atomicAdd(nfail, 1u);
+      continue;
+    }
+    unsigned long long et = 0, el = 0;
+    uint32_t mo = 0;
+    for (uint32_t k = 0; k < nseg; ++k) {
+      const size_t slot = size_t(i) * aw.nseg_max + k;
+      et += aw.segc[2 * slot];
+      el += aw.segc[2 * slot + 1];
+      mo = max(mo, aw.segm[slot]);
+    }
+    acc[lp.inst].ev_trim = et;
+    acc[lp.inst].ev_lru = el;
+    acc[lp.inst].max_occ = mo;
   }
 }
 
@@ -263,8 +407,10 @@ struct Plan {
   std::vector<LaneDev> lanes;
   std::vector<GroupDev> groups;
   std::vector<ItemDev> items[kNumW];
-  std::vector<ItemDev> items_aware[kNumW];  // whole-trace End-/Length-Aware chains
+  std::vector<ItemDev> items_aware[kNumW];  // End-/Length-Aware segments (burn-in + fix-up)
   bool any_aware = false;
+  std::vector<uint32_t> alane, atrace;       // aware lane -> global lane index, trace
+  uint32_t aseg = 8192, aburn = 4096, anseg_max = 1, awsnap = 32;
   std::vector<TraceDev> traces;
   std::vector<SegDev> segs;
   uint32_t seg_len = 0;
@@ -308,6 +454,8 @@ static tlru_status make_plan(const tlru_trace* traces, uint32_t nt, const tlru_i
     order[i] = i;
     const uint32_t C = std::min<uint32_t>(in.capacity, 0x7FFF0000u);
     wc[i] = g_opt_w >= 0 ? g_opt_w : w_class(C, traces[in.trace].num_conversations);
+    // aware chains keep 8 B per entry: 1024 x 32 lanes would exceed shared memory (spill covers the rest)
+    if (is_aware(in)) wc[i] = std::min(wc[i], kNumW - 2);
     const uint64_t E = traces[in.trace].num_events;
     const uint64_t off = offsets ? offsets[i] : packed;
     packed += E;
@@ -336,6 +484,14 @@ static tlru_status make_plan(const tlru_trace* traces, uint32_t nt, const tlru_i
                 : 0u;  // free tail
       l.policy = in.policy;
       l.xi = in.xi;
+      l.aidx = 0;
+      l.pad = 0;
+      if (aw) {
+        l.aidx = static_cast<uint32_t>(P->alane.size());
+        P->alane.push_back(static_cast<uint32_t>(P->lanes.size()));
+        P->atrace.push_back(t);
+        P->awsnap = std::max<uint32_t>(P->awsnap, static_cast<uint32_t>(kWClasses[w]));
+      }
       l.T = in.policy == TLRU_POLICY_THRESHOLD ? in.threshold : 0u;  // admission (Reading #23)
       l.boff = P->segs[order[k]].begin;
       P->lanes.push_back(l);
@@ -354,15 +510,23 @@ static tlru_status make_plan(const tlru_trace* traces, uint32_t nt, const tlru_i
   seg = std::min<uint64_t>(seg, 32768);  // u32 per-chain counters stay below 2^31
   seg = (seg + 31) & ~31ull;
   P->seg_len = static_cast<uint32_t>(seg);
+  {  // aware segments: enough warps to fill the GPU, but >= 2x the burn-in
+    uint64_t ag = 0;
+    for (const GroupDev& g : P->groups) ag += g.aware;
+    const uint64_t pa = ag ? (148ull * 8ull + ag - 1) / ag : 1;
+    uint64_t sa = Emax ? (Emax + pa - 1) / pa : 8192;
+    sa = std::min<uint64_t>(std::max<uint64_t>(sa, 2ull * P->aburn), 1ull << 20);
+    P->aseg = static_cast<uint32_t>((sa + 31) & ~31ull);
+  }
   uint64_t nitems = 0;
   for (uint32_t gi = 0; gi < P->groups.size(); ++gi) {
     const GroupDev& g = P->groups[gi];
     const uint64_t E = P->traces[g.trace].E;
-    if (g.aware) {  // one whole-trace chain per lane group
-      if (E > 0) {
-        P->items_aware[g.W].push_back(ItemDev{gi, 0u});
-        ++nitems;
-      }
+    if (g.aware) {  // segments of aseg events, each with an aburn-event burn-in
+      const uint64_t nsa = (E + P->aseg - 1) / P->aseg;
+      for (uint64_t sgi = 0; sgi < nsa; ++sgi) P->items_aware[g.W].push_back(ItemDev{gi, static_cast<uint32_t>(sgi)});
+      P->anseg_max = std::max<uint32_t>(P->anseg_max, static_cast<uint32_t>(nsa));
+      nitems += nsa;
       continue;
     }
     const uint64_t nseg = (E + seg - 1) / seg;
@@ -395,6 +559,12 @@ struct SimWs {
   uint32_t* tau_pool;
   uint16_t* X_pool;
   uint16_t* S_pool;
+  AwareDev aw;
+  uint32_t* alane;
+  uint32_t* atrace;
+  uint32_t* atau;   // fix-up state pool [aware lane][awsnap]
+  uint16_t* aX;
+  uint16_t* aS;
 };
 
 static void carve_sim(Carver& cv, const Plan& P, uint32_t ni, SimWs* w) {
@@ -407,12 +577,27 @@ static void carve_sim(Carver& cv, const Plan& P, uint32_t ni, SimWs* w) {
   w->segs = cv.take<SegDev>(ni + 1);
   w->acc = cv.take<AccDev>(ni + 1);
   w->spill = cv.take<SpillDev>(nitems * 32 + 1);
-  w->counters = cv.take<unsigned int>(2);
+  w->counters = cv.take<unsigned int>(3);  // nspill, nfail, aware segments re-run
   w->hist = cv.take<uint32_t>(uint64_t(ni + 1) * P.bins);
   w->clamped = cv.take<unsigned long long>(ni + 1);
   w->tau_pool = cv.take<uint32_t>(uint64_t(kSpillSlots) * P.W_big);
   w->X_pool = cv.take<uint16_t>(uint64_t(kSpillSlots) * P.W_big);
   w->S_pool = cv.take<uint16_t>(uint64_t(kSpillSlots) * P.W_big);
+  const uint64_t nal = P.alane.size();
+  const uint64_t nsl = std::max<uint64_t>(nal, 1) * P.anseg_max;
+  w->aw.seg_len = P.aseg;
+  w->aw.burn = P.aburn;
+  w->aw.nseg_max = P.anseg_max;
+  w->aw.wsnap = P.awsnap;
+  w->aw.snap = cv.take<uint32_t>(nal ? nsl * 2 * snap_words(P.awsnap) : 1);
+  w->aw.segc = cv.take<unsigned long long>(nal ? 2 * nsl : 1);
+  w->aw.segm = cv.take<uint32_t>(nal ? nsl : 1);
+  w->aw.ovf = cv.take<uint32_t>(nal ? nsl : 1);
+  w->alane = cv.take<uint32_t>(nal + 1);
+  w->atrace = cv.take<uint32_t>(nal + 1);
+  w->atau = cv.take<uint32_t>(nal ? nal * P.W_big : 1);  // fix-up state: as large as the spill state
+  w->aX = cv.take<uint16_t>(nal ? nal * P.W_big : 1);
+  w->aS = cv.take<uint16_t>(nal ? nal * P.W_big : 1);
 }
 
 static thread_local tlru_sim_stats g_stats;
@@ -437,7 +622,7 @@ static tlru_status launch_w(const std::vector<ItemDev>& items, const ItemDev* d_
                                  static_cast<int>(smem)));
   sim_kernel<W, AWARE><<<static_cast<unsigned>(items.size()), 32, smem, st>>>(d_items, w.groups, w.lanes, w.traces,
                                                                               seg_len, bout, w.acc, w.spill,
-                                                                              w.counters);
+                                                                              w.counters, w.aw);
   TLRU_CHECK_LAUNCH();
   ++g_stats.kernels;
   return TLRU_OK;
@@ -531,7 +716,11 @@ extern "C" tlru_status tlru_simulate_batch(const tlru_trace* traces, uint32_t nt
   TLRU_CUDA(cudaMemcpyAsync(w.traces, P.traces.data(), P.traces.size() * sizeof(TraceDev), cudaMemcpyHostToDevice, st));
   TLRU_CUDA(cudaMemcpyAsync(w.segs, P.segs.data(), ni * sizeof(SegDev), cudaMemcpyHostToDevice, st));
   TLRU_CUDA(cudaMemsetAsync(w.acc, 0, ni * sizeof(AccDev), st));
-  TLRU_CUDA(cudaMemsetAsync(w.counters, 0, 2 * sizeof(unsigned int), st));
+  TLRU_CUDA(cudaMemsetAsync(w.counters, 0, 3 * sizeof(unsigned int), st));
+  if (!P.alane.empty()) {
+    TLRU_CUDA(cudaMemcpyAsync(w.alane, P.alane.data(), P.alane.size() * 4, cudaMemcpyHostToDevice, st));
+    TLRU_CUDA(cudaMemcpyAsync(w.atrace, P.atrace.data(), P.atrace.size() * 4, cudaMemcpyHostToDevice, st));
+  }
   TLRU_CUDA(cudaMemsetAsync(w.hist, 0, uint64_t(ni) * P.bins * sizeof(uint32_t), st));
   TLRU_CUDA(cudaMemsetAsync(w.clamped, 0, ni * sizeof(unsigned long long), st));
   // K2: largest state class first (longest per-event latency)
@@ -561,6 +750,13 @@ extern "C" tlru_status tlru_simulate_batch(const tlru_trace* traces, uint32_t nt
                                                     w.counters + 1);
   TLRU_CHECK_LAUNCH();
   ++g_stats.kernels;
+  if (!P.alane.empty()) {  // End-/Length-Aware fix-up (exactness of the burn-in segments)
+    const uint32_t nal = static_cast<uint32_t>(P.alane.size());
+    aware_fix_kernel<<<(nal + 31) / 32, 32, 0, st>>>(w.lanes, w.alane, w.atrace, nal, w.traces, uncached, w.acc, w.aw,
+                                                     w.atau, w.aX, w.aS, P.W_big, w.counters + 1, w.counters + 2);
+    TLRU_CHECK_LAUNCH();
+    ++g_stats.kernels;
+  }
   TLRU_TRY(record(1, st));
   // K3: histogram of b per instance -> percentiles, TEL, SLO; then the counters
   TLRU_TRY(launch_hist(uncached, w.segs, ni, P.bins, w.hist, w.clamped, st));
@@ -609,10 +805,10 @@ extern "C" tlru_status tlru_last_sim_stats(tlru_sim_stats* out) {
   if (!out) TLRU_FAIL(TLRU_EINVAL, "out is NULL");
   *out = g_stats;
   if (g_counters) {
-    unsigned int c[2] = {0, 0};
+    unsigned int c[3] = {0, 0, 0};
     TLRU_CUDA(cudaDeviceSynchronize());
     TLRU_CUDA(cudaMemcpy(c, g_counters, sizeof(c), cudaMemcpyDeviceToHost));
-    out->spilled_chains = c[0];
+    out->spilled_chains = c[0] + c[2];  // incl. End-/Length-Aware segments re-run by the fix-up
     out->failed_chains = c[1];
   }
   if (g_ev_recorded) {
