@@ -169,6 +169,48 @@ __global__ void gen_emit_kernel(GenDev g, const uint64_t* birth, const uint32_t*
   warp_atomic_add_u32(nvalid, nv);
 }
 
+// ---- time order: bucket sort on the arrival tick (buckets of 2^sh ticks, ~2 events each),
+// then each bucket is sorted by (tick, slot) -- slot order is (conversation, turn), so ties come
+// out as Reading #9 requires and the result does not depend on the atomics' order.  Slots with
+// the sentinel key (context-capped turns) go to the extra last bucket (never read).
+__global__ void gen_bucket_count_kernel(uint32_t n, const uint64_t* __restrict__ key, uint32_t sh, uint32_t nb,
+                                        uint64_t sentinel, uint32_t* cnt) {
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+    const uint64_t k = key[j];
+    atomicAdd(&cnt[k == sentinel ? nb : static_cast<uint32_t>(k >> sh)], 1u);
+  }
+}
+
+__global__ void gen_bucket_place_kernel(uint32_t n, const uint64_t* __restrict__ key, uint32_t sh, uint32_t nb,
+                                        uint64_t sentinel, const uint32_t* __restrict__ start, uint32_t* fill,
+                                        uint64_t* okey, uint32_t* oval) {
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+    const uint64_t k = key[j];
+    const uint32_t b = k == sentinel ? nb : static_cast<uint32_t>(k >> sh);
+    const uint32_t p = start[b] + atomicAdd(&fill[b], 1u);
+    okey[p] = k;
+    oval[p] = j;  // the slot index
+  }
+}
+
+__global__ void gen_bucket_sort_kernel(uint32_t nb, const uint32_t* __restrict__ start, uint64_t* key, uint32_t* val) {
+  for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += gridDim.x * blockDim.x) {
+    const uint32_t lo = start[b], hi = start[b + 1];
+    for (uint32_t i = lo + 1; i < hi; ++i) {  // insertion sort by (tick, slot)
+      const uint64_t k = key[i];
+      const uint32_t v = val[i];
+      uint32_t j = i;
+      while (j > lo && (key[j - 1] > k || (key[j - 1] == k && val[j - 1] > v))) {
+        key[j] = key[j - 1];
+        val[j] = val[j - 1];
+        --j;
+      }
+      key[j] = k;
+      val[j] = v;
+    }
+  }
+}
+
 __global__ void gen_scatter_kernel(uint64_t E, const uint64_t* skey, const uint32_t* sval, const uint32_t* cid,
                                    const uint16_t* q16, const uint16_t* a16, const uint8_t* last8, uint32_t* pos,
                                    uint64_t* time_ticks, uint32_t* conv, uint16_t* prompt, uint16_t* response,
@@ -260,6 +302,8 @@ struct GenWs {
   uint16_t *q16, *a16, *J16, *La16;
   uint8_t* last8;
   uint32_t* pos;
+  uint32_t* bcnt;    // [cap / 2 + 2] time-bucket counts, then bucket starts (bucket sort)
+  uint32_t* bfill;   // [cap / 2 + 2] bucket fill cursors
   void* cub_tmp;
   size_t cub_bytes;
 };
@@ -288,6 +332,8 @@ static tlru_status carve_gen(Carver& cv, uint32_t N, uint64_t cap, GenWs* w) {
   w->La16 = cv.take<uint16_t>(cap);
   w->last8 = cv.take<uint8_t>(cap);
   w->pos = cv.take<uint32_t>(cap);
+  w->bcnt = cv.take<uint32_t>(cap / 2 + 3);
+  w->bfill = cv.take<uint32_t>(cap / 2 + 3);
   size_t s1 = 0, s2 = 0, s3 = 0;
   cub::DoubleBuffer<uint64_t> kb(nullptr, nullptr);
   cub::DoubleBuffer<uint32_t> vb(nullptr, nullptr);
@@ -297,7 +343,11 @@ static tlru_status carve_gen(Carver& cv, uint32_t N, uint64_t cap, GenWs* w) {
       cub::DeviceScan::ExclusiveSum(nullptr, s3, (uint32_t*)nullptr, (uint32_t*)nullptr, static_cast<int>(N + 1)) !=
           cudaSuccess)
     TLRU_FAIL(TLRU_ECUDA, "cub temp-storage query failed");
-  w->cub_bytes = std::max(s1, std::max(s2, s3));
+  size_t s4 = 0;
+  if (cub::DeviceScan::ExclusiveSum(nullptr, s4, (uint32_t*)nullptr, (uint32_t*)nullptr,
+                                    static_cast<int>(cap / 2 + 3)) != cudaSuccess)
+    TLRU_FAIL(TLRU_ECUDA, "cub temp-storage query failed");
+  w->cub_bytes = std::max(std::max(s1, s4), std::max(s2, s3));
   w->cub_tmp = cv.take<char>(w->cub_bytes);
   return TLRU_OK;
 }
@@ -496,20 +546,31 @@ extern "C" tlru_status tlru_generate_traces(const tlru_gen_params* params, uint3
     const uint64_t slots = E;
     E = stats[2];  // events that survive the context cap
     if (E > 0) {
-      cub::DoubleBuffer<uint64_t> kb(w.key[0], w.key[1]);
-      cub::DoubleBuffer<uint32_t> vb(w.val[0], w.val[1]);
-      size_t b = w.cub_bytes;
-      TLRU_CUDA(cub::DeviceRadixSort::SortPairs(w.cub_tmp, b, kb, vb, static_cast<int>(slots), 0, end_bit, st));
-      gen_scatter_kernel<<<grid_for(E, 256), 256, 0, st>>>(E, kb.Current(), vb.Current(), w.cid, w.q16, w.a16,
-                                                           w.last8, w.pos, tr->time_ticks, tr->conv, tr->prompt,
-                                                           tr->response, tr->is_last);
+      // bucket width 2^sh ticks: about two events per bucket over [0, max_tick]
+      uint32_t sh = 0;
+      while (sh < 63 && ((max_tick >> sh) + 1) > slots / 2 + 1) ++sh;
+      const uint32_t nb = static_cast<uint32_t>((max_tick >> sh) + 1);  // + 1 sentinel bucket at nb
+      const uint32_t n = static_cast<uint32_t>(slots);
+      TLRU_CUDA(cudaMemsetAsync(w.bcnt, 0, (nb + 2) * sizeof(uint32_t), st));
+      TLRU_CUDA(cudaMemsetAsync(w.bfill, 0, (nb + 2) * sizeof(uint32_t), st));
+      gen_bucket_count_kernel<<<grid_for(n, 256), 256, 0, st>>>(n, w.key[0], sh, nb, sentinel, w.bcnt);
       TLRU_CHECK_LAUNCH();
-      gen_link_kernel<<<grid_for(E, 256), 256, 0, st>>>(E, vb.Current(), w.cid, w.off, w.J16, w.La16, w.last8, w.pos,
+      size_t b = w.cub_bytes;  // in place: starts[b] = exclusive prefix of counts, starts[nb + 1] = n
+      TLRU_CUDA(cub::DeviceScan::ExclusiveSum(w.cub_tmp, b, w.bcnt, w.bcnt, static_cast<int>(nb + 2), st));
+      gen_bucket_place_kernel<<<grid_for(n, 256), 256, 0, st>>>(n, w.key[0], sh, nb, sentinel, w.bcnt, w.bfill,
+                                                                w.key[1], w.val[1]);
+      TLRU_CHECK_LAUNCH();
+      gen_bucket_sort_kernel<<<grid_for(nb, 256), 256, 0, st>>>(nb, w.bcnt, w.key[1], w.val[1]);
+      TLRU_CHECK_LAUNCH();
+      gen_scatter_kernel<<<grid_for(E, 256), 256, 0, st>>>(E, w.key[1], w.val[1], w.cid, w.q16, w.a16, w.last8,
+                                                           w.pos, tr->time_ticks, tr->conv, tr->prompt, tr->response,
+                                                           tr->is_last);
+      TLRU_CHECK_LAUNCH();
+      gen_link_kernel<<<grid_for(E, 256), 256, 0, st>>>(E, w.val[1], w.cid, w.off, w.J16, w.La16, w.last8, w.pos,
                                                         tr->sim, tr->next);
       TLRU_CHECK_LAUNCH();
     }
-    TLRU_CUDA(cudaStreamSynchronize(st));
-    tr->num_events = E;
+    tr->num_events = E;  // known since the stats copy: the rest of the generation stays asynchronous
     tr->max_history = stats[0];
     tr->num_conversations = stats[1];
   }
