@@ -190,6 +190,7 @@ TLRU = 1
 THRESHOLD = 2
 END_AWARE = 3
 LENGTH_AWARE = 4
+TAIL_BELADY = 5  # Thm 1 hindsight policy, Reading #26
 
 
 @dataclass

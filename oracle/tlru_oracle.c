@@ -20,7 +20,9 @@
  *   4. Trace derivation: J = L_before + q, L_after = J + a, prev links
  *      (Sec. 3 explicit TEL form).
  *   5. Alg. 1 replay (Sec. 4): LRU (Phase 2 only) and T-LRU
- *      (Phase 1 TEL-safe trimming then Phase 2 LRU).
+ *      (Phase 1 TEL-safe trimming then Phase 2 LRU); Threshold-LRU,
+ *      End-/Length-Aware T-LRU and the hindsight Tail-Optimized
+ *      Belady (Thm 1).
  *   6. Metrics: TTFT = alpha*b (Eq. 2), TEL (Eq. 1/3),
  *      nearest-rank percentiles (Reading #11), SLO count (strict >).
  */
@@ -371,6 +373,89 @@ static void list_push_tail(conv_state* s, list_ends* l, int which, int64_t i) {
     l->tail = i;
 }
 
+/* Tail-Optimized Belady (Thm 1; its proof App. A), the hindsight
+   policy: clairvoyant, it knows each conversation's next arrival and next prompt length
+   from the trace.  Reading #26: on arrival theta caches its whole history (optional caching,
+   as Alg. 1, Reading #7); only on overflow and only as much as needed (Reading #8):
+   Phase 1 trims blocks above each conversation's exact TEL-safe budget
+   (L + q_next - xi)^+ (budget 0 for a conversation that never returns),
+   furthest next arrival first; Phase 2 evicts from the conversation "whose next requests
+   are expected to arrive furthest in the future", partial, tail blocks first.
+   Written plainly: the resident conversations live in an unordered array and every
+   eviction step scans it for the maximum next arrival (never-returning = +infinity; ties
+   among those by lower conversation id, SPEC S:248 -- unobservable: they never return
+   and are all free).  Counters as oracle_replay (Phase 1 -> evicted_trim). */
+static int replay_tail_belady(const uint32_t* dense, int64_t n, const uint32_t* q, const uint32_t* a,
+                              const uint64_t* nxt, uint64_t E, uint64_t C, uint64_t xi,
+                              uint64_t* b_out, uint64_t* counters_out) {
+    uint64_t* X = (uint64_t*)calloc((size_t)(n ? n : 1), 8);   /* cached blocks x_i */
+    uint64_t* L = (uint64_t*)calloc((size_t)(n ? n : 1), 8);   /* history length L_i */
+    uint64_t* sur = (uint64_t*)calloc((size_t)(n ? n : 1), 8); /* blocks above the budget */
+    uint64_t* nx = (uint64_t*)calloc((size_t)(n ? n : 1), 8);  /* next arrival (UINT64_MAX: never) */
+    int64_t* res = (int64_t*)malloc((size_t)(n ? n : 1) * 8);  /* resident conversations */
+    unsigned char* in_res = (unsigned char*)calloc((size_t)(n ? n : 1), 1);
+    if (!X || !L || !sur || !nx || !res || !in_res) {
+        free(X); free(L); free(sur); free(nx); free(res); free(in_res);
+        return -1;
+    }
+    int64_t nres = 0;
+    uint64_t used = 0, ev_trim = 0, ev_far = 0, max_occ = 0;
+    for (uint64_t t = 0; t < E; ++t) {
+        int64_t c = dense[t];
+        uint64_t J = L[c] + q[t];
+        b_out[t] = J - X[c];                         /* job - x */
+        uint64_t L_after = J + a[t];
+        used = used - X[c] + L_after;                /* X_theta <- L_theta (Reading #7) */
+        X[c] = L_after;
+        L[c] = L_after;
+        nx[c] = nxt[t];
+        /* exact TEL-safe budget: (L + q_next - xi)^+, 0 if theta never returns */
+        uint64_t budget = 0;
+        if (nxt[t] != (uint64_t)-1) {
+            uint64_t need = L_after + q[nxt[t]];
+            budget = need > xi ? need - xi : 0;
+        }
+        sur[c] = L_after > budget ? L_after - budget : 0;
+        if (!in_res[c] && X[c] > 0) { res[nres++] = c; in_res[c] = 1; }
+        if (used > C) {
+            uint64_t over = used - C;
+            for (int phase = 1; phase <= 2 && over > 0; ++phase) {
+                while (over > 0) {
+                    /* the resident conversation with the furthest next arrival that still
+                       has evictable blocks (Phase 1: blocks above its budget) */
+                    int64_t best = -1;
+                    for (int64_t k = 0; k < nres; ++k) {
+                        int64_t i = res[k];
+                        uint64_t avail = phase == 1 ? sur[i] : X[i];
+                        if (avail == 0) continue;
+                        if (best < 0 || nx[i] > nx[best] || (nx[i] == nx[best] && i < best)) best = i;
+                    }
+                    if (best < 0) break;
+                    uint64_t avail = phase == 1 ? sur[best] : X[best];
+                    uint64_t k = avail < over ? avail : over;
+                    X[best] -= k;
+                    if (phase == 1) { sur[best] -= k; ev_trim += k; } else { ev_far += k; }
+                    used -= k;
+                    over -= k;
+                }
+            }
+            /* drop conversations left with no cached block from the resident array */
+            int64_t w = 0;
+            for (int64_t k = 0; k < nres; ++k) {
+                if (X[res[k]] > 0) res[w++] = res[k];
+                else in_res[res[k]] = 0;
+            }
+            nres = w;
+        }
+        if (used > max_occ) max_occ = used;
+    }
+    counters_out[0] = ev_trim;
+    counters_out[1] = ev_far;
+    counters_out[2] = max_occ;
+    free(X); free(L); free(sur); free(nx); free(res); free(in_res);
+    return 0;
+}
+
 /* policy: 0 = LRU, 1 = T-LRU, 2 = Threshold-LRU (LRU that caches a
    conversation's history only when its length reaches `threshold` blocks; below it
    nothing is cached -- Reading #23: L_after >= threshold), 3 = End-Aware T-LRU and
@@ -379,8 +464,9 @@ static void list_push_tail(conv_state* s, list_ends* l, int which, int64_t i) {
    history (Reading #24); Length-Aware also budgets with the true next prompt length,
    surplus = min(L, max(xi - q_next, 0)) (Reading #25)).  b_out[E] receives the
    uncached blocks of each request (u64).  counters_out[3] = {evicted_trim,
-   evicted_lru, max_occupancy}; released blocks are not evictions.  Returns 0, or -1
-   on allocation failure. */
+   evicted_lru, max_occupancy}; released blocks are not evictions.  5 = Tail-Optimized
+   Belady (Thm 1, replay_tail_belady above; evicted_lru counts its Phase-2
+   furthest-in-future evictions).  Returns 0, or -1 on allocation failure. */
 int oracle_replay(const uint32_t* conv, const uint32_t* q, const uint32_t* a, uint64_t E,
                   int policy, uint64_t C, uint64_t xi, uint64_t q_hat, uint64_t threshold,
                   uint64_t* b_out, uint64_t* counters_out) {
@@ -400,6 +486,13 @@ int oracle_replay(const uint32_t* conv, const uint32_t* q, const uint32_t* a, ui
         seen[dense[t]] = (int64_t)t;
     }
     free(seen);
+    if (policy == 5) {  /* Tail-Optimized Belady (Thm 1) */
+        int rc = replay_tail_belady(dense, n, q, a, nxt, E, C, xi, b_out, counters_out);
+        free(s);
+        free(dense);
+        free(nxt);
+        return rc;
+    }
     list_ends res = {-1, -1}, fre = {-1, -1};
     /* Free tail per conversation D = max(xi - q_hat, 0): the blocks at the end
        of the history beyond the TEL-safe budget L + Q_hat - xi (P:56, P:62
