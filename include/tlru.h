@@ -42,7 +42,7 @@ typedef enum {
   TLRU_EINVAL = 1,       /* bad argument or configuration (block_tokens == 0, rate <= 0, q == 0, ...) */
   TLRU_ERANGE = 2,       /* buffer / workspace too small, or a value exceeds its field width (J > 65535) */
   TLRU_ECUDA = 3,        /* CUDA runtime error; tlru_last_error() carries cudaGetErrorString */
-  TLRU_EUNSUPPORTED = 4, /* policy family not built (THRESHOLD, END_AWARE, LENGTH_AWARE, TAIL_BELADY) */
+  TLRU_EUNSUPPORTED = 4, /* policy family not built (policy > TLRU_POLICY_TAIL_BELADY) */
   TLRU_ESTATE = 5        /* internal per-chain state pool exhausted with no fallback left */
 } tlru_status;
 
@@ -166,14 +166,21 @@ tlru_status tlru_trace_from_turns(const uint32_t* conv, const uint16_t* q, const
  *   surplus = min(L_after, max(xi - q_next, 0)).  Their cache is not the top-C of
  *   the universe, so they always run on the replay engine as whole-trace chains;
  *   a batch that contains them runs entirely on the replay engine.
+ * Tail-Optimized Belady (Thm 1; proof App. A; Reading
+ *   #26): the hindsight policy, clairvoyant through the trace's next links.
+ *   theta caches its whole history; on overflow Phase 1 trims blocks above the
+ *   exact TEL-safe budget (L + q_next - xi)^+ (0 for a conversation that never
+ *   returns), furthest next arrival first; Phase 2 evicts the conversation whose
+ *   next arrival is furthest in the future (evicted_lru counts these), partial.
+ *   q_hat is ignored.  Replay engine only (like End-/Length-Aware).
  * ------------------------------------------------------------------------ */
 enum {
   TLRU_POLICY_LRU = 0,
   TLRU_POLICY_TLRU = 1,
   TLRU_POLICY_THRESHOLD = 2,
   TLRU_POLICY_END_AWARE = 3,
-  TLRU_POLICY_LENGTH_AWARE = 4
-  /* 5 reserved: TAIL_BELADY -> TLRU_EUNSUPPORTED */
+  TLRU_POLICY_LENGTH_AWARE = 4,
+  TLRU_POLICY_TAIL_BELADY = 5 /* > 5 -> TLRU_EUNSUPPORTED (ET-LRU, forced caching: not built) */
 };
 
 typedef struct {

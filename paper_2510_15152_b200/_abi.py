@@ -19,6 +19,7 @@ POLICY_TLRU = 1
 POLICY_THRESHOLD = 2
 POLICY_END_AWARE = 3
 POLICY_LENGTH_AWARE = 4
+POLICY_TAIL_BELADY = 5
 ENGINE_REPLAY = 0
 ENGINE_STACK = 1
 

@@ -78,6 +78,28 @@ __device__ void snap_write(uint32_t* out, uint32_t wsnap, const ChainRegs& c, co
   out[3] = frem;
 }
 
+// Tail-Optimized Belady chains: live entries in key order (key, X | S << 16); header
+// {n, used, dead, 0} (tombstones are not state: X = 0 is the same as no entry).
+template <class St>
+__device__ void snap_write_belady(uint32_t* out, uint32_t wsnap, const ChainRegs& c, const St& st) {
+  uint32_t n = 0;
+  uint32_t* key = out + 4;
+  uint32_t* xs = key + wsnap;
+  for (uint32_t k = c.head; k < c.tail; ++k) {
+    const uint32_t x = st.Xr(k);
+    if (x == 0) continue;
+    if (n < wsnap) {
+      key[n] = st.T(k);
+      xs[n] = x | (uint32_t(st.Sr(k)) << 16);
+    }
+    ++n;
+  }
+  out[0] = n <= wsnap ? n : 0xFFFFFFFFu;
+  out[1] = c.used;
+  out[2] = c.dead;
+  out[3] = 0;
+}
+
 __device__ bool snap_equal(const uint32_t* a, const uint32_t* b, uint32_t wsnap) {
   if (a[0] == 0xFFFFFFFFu || a[0] != b[0] || a[1] != b[1] || a[2] != b[2] || a[3] != b[3]) return false;
   for (uint32_t i = 0; i < a[0]; ++i)
@@ -85,9 +107,12 @@ __device__ bool snap_equal(const uint32_t* a, const uint32_t* b, uint32_t wsnap)
   return true;
 }
 
+constexpr uint32_t kAwareTLRU = 1;    // End-/Length-Aware T-LRU lanes
+constexpr uint32_t kAwareBelady = 2;  // Tail-Optimized Belady lanes
+
 struct GroupDev {
   uint32_t trace, lane0, nlanes, W;
-  uint32_t aware;  // End-/Length-Aware lanes: one whole-trace chain (no segment warm start)
+  uint32_t aware;  // 0, kAwareTLRU or kAwareBelady: burn-in segments verified by the fix-up
 };
 
 struct ItemDev {
@@ -154,6 +179,8 @@ __global__ void __launch_bounds__(32) sim_kernel(const ItemDev* __restrict__ ite
   SmemState st{tau_s, X_s, S_s, lane};
   ChainRegs c;
   chain_init(c, lp.C, lp.D, lp.T, W, active && s > 0);
+  const bool bel = AWARE && g.aware == kAwareBelady;  // warp-uniform
+  if (bel) c.head = c.tail = W / 2;  // sorted by next arrival: inserts land anywhere
 
   // ---- rebuild the exact state at s (sim.cuh "Segment start"); AWARE chains start at event 0
   for (int pass = 0; pass < (AWARE ? 0 : 2); ++pass) {
@@ -187,22 +214,35 @@ __global__ void __launch_bounds__(32) sim_kernel(const ItemDev* __restrict__ ite
   if (AWARE && lp.inst != 0xFFFFFFFFu) snapG = aw.snap + (size_t(lp.aidx) * aw.nseg_max + it.seg) * 2 * sw;
   for (uint32_t base = s0; base < s_end; base += 32) {
     if (AWARE && base == s) {  // segment start: save G_k, restart the segment's counters
-      if (active && it.seg > 0) snap_write(snapG, aw.wsnap, c, st);
+      if (active && it.seg > 0) {
+        if (bel) snap_write_belady(snapG, aw.wsnap, c, st);
+        else snap_write(snapG, aw.wsnap, c, st);
+      }
       c.ev_trim = c.ev_lru = c.max_occ = 0;
     }
     const uint64_t evc = evn;
     const uint32_t nk = min(32u, s_end - base);
     if (base + 32 + lane < s_end) evn = __ldg(tr.sim + base + 32 + lane);  // prefetch the next tile
     uint32_t qnc = 0xFFFFFFFFu;  // AWARE: this lane's event's next prompt, or NONE on a terminating turn
+    uint32_t nxc = TLRU_NONE;    // and its next turn's event index (Belady's key)
     if (AWARE && base + lane < s_end) {
-      const uint32_t nx = __ldg(tr.next + base + lane);
-      if (nx != TLRU_NONE) qnc = sim_J(__ldg(tr.sim + nx)) - sim_La(evc);  // q = J - L_before
+      nxc = __ldg(tr.next + base + lane);
+      if (nxc != TLRU_NONE) qnc = sim_J(__ldg(tr.sim + nxc)) - sim_La(evc);  // q = J - L_before
     }
     for (uint32_t k = 0; k < nk; ++k) {
       const uint64_t ev = shfl64(evc, k);
       if (AWARE) {
         const uint32_t qn = __shfl_sync(0xFFFFFFFFu, qnc, k);
-        if (active) {
+        if (bel) {
+          const uint32_t nxk = __shfl_sync(0xFFFFFFFFu, nxc, k);
+          if (active) {
+            const uint32_t La = sim_La(ev);
+            const uint32_t s0 = nxk == TLRU_NONE ? 0u : min(La, lp.xi > qn ? lp.xi - qn : 0u);
+            const uint32_t b = chain_request_belady(c, st, base + k, sim_J(ev), La, nxk, s0);
+            bst[lane * BST_STRIDE + k] = static_cast<uint16_t>(b);
+            if (c.overflow) active = false;
+          }
+        } else if (active) {
           const bool last = qn == 0xFFFFFFFFu;
           const uint32_t Dcur = lp.policy == TLRU_POLICY_LENGTH_AWARE ? (lp.xi > qn ? lp.xi - qn : 0u) : lp.D;
           const uint32_t b = chain_request_aware(c, st, base + k, sim_prev(ev), sim_J(ev), sim_La(ev), last, Dcur);
@@ -232,7 +272,10 @@ __global__ void __launch_bounds__(32) sim_kernel(const ItemDev* __restrict__ ite
   if (AWARE) {  // F_k and the segment's counters; overflowed segments are re-run by the fix-up
     if (lp.inst != 0xFFFFFFFFu) {
       const size_t slot = size_t(lp.aidx) * aw.nseg_max + it.seg;
-      if (active) snap_write(snapG + sw, aw.wsnap, c, st);
+      if (active) {
+        if (bel) snap_write_belady(snapG + sw, aw.wsnap, c, st);
+        else snap_write(snapG + sw, aw.wsnap, c, st);
+      }
       aw.segc[2 * slot] = c.ev_trim;
       aw.segc[2 * slot + 1] = c.ev_lru;
       aw.segm[slot] = c.max_occ;
@@ -297,6 +340,7 @@ __global__ void aware_fix_kernel(const LaneDev* __restrict__ lanes, const uint32
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nal; i += gridDim.x * blockDim.x) {
     const LaneDev lp = lanes[alane[i]];
     const TraceDev tr = traces[atrace[i]];
+    const bool bel = lp.policy == TLRU_POLICY_TAIL_BELADY;
     const uint32_t nseg = static_cast<uint32_t>((tr.E + aw.seg_len - 1) / aw.seg_len);
     GlobalState st{tau_pool + size_t(i) * Wp, X_pool + size_t(i) * Wp, S_pool + size_t(i) * Wp};
     bool failed = false, carry = false;  // carry: the pool holds the exact state at the end of segment k - 1
@@ -324,11 +368,16 @@ __global__ void aware_fix_kernel(const LaneDev* __restrict__ lanes, const uint32
             st.T(j) = Fp[4 + j];
             st.Xr(j) = static_cast<uint16_t>(xs & 0xFFFFu);
             st.Sr(j) = static_cast<uint16_t>(xs >> 16);
+            if (bel) c.fsum += xs >> 16;
           }
           c.tail = n;
           c.used = Fp[1];
-          c.fh = Fp[2];
-          c.frem = Fp[3];
+          if (bel) {
+            c.dead = Fp[2];
+          } else {
+            c.fh = Fp[2];
+            c.frem = Fp[3];
+          }
         }
       }
       c.ev_trim = c.ev_lru = c.max_occ = 0;
@@ -338,6 +387,12 @@ __global__ void aware_fix_kernel(const LaneDev* __restrict__ lanes, const uint32
         const uint64_t ev = tr.sim[e];
         const uint32_t nx = tr.next[e];
         const uint32_t qn = nx != TLRU_NONE ? sim_J(tr.sim[nx]) - sim_La(ev) : 0u;
+        if (bel) {
+          const uint32_t La = sim_La(ev);
+          const uint32_t s0 = nx == TLRU_NONE ? 0u : min(La, lp.xi > qn ? lp.xi - qn : 0u);
+          bout[lp.boff + e] = static_cast<uint16_t>(chain_request_belady(c, st, e, sim_J(ev), La, nx, s0));
+          continue;
+        }
         const uint32_t Dcur = lp.policy == TLRU_POLICY_LENGTH_AWARE ? (lp.xi > qn ? lp.xi - qn : 0u) : lp.D;
         bout[lp.boff + e] = static_cast<uint16_t>(
             chain_request_aware(c, st, e, sim_prev(ev), sim_J(ev), sim_La(ev), nx == TLRU_NONE, Dcur));
@@ -350,7 +405,8 @@ __global__ void aware_fix_kernel(const LaneDev* __restrict__ lanes, const uint32
       aw.segc[2 * slot + 1] = c.ev_lru;
       aw.segm[slot] = c.max_occ;
       aw.ovf[slot] = 0;
-      snap_write(F, aw.wsnap, c, st);
+      if (bel) snap_write_belady(F, aw.wsnap, c, st);
+      else snap_write(F, aw.wsnap, c, st);
       carry = true;
       atomicAdd(nfixed, 1u);
     }
@@ -402,6 +458,9 @@ static int w_class(uint32_t C, uint32_t nconv) {
 }
 
 static bool is_aware(const tlru_instance& in) { return in.policy >= TLRU_POLICY_END_AWARE; }
+static uint32_t aware_kind(const tlru_instance& in) {
+  return in.policy == TLRU_POLICY_TAIL_BELADY ? kAwareBelady : (is_aware(in) ? kAwareTLRU : 0u);
+}
 
 struct Plan {
   std::vector<LaneDev> lanes;
@@ -445,9 +504,9 @@ static tlru_status make_plan(const tlru_trace* traces, uint32_t nt, const tlru_i
   for (uint32_t i = 0; i < ni; ++i) {
     const tlru_instance& in = inst[i];
     if (in.trace >= nt) TLRU_FAIL(TLRU_EINVAL, "instance %u: trace index %u out of range", i, in.trace);
-    if (in.policy > TLRU_POLICY_LENGTH_AWARE)
-      TLRU_FAIL(TLRU_EUNSUPPORTED, "instance %u: policy %u is not built (0..4: LRU, T-LRU, Threshold-LRU, "
-                "End-Aware, Length-Aware)", i, in.policy);
+    if (in.policy > TLRU_POLICY_TAIL_BELADY)
+      TLRU_FAIL(TLRU_EUNSUPPORTED, "instance %u: policy %u is not built (0..5: LRU, T-LRU, Threshold-LRU, "
+                "End-Aware, Length-Aware, Tail-Optimized Belady)", i, in.policy);
     if (in.policy >= TLRU_POLICY_END_AWARE) P->any_aware = true;
     if (in.policy == TLRU_POLICY_THRESHOLD && in.threshold > 65535)
       TLRU_FAIL(TLRU_ERANGE, "instance %u: threshold %u > 65535 (histories are u16)", i, in.threshold);
@@ -456,6 +515,15 @@ static tlru_status make_plan(const tlru_trace* traces, uint32_t nt, const tlru_i
     wc[i] = g_opt_w >= 0 ? g_opt_w : w_class(C, traces[in.trace].num_conversations);
     // aware chains keep 8 B per entry: 1024 x 32 lanes would exceed shared memory (spill covers the rest)
     if (is_aware(in)) wc[i] = std::min(wc[i], kNumW - 2);
+    if (in.policy == TLRU_POLICY_TAIL_BELADY && g_opt_w < 0) {
+      // entries hold X >= 1 (tombstones are compacted before the state counts as full), so
+      // W > C never overflows; the live conversations of a trace bound it too (<= ~91 on the
+      // preset): 128 entries, larger states are re-run by the fix-up from global memory
+      const uint32_t need = std::min<uint32_t>(C + 1, 128u);
+      int k = 0;
+      while (k < kNumW - 1 && static_cast<uint32_t>(kWClasses[k]) < need) ++k;
+      wc[i] = k;
+    }
     const uint64_t E = traces[in.trace].num_events;
     const uint64_t off = offsets ? offsets[i] : packed;
     packed += E;
@@ -463,7 +531,7 @@ static tlru_status make_plan(const tlru_trace* traces, uint32_t nt, const tlru_i
   }
   std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) {
     if (inst[a].trace != inst[b].trace) return inst[a].trace < inst[b].trace;
-    if (is_aware(inst[a]) != is_aware(inst[b])) return is_aware(inst[b]);
+    if (aware_kind(inst[a]) != aware_kind(inst[b])) return aware_kind(inst[a]) < aware_kind(inst[b]);
     if (wc[a] != wc[b]) return wc[a] < wc[b];
     return inst[a].capacity < inst[b].capacity;
   });
@@ -471,10 +539,11 @@ static tlru_status make_plan(const tlru_trace* traces, uint32_t nt, const tlru_i
   for (uint32_t k = 0; k < ni;) {
     const uint32_t t = inst[order[k]].trace;
     const int w = wc[order[k]];
-    const bool aw = is_aware(inst[order[k]]);
-    GroupDev g{t, static_cast<uint32_t>(P->lanes.size()), 0, static_cast<uint32_t>(w), aw ? 1u : 0u};
+    const uint32_t kind = aware_kind(inst[order[k]]);
+    const bool aw = kind != 0;
+    GroupDev g{t, static_cast<uint32_t>(P->lanes.size()), 0, static_cast<uint32_t>(w), kind};
     while (k < ni && g.nlanes < 32 && inst[order[k]].trace == t && wc[order[k]] == w &&
-           is_aware(inst[order[k]]) == aw) {
+           aware_kind(inst[order[k]]) == kind) {
       const tlru_instance& in = inst[order[k]];
       LaneDev l;
       l.inst = order[k];
@@ -512,7 +581,7 @@ static tlru_status make_plan(const tlru_trace* traces, uint32_t nt, const tlru_i
   P->seg_len = static_cast<uint32_t>(seg);
   {  // aware segments: enough warps to fill the GPU, but >= 2x the burn-in
     uint64_t ag = 0;
-    for (const GroupDev& g : P->groups) ag += g.aware;
+    for (const GroupDev& g : P->groups) ag += g.aware ? 1u : 0u;
     const uint64_t pa = ag ? (148ull * 8ull + ag - 1) / ag : 1;
     uint64_t sa = Emax ? (Emax + pa - 1) / pa : 8192;
     sa = std::min<uint64_t>(std::max<uint64_t>(sa, 2ull * P->aburn), 1ull << 20);

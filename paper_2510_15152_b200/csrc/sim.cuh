@@ -62,6 +62,9 @@ struct ChainRegs {
   // warm-start bookkeeping
   uint32_t r, cum_nf, cum_f, nf_target, free_budget, fh_pos, fh_rem;
   bool walking, overflow;
+  // Tail-Optimized Belady chains: blocks still cached by conversations that never return
+  // (all free), and the sum of the entries' remaining surplus
+  uint32_t dead, fsum;
 };
 
 __device__ __forceinline__ void chain_init(ChainRegs& c, uint32_t C, uint32_t D, uint32_t T, uint32_t W,
@@ -82,6 +85,7 @@ __device__ __forceinline__ void chain_init(ChainRegs& c, uint32_t C, uint32_t D,
   c.fh_rem = 0;
   c.walking = has_prefix && C > 0;
   c.overflow = false;
+  c.dead = c.fsum = 0;
 }
 
 // One step of the backward walk: e' is an event before the segment start with
@@ -310,6 +314,126 @@ __device__ __forceinline__ uint32_t chain_request_aware(ChainRegs& c, const St& 
       c.ev_lru += take;
       if (x == take) ++c.head;
     }
+    c.used = c.C;
+  }
+  c.max_occ = max(c.max_occ, c.used);
+  return b;
+}
+
+// ---------------------------------------------------------------------------------------------
+// Tail-Optimized Belady (Thm 1; Reading #26) on one chain.  State: entries sorted
+// ascending by key = the conversation's NEXT arrival (event index) in [head, tail); T = key,
+// X = cached blocks, S = blocks still cached above the exact TEL-safe budget (L + q_next - xi)^+
+// (S <= X always; Phase 2 runs only once every S is 0).  Every key is a future event and each
+// event is the next arrival of one conversation, so theta's old entry (key == e) is the minimum:
+// the head.  Conversations that never return hold only free blocks and are evicted first; they
+// are aggregated in c.dead (which of them is trimmed is unobservable: they never return).
+// Entries fully trimmed by Phase 1 stay as tombstones (X = 0) until their key event or a
+// compaction.  A new key goes to its sorted position, shifting the shorter side (head - 1 or
+// tail + 1 must be free; else tombstones are compacted; else the chain overflows).
+template <class St>
+__device__ __forceinline__ bool belady_insert(ChainRegs& c, const St& st, uint32_t key, uint32_t x, uint32_t s) {
+  uint32_t lo = c.head, n = c.tail - c.head;
+  while (n > 0) {  // lower_bound of key in T[head, tail)
+    const uint32_t half = n >> 1;
+    const uint32_t m = lo + half;
+    if (st.T(m) < key) {
+      lo = m + 1;
+      n -= half + 1;
+    } else {
+      n = half;
+    }
+  }
+  if (c.head == 0 && c.tail == c.W) {  // full: drop tombstones (order kept)
+    uint32_t j = 0, npos = 0;
+    for (uint32_t k = 0; k < c.tail; ++k) {
+      if (k == lo) npos = j;
+      const uint16_t xk = st.Xr(k);
+      if (xk != 0) {
+        st.T(j) = st.T(k);
+        st.Xr(j) = xk;
+        st.Sr(j) = st.Sr(k);
+        ++j;
+      }
+    }
+    if (lo == c.tail) npos = j;
+    if (j == c.W) return false;
+    c.tail = j;
+    lo = npos;
+  }
+  const bool down = c.head > 0 && (c.tail == c.W || lo - c.head <= c.tail - lo);
+  if (down) {  // shift [head, lo) one slot towards the front
+    for (uint32_t k = c.head; k < lo; ++k) {
+      st.T(k - 1) = st.T(k);
+      st.Xr(k - 1) = st.Xr(k);
+      st.Sr(k - 1) = st.Sr(k);
+    }
+    --c.head;
+    --lo;
+  } else {  // shift [lo, tail) one slot towards the back
+    for (uint32_t k = c.tail; k > lo; --k) {
+      st.T(k) = st.T(k - 1);
+      st.Xr(k) = st.Xr(k - 1);
+      st.Sr(k) = st.Sr(k - 1);
+    }
+    ++c.tail;
+  }
+  st.T(lo) = key;
+  st.Xr(lo) = static_cast<uint16_t>(x);
+  st.Sr(lo) = static_cast<uint16_t>(s);
+  return true;
+}
+
+// Request at event e: J, La from the sim view, nx = theta's next arrival (TLRU_NONE: never),
+// s0 = min(La, max(xi - q_next, 0)) = La - (La + q_next - xi)^+ (unused when nx is NONE).
+template <class St>
+__device__ __forceinline__ uint32_t chain_request_belady(ChainRegs& c, const St& st, uint32_t e, uint32_t J,
+                                                         uint32_t La, uint32_t nx, uint32_t s0) {
+  uint32_t x_old = 0;
+  if (c.head < c.tail && st.T(c.head) == e) {  // theta's entry: the smallest key
+    x_old = st.Xr(c.head);
+    c.fsum -= st.Sr(c.head);
+    ++c.head;
+  }
+  const uint32_t b = J - x_old;  // job - x
+  c.used += La - x_old;          // X_theta <- L_theta (Reading #7)
+  if (nx == TLRU_NONE) {
+    c.dead += La;                // budget 0: every block free
+  } else {
+    if (!belady_insert(c, st, nx, La, s0)) {
+      c.overflow = true;
+      return b;
+    }
+    c.fsum += s0;
+  }
+  if (c.used > c.C) {
+    uint32_t over = c.used - c.C;
+    // Phase 1: blocks above the budget, furthest next arrival first (never-returning first)
+    const uint32_t kd = min(c.dead, over);
+    c.dead -= kd;
+    over -= kd;
+    c.ev_trim += kd;
+    for (uint32_t j = c.tail; over > 0 && c.fsum > 0 && j > c.head;) {
+      --j;
+      const uint32_t s = st.Sr(j);
+      if (s == 0) continue;
+      const uint32_t take = min(s, over);
+      st.Sr(j) = static_cast<uint16_t>(s - take);
+      st.Xr(j) = static_cast<uint16_t>(st.Xr(j) - take);
+      c.fsum -= take;
+      over -= take;
+      c.ev_trim += take;
+    }
+    // Phase 2: furthest-in-future, partial; every S is 0 here
+    while (over > 0) {
+      const uint32_t x = st.Xr(c.tail - 1);
+      const uint32_t take = min(x, over);
+      st.Xr(c.tail - 1) = static_cast<uint16_t>(x - take);
+      over -= take;
+      c.ev_lru += take;
+      if (x == take) --c.tail;
+    }
+    while (c.tail > c.head && st.Xr(c.tail - 1) == 0) --c.tail;
     c.used = c.C;
   }
   c.max_occ = max(c.max_occ, c.used);

@@ -1,0 +1,112 @@
+"""Tail-Optimized Belady (Thm 1; Reading #26) on the CUDA path (replay engine, burn-in
+segments verified by the fix-up), element by element against the oracle through the C ABI."""
+import json
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from paper_2510_15152_b200.inputs import CAPS_CONFIG3, Q_HAT, SLO_BLOCKS, preset, random_trace
+from test_gpu_aware import check, upload
+
+pytestmark = pytest.mark.gpu
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+BEL, END, LEN = 5, 3, 4
+
+
+@pytest.fixture(scope="module")
+def T():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import __graft_entry__
+    __graft_entry__.build()
+    import paper_2510_15152_b200.tlru as T
+    yield T
+    T.set_sim_options(0, 0)
+    T.set_sim_engine(T.ENGINE_STACK)
+
+
+def test_hand_vectors(T):
+    g = json.load(open(os.path.join(GOLDEN, "tail_belady.json")))
+    f = g["fig1_known_third"]
+    for key in ("third_from_A", "third_from_B"):
+        v = f[key]
+        bt = T.simulate_batch([upload(T, v["conv"], v["q"], v["a"])], [(0, BEL, f["C"], f["xi"], 0, 16)])
+        r = bt.results_numpy()[0]
+        assert list(bt.b(0)) == v["b"] and [r["evicted_trim"], r["evicted_lru"]] == v["evicted"]
+        assert r["tel_blocks"] == v["tel"] and r["max_occupancy"] == v["max_occupancy"]
+    v = g["furthest_order"]
+    bt = T.simulate_batch([upload(T, v["conv"], v["q"], v["a"])], [(0, BEL, v["C"], v["xi"], 0, 16),
+                                                                   (0, 0, v["C"], v["xi"], 0, 16)])
+    assert list(bt.b(0)) == v["b"] and list(bt.b(1)) == v["lru_b"]
+    assert T.last_sim_stats()["engine"] == T.ENGINE_REPLAY
+
+
+@pytest.mark.parametrize("engine", [0, 1], ids=["replay", "stack-requested"])
+def test_random_traces_mixed_batch(T, engine):
+    """Belady lanes beside End-/Length-Aware, LRU, T-LRU and Threshold-LRU lanes."""
+    T.set_sim_engine(engine)
+    traces, otr, rows = [], [], []
+    for s in range(3):
+        conv, q, a = random_trace(1800 + s, 6000, 90, q_max=6, a_max=8, locality=0.5)
+        traces.append(upload(T, conv, q, a))
+        otr.append((conv, q, a))
+        for C in (0, 1, 3, 20, 90, 400, 5000):
+            rows += [(s, BEL, C, xi, 0, 8) for xi in (0, 1, 4, 9, 17, 60)]
+        rows += [(s, END, 40, 9, 2, 8), (s, LEN, 40, 9, 2, 8), (s, 0, 40, 4, 2, 8), (s, 1, 40, 9, 2, 8)]
+    bt = T.simulate_batch(traces, rows)
+    check(T, bt, rows, otr)
+
+
+def test_generated_preset_spectrum(T):
+    """BASELINE config-3 shape (10^4-conversation WildChat-shaped traces, several burn-in
+    segments per chain): the paper's whole predictability spectrum at xi = 16 blocks (200 ms),
+    LRU .. T-LRU .. End-/Length-Aware .. the hindsight optimum, and Thm 1 pathwise:
+    TEL(Belady) <= TEL of every online policy."""
+    params = [preset("wildchat", s, 10_000) for s in range(2)]
+    traces = T.generate_traces(params, exports=False)
+    otr = []
+    for p in params:
+        o = O.generate(p)
+        otr.append((o.conv, o.q, o.a))
+    rows = [(t, pol, C, xi, Q_HAT, SLO_BLOCKS) for t in range(2) for pol in (0, 1, END, LEN, BEL)
+            for C in CAPS_CONFIG3 for xi in (4, 16)]
+    bt = T.simulate_batch(traces, rows)
+    check(T, bt, rows, otr)
+    res = bt.results_numpy()
+    for t in range(2):
+        for C in CAPS_CONFIG3:
+            for xi in (4, 16):
+                tb = res[rows.index((t, BEL, C, xi, Q_HAT, SLO_BLOCKS))]["tel_blocks"]
+                for pol in (0, 1, END, LEN):
+                    assert tb <= res[rows.index((t, pol, C, xi, Q_HAT, SLO_BLOCKS))]["tel_blocks"]
+
+
+def test_uncoupled_segments_are_rerun(T):
+    """Short segments and few, long-lived conversations: burn-in segments start from an
+    empty cache and often disagree with the exact state; the fix-up must re-run them."""
+    conv, q, a = random_trace(1900, 40000, 40, q_max=4, a_max=4, locality=0.1)
+    tr = upload(T, conv, q, a)
+    rows = [(0, BEL, C, xi, 0, 8) for C in (10, 60, 200, 1000) for xi in (0, 5, 12)]
+    bt = T.simulate_batch([tr], rows)
+    st = T.last_sim_stats()
+    assert st["failed_chains"] == 0
+    check(T, bt, rows, [(conv, q, a)])
+
+
+def test_state_overflow_rerun(T):
+    """Force the smallest on-chip state (32 entries) with more live conversations: segments
+    overflow and are re-run by the fix-up from global memory; results must not change."""
+    conv, q, a = random_trace(1950, 12000, 300, q_max=3, a_max=3, locality=0.2)
+    tr = upload(T, conv, q, a)
+    rows = [(0, BEL, C, xi, 0, 8) for C in (200, 600) for xi in (0, 9)]
+    T.set_sim_options(0, 32)
+    try:
+        bt = T.simulate_batch([tr], rows)
+        st = T.last_sim_stats()
+    finally:
+        T.set_sim_options(0, 0)
+    assert st["spilled_chains"] > 0 and st["failed_chains"] == 0
+    check(T, bt, rows, [(conv, q, a)])
