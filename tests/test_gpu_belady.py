@@ -110,3 +110,32 @@ def test_state_overflow_rerun(T):
         T.set_sim_options(0, 0)
     assert st["spilled_chains"] > 0 and st["failed_chains"] == 0
     check(T, bt, rows, [(conv, q, a)])
+
+
+def test_full_size_spectrum_sampled(T):
+    """BASELINE full trace size (10^6 conversations, ~2.5x10^6 requests) in the launch
+    configuration `bench.py --config spectrum` times (one trace, its 300 spectrum rows in one
+    batch): sampled instances against the oracle element by element."""
+    from paper_2510_15152_b200.inputs import CAPS_CONFIG5
+    p = preset("wildchat", 3, 1_000_000)
+    tr = T.generate_traces([p], exports=False)[0]
+    rows = [(0, pol, C, xi, Q_HAT, SLO_BLOCKS) for pol in (END, LEN, BEL) for C in CAPS_CONFIG5
+            for xi in (4, 8, 16, 24)]
+    bt = T.simulate_batch([tr], rows)
+    assert T.last_sim_stats()["failed_chains"] == 0
+    o = O.generate(p)
+    picks = [(BEL, 16, 4), (BEL, 256, 24), (BEL, 4096, 16), (BEL, CAPS_CONFIG5[9], 8), (END, 512, 16),
+             (LEN, 64, 24)]
+    sub_rows = [rows.index((0, pol, C, xi, Q_HAT, SLO_BLOCKS)) for pol, C, xi in picks]
+
+    class Sub:  # the picked instances of the full batch
+        def __init__(self, bt, idx):
+            self.bt, self.idx = bt, idx
+
+        def b(self, k):
+            return self.bt.b(self.idx[k])
+
+        def results_numpy(self):
+            return self.bt.results_numpy()[self.idx]
+
+    check(T, Sub(bt, sub_rows), [rows[i] for i in sub_rows], [(o.conv, o.q, o.a)])
