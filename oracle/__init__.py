@@ -67,6 +67,10 @@ def lib():
         L.oracle_replay.argtypes = [u32p, u32p, u32p, ctypes.c_uint64, ctypes.c_int, ctypes.c_uint64,
                                     ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, u64p, u64p]
         L.oracle_replay.restype = ctypes.c_int
+        L.oracle_replay_etlru.argtypes = [u32p, u32p, u32p, u64p, ctypes.c_uint64, ctypes.c_uint64,
+                                          ctypes.c_uint64, ctypes.c_double, ctypes.POINTER(ctypes.c_double),
+                                          ctypes.c_uint64, u64p, u64p]
+        L.oracle_replay_etlru.restype = ctypes.c_int
         L.oracle_tail.argtypes = [u64p, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_double, ctypes.c_uint64,
                                   ctypes.c_double, u64p, ctypes.POINTER(ctypes.c_double)]
         L.oracle_tail.restype = ctypes.c_int
@@ -191,6 +195,7 @@ THRESHOLD = 2
 END_AWARE = 3
 LENGTH_AWARE = 4
 TAIL_BELADY = 5  # Thm 1 hindsight policy, Reading #26
+ET_LRU = 6  # Def. 1 / Alg. 2, Reading #27 -- see replay_etlru
 
 
 @dataclass
@@ -215,6 +220,28 @@ def replay(conv, q, a, policy: int, C: int, xi: int = 0, q_hat: int = 0, thresho
                              _p(cnt, ctypes.c_uint64))
     if rc != 0:
         raise MemoryError("oracle_replay")
+    return Replay(b, int(cnt[0]), int(cnt[1]), int(cnt[2]))
+
+
+def replay_etlru(conv, q, a, ticks, C: int, xi: int, mu_tick: float, ln_surv) -> Replay:
+    """Expected-Tail-Optimized LRU (Def. 1 / Alg. 2; Reading #27):
+    greedy block-by-block eviction by the ranking criterion mu * time_i + ln P(Q >= X_i - L_i + xi).
+    ticks[E]: event times (u64 microseconds); ln_surv[k] = ln P(Q >= k), k = 0..K.
+    evicted_trim = blocks evicted with P = 0, evicted_lru = the others."""
+    conv = np.ascontiguousarray(conv, dtype=np.uint32)
+    q = np.ascontiguousarray(q, dtype=np.uint32)
+    a = np.ascontiguousarray(a, dtype=np.uint32)
+    ticks = np.ascontiguousarray(ticks, dtype=np.uint64)
+    ls = np.ascontiguousarray(ln_surv, dtype=np.float64)
+    E = conv.shape[0]
+    b = np.zeros(E, np.uint64)
+    cnt = np.zeros(3, np.uint64)
+    rc = lib().oracle_replay_etlru(_p(conv, ctypes.c_uint32), _p(q, ctypes.c_uint32), _p(a, ctypes.c_uint32),
+                                   _p(ticks, ctypes.c_uint64), E, int(C), int(xi), float(mu_tick),
+                                   _p(ls, ctypes.c_double), ls.shape[0] - 1, _p(b, ctypes.c_uint64),
+                                   _p(cnt, ctypes.c_uint64))
+    if rc != 0:
+        raise MemoryError("oracle_replay_etlru")
     return Replay(b, int(cnt[0]), int(cnt[1]), int(cnt[2]))
 
 

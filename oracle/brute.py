@@ -18,6 +18,11 @@ rational arithmetic (``fractions.Fraction``):
   Theorem 2's corollary says T-LRU (Alg. 1 with Q_hat = Q) attains the
   minimum; its first corollary says LRU does when xi = 0.
 
+* ``etlru_step`` / ``etlru_objective_min``: Expected-Tail-Optimized LRU (Def. 1)
+  in exact rationals -- the greedy of Alg. 2 and, independently, the exhaustive
+  minimum of Def. 1's objective (8) over every feasible allocation (the Lemma).
+  ``belief_mdp_value(..., q_pmf=...)`` draws the next prompt from a pmf (Thm 3).
+
 ``tlru_step`` is a plain Python transcription of Alg. 1 used only
 inside these recursions (and by the convention-vector tests); it shares no
 code with the C oracle or the CUDA path.
@@ -58,6 +63,48 @@ def tlru_step(X, L, ages, theta, C, xi, q_hat, policy, budget="strict"):
     return X
 
 
+# ----------------------------------------------------------------------------- Def. 1 / Alg. 2
+def surv(q_pmf, k):
+    """P(Q >= k) for a pmf {q: p} (exact)."""
+    return sum((p for qq, p in q_pmf.items() if qq >= k), Fraction(0))
+
+
+def etlru_step(X, L, lam, C, xi, q_pmf, tau=None):
+    """Alg. 2: evict sum(X) - C blocks one at a time from argmin of
+    v_i = lam_i * P(L_i + Q_i - xi >= X_i) (X_i >= 1), re-scoring after each block.
+    Ties -> smaller tau (older last turn) first.  X, L, lam (Fractions), tau: lists."""
+    X = list(X)
+    tau = tau if tau is not None else list(range(len(X)))
+    while sum(X) > C:
+        best = None
+        for i in range(len(X)):
+            if X[i] < 1:
+                continue
+            v = lam[i] * surv(q_pmf, X[i] - L[i] + xi)
+            if best is None or v < best[0] or (v == best[0] and tau[i] < tau[best[1]]):
+                best = (v, i)
+        X[best[1]] -= 1
+    return X
+
+
+def etlru_objective(Y, L, lam, xi, q_pmf):
+    """Def. 1 objective (8): sum_i lam_i E[(L_i + Q_i - Y_i - xi)^+]."""
+    return sum(lam[i] * sum(p * max(L[i] + qq - Y[i] - xi, 0) for qq, p in q_pmf.items())
+               for i in range(len(Y)))
+
+
+def etlru_objective_min(X, L, lam, C, xi, q_pmf):
+    """min of (8) over Y with Y_i <= X_i (X_theta = L_theta already) and sum Y <= C."""
+    best = None
+    for Y in product(*[range(u + 1) for u in X]):
+        if sum(Y) > C:
+            continue
+        v = etlru_objective(Y, L, lam, xi, q_pmf)
+        if best is None or v < best:
+            best = v
+    return best
+
+
 # ----------------------------------------------------------------------------- Thm 1 / Eq. 5
 def hindsight_opt(conv, q, a, C: int, xi: int) -> int:
     """min sum_t (J_t - x_{theta,t} - xi)^+ over cache schedules obeying (2)-(4)."""
@@ -90,10 +137,12 @@ def hindsight_opt(conv, q, a, C: int, xi: int) -> int:
 
 
 # ----------------------------------------------------------------------------- Thm 2 belief MDP
-def belief_mdp_value(C, xi, Q, A_set, rho, w_new, n_max, M, policy=None, budget="strict"):
+def belief_mdp_value(C, xi, Q, A_set, rho, w_new, n_max, M, policy=None, budget="strict", q_pmf=None):
     """Expected TEL (in blocks) over M arrivals from an empty system.
 
-    policy: None (optimal), 'tlru' (Alg. 1 with Q_hat = Q) or 'lru'."""
+    policy: None (optimal), 'tlru' (Alg. 1 with Q_hat = Q), 'lru' or 'etlru' (Alg. 2 with the
+    belief lam_j = rho**age_j).  q_pmf: {q: p} prompt law (default: deterministic Q)."""
+    q_pmf = {Q: Fraction(1)} if q_pmf is None else {int(k): Fraction(v) for k, v in q_pmf.items()}
     rho = Fraction(rho)
     w_new = Fraction(w_new)
     A_set = tuple(A_set)
@@ -121,31 +170,35 @@ def belief_mdp_value(C, xi, Q, A_set, rho, w_new, n_max, M, policy=None, budget=
             else:
                 L, X = 0, 0
                 rest = convs
-            cost = max(L + Q - X - xi, 0)  # (L_theta + Q - X_theta - xi)^+, App. B
-            for A in A_set:
-                L_new = L + Q + A
-                others = [(Lr, Xr, ager + 1) for (Lr, Xr, ager) in rest]  # Phi: discount all others
-                # decision over theta (first, age 0) and the others
-                Ls = [L_new] + [o[0] for o in others]
-                Xs = [L_new] + [o[1] for o in others]   # X_theta <- L_theta
-                ages = [0] + [o[2] for o in others]
-                if policy is None:
-                    ub = Xs
-                    target = min(C, sum(ub))
-                    best = None
-                    for Y in product(*[range(u + 1) for u in ub]):
-                        if sum(Y) != target:
-                            continue
+            for Qd, pQ in q_pmf.items():
+                cost = max(L + Qd - X - xi, 0)  # (L_theta + Q - X_theta - xi)^+, App. B
+                for A in A_set:
+                    L_new = L + Qd + A
+                    others = [(Lr, Xr, ager + 1) for (Lr, Xr, ager) in rest]  # Phi: discount all others
+                    # decision over theta (first, age 0) and the others
+                    Ls = [L_new] + [o[0] for o in others]
+                    Xs = [L_new] + [o[1] for o in others]   # X_theta <- L_theta
+                    ages = [0] + [o[2] for o in others]
+                    if policy is None:
+                        ub = Xs
+                        target = min(C, sum(ub))
+                        best = None
+                        for Y in product(*[range(u + 1) for u in ub]):
+                            if sum(Y) != target:
+                                continue
+                            nxt = canon(tuple((Ls[i], Y[i], ages[i]) for i in range(len(Y))))
+                            v = V(k + 1, nxt)
+                            if best is None or v < best:
+                                best = v
+                        cont = best
+                    else:
+                        if policy == "etlru":  # belief lam = rho**age, older = larger age
+                            Y = etlru_step(Xs, Ls, [rho ** g for g in ages], C, xi, q_pmf, [-g for g in ages])
+                        else:
+                            Y = tlru_step(Xs, Ls, ages, 0, C, xi, Q, policy, budget)
                         nxt = canon(tuple((Ls[i], Y[i], ages[i]) for i in range(len(Y))))
-                        v = V(k + 1, nxt)
-                        if best is None or v < best:
-                            best = v
-                    cont = best
-                else:
-                    Y = tlru_step(Xs, Ls, ages, 0, C, xi, Q, policy, budget)
-                    nxt = canon(tuple((Ls[i], Y[i], ages[i]) for i in range(len(Y))))
-                    cont = V(k + 1, nxt)
-                ev += p * pA * (cost + cont)
+                        cont = V(k + 1, nxt)
+                    ev += p * pQ * pA * (cost + cont)
         return ev
 
     return V(0, tuple())

@@ -21,8 +21,9 @@
  *      (Sec. 3 explicit TEL form).
  *   5. Alg. 1 replay (Sec. 4): LRU (Phase 2 only) and T-LRU
  *      (Phase 1 TEL-safe trimming then Phase 2 LRU); Threshold-LRU,
- *      End-/Length-Aware T-LRU and the hindsight Tail-Optimized
- *      Belady (Thm 1).
+ *      End-/Length-Aware T-LRU, the hindsight Tail-Optimized
+ *      Belady (Thm 1) and Expected-Tail-Optimized LRU (Def. 1,
+ *      Alg. 2).
  *   6. Metrics: TTFT = alpha*b (Eq. 2), TEL (Eq. 1/3),
  *      nearest-rank percentiles (Reading #11), SLO count (strict >).
  */
@@ -572,6 +573,78 @@ int oracle_replay(const uint32_t* conv, const uint32_t* q, const uint32_t* a, ui
     free(s);
     free(dense);
     free(nxt);
+    return 0;
+}
+
+/* Expected-Tail-Optimized LRU (Def. 1; greedy Alg. 2), literal:
+   after serving theta (L_theta += Q + A, X_theta <- L_theta, lambda_theta <- lambda-bar),
+   evict n = overflow blocks one at a time from the conversation with the minimum ranking
+   criterion v_i = lambda_i * P(L_i + Q_i - xi >= X_i), re-scoring after every block.
+   Reading #27: homogeneous lambda-bar (it cancels) and belief lambda_i = exp(-mu (t - tau_i))
+   (P:255), so argmin v_i = argmin of ln v_i + mu t = mu * time_i + ln P(Q >= X_i - L_i + xi),
+   evaluated as (double)ticks_i * mu_tick + ln_surv[k] (one IEEE multiply, one add; ticks in
+   microseconds, mu_tick = mu per tick); ln_surv[k] = ln P(Q >= k) is the caller's table for
+   k = 0..K (k <= 0 -> ln 1 = 0, k > K -> -inf: the block is TEL-safe); ties -> older last
+   turn first (then the same conversation's tail block).  evicted_trim counts blocks evicted
+   with P = 0 (-inf), evicted_lru the others.  time_i = the tick of conversation i's last turn. */
+int oracle_replay_etlru(const uint32_t* conv, const uint32_t* q, const uint32_t* a, const uint64_t* ticks,
+                        uint64_t E, uint64_t C, uint64_t xi, double mu_tick, const double* ln_surv,
+                        uint64_t K, uint64_t* b_out, uint64_t* counters_out) {
+    uint32_t* dense = (uint32_t*)malloc((E ? E : 1) * 4);
+    if (!dense) return -1;
+    int64_t n = densify(conv, E, dense);
+    if (n < 0) { free(dense); return -1; }
+    uint64_t* X = (uint64_t*)calloc((size_t)(n ? n : 1), 8);
+    uint64_t* L = (uint64_t*)calloc((size_t)(n ? n : 1), 8);
+    uint64_t* tau = (uint64_t*)calloc((size_t)(n ? n : 1), 8);
+    int64_t* res = (int64_t*)malloc((size_t)(n ? n : 1) * 8);
+    unsigned char* in_res = (unsigned char*)calloc((size_t)(n ? n : 1), 1);
+    if (!X || !L || !tau || !res || !in_res) {
+        free(dense); free(X); free(L); free(tau); free(res); free(in_res);
+        return -1;
+    }
+    const double NEG_INF = -1.0 / 0.0;
+    int64_t nres = 0;
+    uint64_t used = 0, ev_free = 0, ev_other = 0, max_occ = 0;
+    for (uint64_t t = 0; t < E; ++t) {
+        int64_t c = dense[t];
+        uint64_t J = L[c] + q[t];
+        b_out[t] = J - X[c];                         /* job - x */
+        L[c] = J + a[t];                             /* Alg. 2 line 2 */
+        used = used - X[c] + L[c];
+        X[c] = L[c];                                 /* Alg. 2 line 3 */
+        tau[c] = t;                                  /* line 4: lambda_theta <- lambda-bar */
+        if (!in_res[c] && X[c] > 0) { res[nres++] = c; in_res[c] = 1; }
+        while (used > C) {                           /* lines 8-12: one block per iteration */
+            int64_t best = -1;
+            double best_v = 0.0, best_lg = 0.0;
+            for (int64_t k = 0; k < nres; ++k) {
+                int64_t i = res[k];
+                if (X[i] == 0) continue;
+                /* P(L_i + Q_i - xi >= X_i) = P(Q_i >= X_i - L_i + xi) */
+                int64_t kk = (int64_t)X[i] - (int64_t)L[i] + (int64_t)xi;
+                double lg = kk <= 0 ? 0.0 : ((uint64_t)kk > K ? NEG_INF : ln_surv[kk]);
+                double v = (double)ticks[tau[i]] * mu_tick + lg;
+                if (best < 0 || v < best_v || (v == best_v && tau[i] < tau[best])) {
+                    best = i; best_v = v; best_lg = lg;
+                }
+            }
+            X[best] -= 1;
+            used -= 1;
+            if (best_lg == NEG_INF) ev_free += 1; else ev_other += 1;
+        }
+        int64_t w = 0;
+        for (int64_t k = 0; k < nres; ++k) {
+            if (X[res[k]] > 0) res[w++] = res[k];
+            else in_res[res[k]] = 0;
+        }
+        nres = w;
+        if (used > max_occ) max_occ = used;
+    }
+    counters_out[0] = ev_free;
+    counters_out[1] = ev_other;
+    counters_out[2] = max_occ;
+    free(dense); free(X); free(L); free(tau); free(res); free(in_res);
     return 0;
 }
 
