@@ -180,6 +180,15 @@ def workload(name: str, rank: int):
             "predictability spectrum per GPU (P:389-395, Thm 1): 10 seeds x 10^6-conversation traces x 25 "
             "capacities x xi in {4, 8, 16, 24} x {End-Aware, Length-Aware T-LRU, Tail-Optimized Belady} = 3000 "
             "instances (replay engine, burn-in segments verified by the fix-up)")
+    if name == "etlru":
+        from paper_2510_15152_b200.inputs import CAPS_CONFIG5, Q_HAT, SLO_BLOCKS
+        seeds = [SEEDS_CONFIG5 * rank + k for k in range(SEEDS_CONFIG5)]
+        rows = [(t, 6, C, xi, Q_HAT, SLO_BLOCKS) for t in range(len(seeds)) for C in CAPS_CONFIG5
+                for xi in (4, 8, 16, 24)]
+        return seeds, rows, (
+            "ET-LRU per GPU (Def. 1 / Alg. 2, P:261-275): 10 seeds x 10^6-conversation traces x 25 capacities x "
+            "xi in {4, 8, 16, 24} = 1000 instances, belief mu = 1/90 s, the preset's prompt law (one warp per "
+            "instance)")
     if name == "config5x3":
         seeds = [SEEDS_CONFIG5 * rank + k for k in range(SEEDS_CONFIG5)]
         return seeds, config5_rows(len(seeds), threshold_lru=True), (
@@ -211,6 +220,9 @@ def run_ours(args, rank, world, local_rank):
     stream = torch.cuda.current_stream()
     seeds, rows, wl_desc = workload(args.config, rank)
     params = [preset("wildchat", s, args.conversations) for s in seeds]
+    if any(r[1] == T.POLICY_ET_LRU for r in rows):  # ET-LRU model: belief decay per µs tick, prompt law
+        from paper_2510_15152_b200.inputs import WILDCHAT, prompt_law_ln_surv
+        T.set_etlru_model(params[0]["death_rate"] * 1e-6, prompt_law_ln_surv(WILDCHAT))
 
     # ---- setup (untimed): traces at their exact size, one batch per trace, workspaces, streams
     traces = T.generate_traces(params, device=dev, exports=True)
@@ -330,7 +342,7 @@ def run_ours(args, rank, world, local_rank):
 
     # ---- replay engine (Alg. 1 request by request) on seed 0's instances; must give identical bytes
     rep = None
-    if not args.no_replay:
+    if not args.no_replay and stats["engine"] == 1:  # replay workloads already ran on the replay engine
         sub = trace_rows[0]
         if args.replay_instances:
             sub = sub[:args.replay_instances]
@@ -347,10 +359,13 @@ def run_ours(args, rank, world, local_rank):
     # ---- e2e: same batches through the public API from pinned host buffers (H2D on stream A,
     # upload + simulation on stream B, pipelined across traces), results read back to the host
     host_turns = []
+    need_ticks = any(r[1] == T.POLICY_ET_LRU for r in rows)  # ET-LRU beliefs read the event times
+    host_ticks = []
     for tr in traces:
         E = tr.num_events
         host_turns.append((tr.conv[:E].cpu().pin_memory(), tr.prompt[:E].view(torch.int16).cpu().pin_memory(),
                            tr.response[:E].view(torch.int16).cpu().pin_memory()))
+        host_ticks.append(tr.time_ticks[:E].cpu().pin_memory() if need_ticks else None)
     dev_turns = [(torch.empty_like(c, device=dev), torch.empty_like(q, device=dev), torch.empty_like(a, device=dev))
                  for c, q, a in host_turns]
     up_ws = []
@@ -360,6 +375,7 @@ def run_ours(args, rank, world, local_rank):
         up_ws.append(torch.empty(max(sz.value, 1), dtype=torch.uint8, device=dev))
     host_results = torch.empty(results_all.numel(), dtype=torch.uint8).pin_memory()
     h2d_bytes = sum(c.numel() * 4 + q.numel() * 2 + a.numel() * 2 for c, q, a in host_turns)
+    h2d_bytes += sum(h.numel() * 8 for h in host_ticks if h is not None)
     d2h_bytes = host_results.numel()
 
     def e2e_step():
@@ -380,6 +396,9 @@ def run_ours(args, rank, world, local_rank):
             sB.wait_event(ev)
             _abi.check(_abi.lib.tlru_trace_from_turns(T._ptr(dc), T._ptr(dq), T._ptr(da), tr.num_events,
                                                       ctypes.byref(ts), T._ptr(w), w.numel(), T._stream(sB)))
+            if host_ticks[t] is not None:  # the upload numbers events; ET-LRU needs the real times
+                with torch.cuda.stream(sB):
+                    tr.time_ticks[:tr.num_events].copy_(host_ticks[t], non_blocking=True)
             bt.run(sB)
             with torch.cuda.stream(sB):
                 results_all[slices[t]].copy_(bt.results)
@@ -498,7 +517,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-replay", action="store_true", help="skip timing the replay engine")
     ap.add_argument("--replay-instances", type=int, default=0, help="limit the replay-engine sample (0 = all of seed 0)")
-    ap.add_argument("--config", choices=("config5", "config5x3", "spectrum", "config4"), default="config5")
+    ap.add_argument("--config", choices=("config5", "config5x3", "spectrum", "etlru", "config4"), default="config5")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

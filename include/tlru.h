@@ -42,7 +42,7 @@ typedef enum {
   TLRU_EINVAL = 1,       /* bad argument or configuration (block_tokens == 0, rate <= 0, q == 0, ...) */
   TLRU_ERANGE = 2,       /* buffer / workspace too small, or a value exceeds its field width (J > 65535) */
   TLRU_ECUDA = 3,        /* CUDA runtime error; tlru_last_error() carries cudaGetErrorString */
-  TLRU_EUNSUPPORTED = 4, /* policy family not built (policy > TLRU_POLICY_TAIL_BELADY) */
+  TLRU_EUNSUPPORTED = 4, /* policy family not built (policy > TLRU_POLICY_ET_LRU) */
   TLRU_ESTATE = 5        /* internal per-chain state pool exhausted with no fallback left */
 } tlru_status;
 
@@ -173,6 +173,15 @@ tlru_status tlru_trace_from_turns(const uint32_t* conv, const uint16_t* q, const
  *   returns), furthest next arrival first; Phase 2 evicts the conversation whose
  *   next arrival is furthest in the future (evicted_lru counts these), partial.
  *   q_hat is ignored.  Replay engine only (like End-/Length-Aware).
+ * Expected-Tail-Optimized LRU (Def. 1; greedy Alg. 2, P:603-650;
+ *   Reading #27): on overflow, evict blocks one at a time from the minimum of
+ *   v_i = lambda_i P(L_i + Q_i - xi >= X_i), belief lambda_i = exp(-mu (t - time_i))
+ *   (P:255); equivalently the minimum static score
+ *   (double)time_ticks_i * mu_tick + ln_surv[X_i - L_i + xi] (IEEE multiply then add;
+ *   ln_surv[k <= 0] = 0, ln_surv[k > K] = -inf), ties -> older last turn.  The model
+ *   comes from tlru_set_etlru_model; the trace must carry time_ticks.  evicted_trim
+ *   counts blocks with P = 0 (TEL-safe), evicted_lru the rest.  q_hat is ignored.
+ *   One warp per instance (replay engine only).
  * ------------------------------------------------------------------------ */
 enum {
   TLRU_POLICY_LRU = 0,
@@ -180,7 +189,8 @@ enum {
   TLRU_POLICY_THRESHOLD = 2,
   TLRU_POLICY_END_AWARE = 3,
   TLRU_POLICY_LENGTH_AWARE = 4,
-  TLRU_POLICY_TAIL_BELADY = 5 /* > 5 -> TLRU_EUNSUPPORTED (ET-LRU, forced caching: not built) */
+  TLRU_POLICY_TAIL_BELADY = 5,
+  TLRU_POLICY_ET_LRU = 6 /* > 6 -> TLRU_EUNSUPPORTED (forced caching: not built) */
 };
 
 typedef struct {
@@ -229,6 +239,14 @@ tlru_status tlru_simulate_batch(const tlru_trace* traces /*host[nt]*/, uint32_t 
  * state_entries: per-chain on-chip state entries W (one of 32..1024); chains that
  *   outgrow it are re-run from global memory, so results do not depend on it. */
 tlru_status tlru_set_sim_options(uint32_t segment_events, uint32_t state_entries);
+
+/* ET-LRU model for the calling thread's later tlru_simulate_batch calls (Def. 1, P:261-275;
+ * Reading #27).  mu_per_tick: belief decay rate per time tick (the trace's time_ticks unit,
+ * microseconds for generated traces), finite and >= 0.  ln_surv: HOST array of K + 1 doubles,
+ * ln P(Q >= k) for k = 0..K (copied; non-increasing, each <= 0, -inf allowed, no NaN) -> else
+ * TLRU_EINVAL; K > 65535 -> TLRU_ERANGE.  A batch with ET-LRU instances and no model set ->
+ * TLRU_EINVAL. */
+tlru_status tlru_set_etlru_model(double mu_per_tick, const double* ln_surv /*host[K+1]*/, uint32_t K);
 
 /* Engine of tlru_simulate_batch on this thread (host).  Both are exact and give
  * identical bytes (tests/test_gpu_parity.py):

@@ -20,6 +20,7 @@ POLICY_THRESHOLD = 2
 POLICY_END_AWARE = 3
 POLICY_LENGTH_AWARE = 4
 POLICY_TAIL_BELADY = 5
+POLICY_ET_LRU = 6
 ENGINE_REPLAY = 0
 ENGINE_STACK = 1
 
@@ -87,7 +88,7 @@ class SimStats(ctypes.Structure):
 EXPORTS = (
     "tlru_last_error", "tlru_version", "tlru_launch_count", "tlru_trace_max_events", "tlru_gen_workspace_size", "tlru_count_events",
     "tlru_generate_traces", "tlru_upload_workspace_size", "tlru_trace_from_turns", "tlru_sim_workspace_size",
-    "tlru_simulate_batch", "tlru_set_sim_options", "tlru_set_sim_engine", "tlru_last_sim_stats", "tlru_tail_workspace_size", "tlru_tail_metrics",
+    "tlru_simulate_batch", "tlru_set_sim_options", "tlru_set_sim_engine", "tlru_set_etlru_model", "tlru_last_sim_stats", "tlru_tail_workspace_size", "tlru_tail_metrics",
 )
 
 
@@ -112,6 +113,7 @@ def _load():
         "tlru_simulate_batch": ([P(Trace), u32, P(Instance), u32, vp, P(u64), vp, vp, sz, vp], st),
         "tlru_set_sim_options": ([u32, u32], st),
         "tlru_set_sim_engine": ([u32], st),
+        "tlru_set_etlru_model": ([ctypes.c_double, P(ctypes.c_double), u32], st),
         "tlru_last_sim_stats": ([P(SimStats)], st),
         "tlru_tail_workspace_size": ([u32, u32, P(sz)], st),
         "tlru_tail_metrics": ([vp, vp, u32, vp, vp, vp, ctypes.c_double, u32, vp, vp, sz, vp], st),

@@ -123,6 +123,7 @@ struct TraceDev {
   const uint64_t* sim;
   const uint32_t* next;
   uint64_t E;
+  const uint64_t* ticks;  // event times (ET-LRU beliefs); may be NULL for the other policies
 };
 
 struct AccDev {  // per-instance accumulators of the counters not derivable from b
@@ -133,6 +134,11 @@ struct AccDev {  // per-instance accumulators of the counters not derivable from
 struct SpillDev {
   uint32_t group, seg, lane, pad;
 };
+}  // namespace tlru
+
+#include "etlru.cuh"
+
+namespace tlru {
 
 constexpr int BST_STRIDE = 34;  // u16 stride of a staged b row: 32 events + 2 pad (conflict-free)
 
@@ -444,6 +450,8 @@ constexpr int kSpillSlots = 128;
 static thread_local uint32_t g_opt_seg = 0;  // tlru_set_sim_options
 static thread_local int g_opt_w = -1;
 static thread_local uint32_t g_opt_engine = TLRU_ENGINE_STACK;  // tlru_set_sim_engine
+static thread_local double g_et_mu = -1.0;                      // tlru_set_etlru_model
+static thread_local std::vector<double> g_et_table;
 
 // Entries needed per lane for capacity C: live conversations are bounded by
 // min(C + 1, conversations); the estimate below is the measured resident count of
@@ -470,6 +478,9 @@ struct Plan {
   bool any_aware = false;
   std::vector<uint32_t> alane, atrace;       // aware lane -> global lane index, trace
   uint32_t aseg = 8192, aburn = 4096, anseg_max = 1, awsnap = 32;
+  std::vector<EtItem> et_items;              // ET-LRU instances (etlru.cuh)
+  std::vector<EtSeg> et_segs[kNumW];         // their (instance, segment) warps per state class
+  uint32_t n_et = 0, et_seg_len = 8192, et_burn = 4096, et_nseg_max = 1, et_wsnap = 32;
   std::vector<TraceDev> traces;
   std::vector<SegDev> segs;
   uint32_t seg_len = 0;
@@ -490,7 +501,7 @@ static tlru_status make_plan(const tlru_trace* traces, uint32_t nt, const tlru_i
     const tlru_trace& tr = traces[t];
     if (tr.num_events > 0 && (!tr.sim || !tr.next)) TLRU_FAIL(TLRU_EINVAL, "trace %u: sim/next is NULL", t);
     if (tr.num_events >= 0xFFFFFFFFull) TLRU_FAIL(TLRU_ERANGE, "trace %u: too many events", t);
-    P->traces[t] = TraceDev{tr.sim, tr.next, tr.num_events};
+    P->traces[t] = TraceDev{tr.sim, tr.next, tr.num_events, tr.time_ticks};
     maxhist = std::max(maxhist, tr.max_history);
     Emax = std::max<uint64_t>(Emax, tr.num_events);
   }
@@ -499,14 +510,21 @@ static tlru_status make_plan(const tlru_trace* traces, uint32_t nt, const tlru_i
   // instance order: by trace, then W class, then C (lanes of a warp see similar state sizes)
   std::vector<uint32_t> order(ni);
   std::vector<int> wc(ni);
+  uint32_t ni_lanes = ni;
+  std::vector<int> et_cls;
   uint64_t packed = 0;
   P->segs.resize(ni);
   for (uint32_t i = 0; i < ni; ++i) {
     const tlru_instance& in = inst[i];
     if (in.trace >= nt) TLRU_FAIL(TLRU_EINVAL, "instance %u: trace index %u out of range", i, in.trace);
-    if (in.policy > TLRU_POLICY_TAIL_BELADY)
-      TLRU_FAIL(TLRU_EUNSUPPORTED, "instance %u: policy %u is not built (0..5: LRU, T-LRU, Threshold-LRU, "
-                "End-Aware, Length-Aware, Tail-Optimized Belady)", i, in.policy);
+    if (in.policy > TLRU_POLICY_ET_LRU)
+      TLRU_FAIL(TLRU_EUNSUPPORTED, "instance %u: policy %u is not built (0..6: LRU, T-LRU, Threshold-LRU, "
+                "End-Aware, Length-Aware, Tail-Optimized Belady, ET-LRU)", i, in.policy);
+    if (in.policy == TLRU_POLICY_ET_LRU) {
+      if (g_et_mu < 0.0) TLRU_FAIL(TLRU_EINVAL, "instance %u: ET-LRU needs tlru_set_etlru_model first", i);
+      if (traces[in.trace].num_events > 0 && !traces[in.trace].time_ticks)
+        TLRU_FAIL(TLRU_EINVAL, "instance %u: ET-LRU needs the trace's time_ticks (beliefs, P:255)", i);
+    }
     if (in.policy >= TLRU_POLICY_END_AWARE) P->any_aware = true;
     if (in.policy == TLRU_POLICY_THRESHOLD && in.threshold > 65535)
       TLRU_FAIL(TLRU_ERANGE, "instance %u: threshold %u > 65535 (histories are u16)", i, in.threshold);
@@ -529,6 +547,39 @@ static tlru_status make_plan(const tlru_trace* traces, uint32_t nt, const tlru_i
     packed += E;
     P->segs[i] = SegDev{off, off + E, in.xi, in.slo, 0.0};
   }
+  // ET-LRU instances run as warp-cooperative chains of their own (etlru.cuh), not in lane groups
+  {
+    std::vector<uint32_t> keep;
+    for (uint32_t i : order) {
+      const tlru_instance& in = inst[i];
+      if (in.policy != TLRU_POLICY_ET_LRU) {
+        keep.push_back(i);
+        continue;
+      }
+      P->any_aware = true;
+      const uint32_t C = std::min<uint32_t>(in.capacity, 0x7FFF0000u);
+      const int k = g_opt_w >= 0 ? g_opt_w : w_class(C, traces[in.trace].num_conversations);
+      P->et_items.push_back(EtItem{i, in.trace, C, in.xi, P->segs[i].begin});
+      et_cls.push_back(k);
+      ++P->n_et;
+    }
+    order.swap(keep);
+    ni_lanes = static_cast<uint32_t>(order.size());
+    if (P->n_et) {  // segments: enough warps to fill the GPU, each >= 2x the burn-in
+      const uint64_t pe = (148ull * 24ull + P->n_et - 1) / P->n_et;
+      uint64_t sl = Emax ? (Emax + pe - 1) / pe : 8192;
+      sl = std::min<uint64_t>(std::max<uint64_t>(sl, 2ull * P->et_burn), 1ull << 24);
+      if (g_opt_seg) sl = std::max<uint32_t>(g_opt_seg, 64);  // tests: short segments exercise the fix-up
+      P->et_seg_len = static_cast<uint32_t>((sl + 31) & ~31ull);
+      for (uint32_t k = 0; k < P->n_et; ++k) {
+        const uint64_t E = traces[P->et_items[k].trace].num_events;
+        const uint64_t ns = std::max<uint64_t>((E + P->et_seg_len - 1) / P->et_seg_len, 1);
+        for (uint64_t sgi = 0; sgi < ns; ++sgi) P->et_segs[et_cls[k]].push_back(EtSeg{k, static_cast<uint32_t>(sgi)});
+        P->et_nseg_max = std::max<uint32_t>(P->et_nseg_max, static_cast<uint32_t>(ns));
+        P->et_wsnap = std::max<uint32_t>(P->et_wsnap, static_cast<uint32_t>(kWClasses[et_cls[k]]));
+      }
+    }
+  }
   std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) {
     if (inst[a].trace != inst[b].trace) return inst[a].trace < inst[b].trace;
     if (aware_kind(inst[a]) != aware_kind(inst[b])) return aware_kind(inst[a]) < aware_kind(inst[b]);
@@ -536,13 +587,13 @@ static tlru_status make_plan(const tlru_trace* traces, uint32_t nt, const tlru_i
     return inst[a].capacity < inst[b].capacity;
   });
   // lane groups
-  for (uint32_t k = 0; k < ni;) {
+  for (uint32_t k = 0; k < ni_lanes;) {
     const uint32_t t = inst[order[k]].trace;
     const int w = wc[order[k]];
     const uint32_t kind = aware_kind(inst[order[k]]);
     const bool aw = kind != 0;
     GroupDev g{t, static_cast<uint32_t>(P->lanes.size()), 0, static_cast<uint32_t>(w), kind};
-    while (k < ni && g.nlanes < 32 && inst[order[k]].trace == t && wc[order[k]] == w &&
+    while (k < ni_lanes && g.nlanes < 32 && inst[order[k]].trace == t && wc[order[k]] == w &&
            aware_kind(inst[order[k]]) == kind) {
       const tlru_instance& in = inst[order[k]];
       LaneDev l;
@@ -634,6 +685,11 @@ struct SimWs {
   uint32_t* atau;   // fix-up state pool [aware lane][awsnap]
   uint16_t* aX;
   uint16_t* aS;
+  EtItem* et_items;         // ET-LRU instances
+  EtSeg* et_segs;           // their segment warps, by state class
+  double* et_table;         // ln P(Q >= k), k = 0..K
+  EtSegs et_sg;             // snapshots and per-segment counters
+  unsigned char* et_gpool;  // fix-up state pools [n_et][W_big slots x 24 B]
 };
 
 static void carve_sim(Carver& cv, const Plan& P, uint32_t ni, SimWs* w) {
@@ -646,7 +702,7 @@ static void carve_sim(Carver& cv, const Plan& P, uint32_t ni, SimWs* w) {
   w->segs = cv.take<SegDev>(ni + 1);
   w->acc = cv.take<AccDev>(ni + 1);
   w->spill = cv.take<SpillDev>(nitems * 32 + 1);
-  w->counters = cv.take<unsigned int>(3);  // nspill, nfail, aware segments re-run
+  w->counters = cv.take<unsigned int>(4);  // nspill, nfail, aware segments re-run, ET-LRU re-runs
   w->hist = cv.take<uint32_t>(uint64_t(ni + 1) * P.bins);
   w->clamped = cv.take<unsigned long long>(ni + 1);
   w->tau_pool = cv.take<uint32_t>(uint64_t(kSpillSlots) * P.W_big);
@@ -667,6 +723,22 @@ static void carve_sim(Carver& cv, const Plan& P, uint32_t ni, SimWs* w) {
   w->atau = cv.take<uint32_t>(nal ? nal * P.W_big : 1);  // fix-up state: as large as the spill state
   w->aX = cv.take<uint16_t>(nal ? nal * P.W_big : 1);
   w->aS = cv.take<uint16_t>(nal ? nal * P.W_big : 1);
+  const uint64_t ne = P.n_et;
+  uint64_t nes = 0;
+  for (int k = 0; k < kNumW; ++k) nes += P.et_segs[k].size();
+  w->et_items = cv.take<EtItem>(ne + 1);
+  w->et_segs = cv.take<EtSeg>(nes + 1);
+  w->et_table = cv.take<double>(g_et_table.size() + 1);
+  const uint64_t nse = std::max<uint64_t>(ne, 1) * P.et_nseg_max;
+  w->et_sg.seg_len = P.et_seg_len;
+  w->et_sg.burn = P.et_burn;
+  w->et_sg.nseg_max = P.et_nseg_max;
+  w->et_sg.wsnap = P.et_wsnap;
+  w->et_sg.snap = cv.take<uint32_t>(ne ? nse * 2 * et_snap_words(P.et_wsnap) : 1);
+  w->et_sg.segc = cv.take<unsigned long long>(ne ? 2 * nse : 1);
+  w->et_sg.segm = cv.take<uint32_t>(ne ? nse : 1);
+  w->et_sg.ovf = cv.take<uint32_t>(ne ? nse : 1);
+  w->et_gpool = cv.take<unsigned char>(ne ? ne * uint64_t(P.W_big) * 24 : 1);
 }
 
 static thread_local tlru_sim_stats g_stats;
@@ -692,6 +764,20 @@ static tlru_status launch_w(const std::vector<ItemDev>& items, const ItemDev* d_
   sim_kernel<W, AWARE><<<static_cast<unsigned>(items.size()), 32, smem, st>>>(d_items, w.groups, w.lanes, w.traces,
                                                                               seg_len, bout, w.acc, w.spill,
                                                                               w.counters, w.aw);
+  TLRU_CHECK_LAUNCH();
+  ++g_stats.kernels;
+  return TLRU_OK;
+}
+
+template <int W>
+static tlru_status launch_et(const std::vector<EtSeg>& segs, const EtSeg* d_segs, const SimWs& w, const EtModel& m,
+                             uint16_t* bout, cudaStream_t st) {
+  if (segs.empty()) return TLRU_OK;
+  const size_t smem = kEtTab * sizeof(double) + size_t(W) * 24;  // table, key, base, tau, X, L
+  TLRU_CUDA(cudaFuncSetAttribute(etlru_seg_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem)));
+  etlru_seg_kernel<W><<<static_cast<unsigned>(segs.size()), 32, smem, st>>>(d_segs, w.et_items, w.traces, m, w.et_sg,
+                                                                            bout);
   TLRU_CHECK_LAUNCH();
   ++g_stats.kernels;
   return TLRU_OK;
@@ -785,7 +871,19 @@ extern "C" tlru_status tlru_simulate_batch(const tlru_trace* traces, uint32_t nt
   TLRU_CUDA(cudaMemcpyAsync(w.traces, P.traces.data(), P.traces.size() * sizeof(TraceDev), cudaMemcpyHostToDevice, st));
   TLRU_CUDA(cudaMemcpyAsync(w.segs, P.segs.data(), ni * sizeof(SegDev), cudaMemcpyHostToDevice, st));
   TLRU_CUDA(cudaMemsetAsync(w.acc, 0, ni * sizeof(AccDev), st));
-  TLRU_CUDA(cudaMemsetAsync(w.counters, 0, 3 * sizeof(unsigned int), st));
+  TLRU_CUDA(cudaMemsetAsync(w.counters, 0, 4 * sizeof(unsigned int), st));
+  std::vector<EtSeg> et_all;
+  size_t et_off[kNumW];
+  for (int k = 0; k < kNumW; ++k) {
+    et_off[k] = et_all.size();
+    et_all.insert(et_all.end(), P.et_segs[k].begin(), P.et_segs[k].end());
+  }
+  if (P.n_et) {
+    TLRU_CUDA(cudaMemcpyAsync(w.et_items, P.et_items.data(), P.n_et * sizeof(EtItem), cudaMemcpyHostToDevice, st));
+    TLRU_CUDA(cudaMemcpyAsync(w.et_segs, et_all.data(), et_all.size() * sizeof(EtSeg), cudaMemcpyHostToDevice, st));
+    TLRU_CUDA(cudaMemcpyAsync(w.et_table, g_et_table.data(), g_et_table.size() * sizeof(double),
+                              cudaMemcpyHostToDevice, st));
+  }
   if (!P.alane.empty()) {
     TLRU_CUDA(cudaMemcpyAsync(w.alane, P.alane.data(), P.alane.size() * 4, cudaMemcpyHostToDevice, st));
     TLRU_CUDA(cudaMemcpyAsync(w.atrace, P.atrace.data(), P.atrace.size() * 4, cudaMemcpyHostToDevice, st));
@@ -813,6 +911,26 @@ extern "C" tlru_status tlru_simulate_batch(const tlru_trace* traces, uint32_t nt
               TLRU_TRY((launch_w<1024, true>(ia, da, w, P.seg_len, uncached, st))); break;
     }
   }
+  if (P.n_et) {  // ET-LRU: one warp per (instance, segment), shared-memory state per class
+    const EtModel m{w.et_table, static_cast<uint32_t>(g_et_table.size() - 1), g_et_mu};
+    for (int k = kNumW - 1; k >= 0; --k) {
+      const std::vector<EtSeg>& v = P.et_segs[k];
+      const EtSeg* d = w.et_segs + et_off[k];
+      switch (k) {
+        case 0: TLRU_TRY((launch_et<32>(v, d, w, m, uncached, st))); break;
+        case 1: TLRU_TRY((launch_et<64>(v, d, w, m, uncached, st))); break;
+        case 2: TLRU_TRY((launch_et<128>(v, d, w, m, uncached, st))); break;
+        case 3: TLRU_TRY((launch_et<256>(v, d, w, m, uncached, st))); break;
+        case 4: TLRU_TRY((launch_et<512>(v, d, w, m, uncached, st))); break;
+        case 5: TLRU_TRY((launch_et<1024>(v, d, w, m, uncached, st))); break;
+      }
+    }
+    // fix-up: re-run every segment whose start state was not exact (or that outgrew its slots)
+    etlru_fix_kernel<<<P.n_et, 32, 0, st>>>(w.et_items, P.n_et, w.traces, m, w.et_sg, uncached, w.acc, w.et_gpool,
+                                            P.W_big, w.counters + 3, w.counters + 1);
+    TLRU_CHECK_LAUNCH();
+    ++g_stats.kernels;
+  }
   // spill path: always launched; exits at once when the queue is empty (no host sync)
   sim_spill_kernel<<<kSpillSlots / 32, 32, 0, st>>>(w.groups, w.lanes, w.traces, P.seg_len, uncached, w.acc, w.spill,
                                                     w.counters, w.tau_pool, w.X_pool, w.S_pool, P.W_big,
@@ -836,7 +954,8 @@ extern "C" tlru_status tlru_simulate_batch(const tlru_trace* traces, uint32_t nt
   g_ev_recorded = true;
   g_stats.kernels += 3;
   g_stats.chains = 0;
-  for (int k = 0; k < kNumW; ++k) g_stats.chains += (P.items[k].size() + P.items_aware[k].size()) * 32;
+  for (int k = 0; k < kNumW; ++k)
+    g_stats.chains += (P.items[k].size() + P.items_aware[k].size()) * 32 + P.et_segs[k].size();
   g_stats.segment_events = P.seg_len;
   for (int k = kNumW - 1; k >= 0; --k)
     if (!P.items[k].empty() || !P.items_aware[k].empty()) {
@@ -861,6 +980,22 @@ extern "C" tlru_status tlru_set_sim_options(uint32_t segment_events, uint32_t st
   return TLRU_OK;
 }
 
+extern "C" tlru_status tlru_set_etlru_model(double mu_per_tick, const double* ln_surv, uint32_t K) {
+  clear_error();
+  if (!(mu_per_tick >= 0.0) || mu_per_tick > 1e300) TLRU_FAIL(TLRU_EINVAL, "mu_per_tick must be finite and >= 0");
+  if (!ln_surv) TLRU_FAIL(TLRU_EINVAL, "ln_surv is NULL");
+  if (K > 65535) TLRU_FAIL(TLRU_ERANGE, "K must be <= 65535");
+  for (uint32_t k = 0; k <= K; ++k) {
+    const double v = ln_surv[k];
+    if (v != v || v > 0.0) TLRU_FAIL(TLRU_EINVAL, "ln_surv[%u] must be <= 0 (a log-probability), not NaN", k);
+    if (k > 0 && v > ln_surv[k - 1]) TLRU_FAIL(TLRU_EINVAL, "ln_surv must be non-increasing (at k = %u)", k);
+  }
+  g_et_table.assign(ln_surv, ln_surv + K + 1);
+  for (double& v : g_et_table) v += 0.0;  // -0.0 -> +0.0 (etlru.cuh orders scores as integers)
+  g_et_mu = mu_per_tick + 0.0;
+  return TLRU_OK;
+}
+
 extern "C" tlru_status tlru_set_sim_engine(uint32_t engine) {
   clear_error();
   if (engine != TLRU_ENGINE_REPLAY && engine != TLRU_ENGINE_STACK)
@@ -874,10 +1009,10 @@ extern "C" tlru_status tlru_last_sim_stats(tlru_sim_stats* out) {
   if (!out) TLRU_FAIL(TLRU_EINVAL, "out is NULL");
   *out = g_stats;
   if (g_counters) {
-    unsigned int c[3] = {0, 0, 0};
+    unsigned int c[4] = {0, 0, 0, 0};
     TLRU_CUDA(cudaDeviceSynchronize());
     TLRU_CUDA(cudaMemcpy(c, g_counters, sizeof(c), cudaMemcpyDeviceToHost));
-    out->spilled_chains = c[0] + c[2];  // incl. End-/Length-Aware segments re-run by the fix-up
+    out->spilled_chains = c[0] + c[2] + c[3];  // incl. aware segments re-run by the fix-up, ET-LRU re-runs
     out->failed_chains = c[1];
   }
   if (g_ev_recorded) {

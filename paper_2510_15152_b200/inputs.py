@@ -56,6 +56,35 @@ XI_CONFIG5 = tuple(range(2, 41, 2))
 SEEDS_CONFIG5 = 10
 
 
+def prompt_law_ln_surv(preset_params: dict, K: int = 160) -> np.ndarray:
+    """ET-LRU's model of the next prompt length (Def. 1; Reading #27): ln P(q >= k)
+    for k = 0..K under the preset's own prompt law, q = max(1, ceil(tok / block_tokens)) with
+    tok = lognormal(mean, sigma_ln) rounded and clipped.  A model parameter handed to both the
+    oracle and the CUDA path (like the preset rates); -inf where the probability is 0.
+    Computed with the lognormal CDF (math.erf) at the rounding boundaries."""
+    import math
+    m, sg = float(preset_params["prompt_mean_tokens"]), float(preset_params["prompt_sigma_ln"])
+    lo, hi = int(preset_params["prompt_min_tokens"]), int(preset_params["prompt_max_tokens"])
+    B = int(preset_params["block_tokens"])
+    mu_ln = math.log(m) - 0.5 * sg * sg
+
+    def cdf_tok_below(x):  # P(rounded, clipped tok < x) for integer x
+        if x <= lo:
+            return 0.0
+        if x > hi:
+            return 1.0
+        return 0.5 * (1.0 + math.erf((math.log(x - 0.5) - mu_ln) / (sg * math.sqrt(2.0))))
+
+    out = np.empty(K + 1, np.float64)
+    for k in range(K + 1):
+        if k <= 1:
+            out[k] = 0.0  # q >= 1 always
+            continue
+        p = 1.0 - cdf_tok_below((k - 1) * B + 1)  # q >= k  <=>  tok > (k - 1) B
+        out[k] = math.log(p) if p > 0.0 else -math.inf
+    return np.minimum.accumulate(out)
+
+
 # Threshold-LRU admission threshold: 1024 tokens (P:307, the OpenAI rule the paper follows) = 8 blocks
 THRESHOLD_BLOCKS = 8
 

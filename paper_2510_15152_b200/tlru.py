@@ -13,12 +13,12 @@ import numpy as np
 import torch
 
 from . import _abi
-from ._abi import (ENGINE_REPLAY, ENGINE_STACK, POLICY_END_AWARE, POLICY_LENGTH_AWARE, POLICY_LRU, POLICY_TAIL_BELADY, POLICY_THRESHOLD, POLICY_TLRU, RESULT_DTYPE, TAIL_DTYPE, TLRU_NONE, GenParams, Instance, SimStats,
+from ._abi import (ENGINE_REPLAY, ENGINE_STACK, POLICY_END_AWARE, POLICY_ET_LRU, POLICY_LENGTH_AWARE, POLICY_LRU, POLICY_TAIL_BELADY, POLICY_THRESHOLD, POLICY_TLRU, RESULT_DTYPE, TAIL_DTYPE, TLRU_NONE, GenParams, Instance, SimStats,
                    Trace, TlruError, check, lib)
 
-__all__ = ["DeviceTrace", "generate_traces", "trace_from_turns", "simulate_batch", "tail_metrics", "last_sim_stats", "set_sim_options", "set_sim_engine",
+__all__ = ["DeviceTrace", "generate_traces", "trace_from_turns", "simulate_batch", "tail_metrics", "last_sim_stats", "set_sim_options", "set_sim_engine", "set_etlru_model",
            "ENGINE_REPLAY", "ENGINE_STACK",
-           "POLICY_LRU", "POLICY_TLRU", "POLICY_THRESHOLD", "POLICY_END_AWARE", "POLICY_LENGTH_AWARE", "POLICY_TAIL_BELADY", "TLRU_NONE", "TlruError", "RESULT_DTYPE", "TAIL_DTYPE", "version"]
+           "POLICY_LRU", "POLICY_TLRU", "POLICY_THRESHOLD", "POLICY_END_AWARE", "POLICY_LENGTH_AWARE", "POLICY_TAIL_BELADY", "POLICY_ET_LRU", "TLRU_NONE", "TlruError", "RESULT_DTYPE", "TAIL_DTYPE", "version"]
 
 
 def version() -> str:
@@ -208,6 +208,15 @@ def simulate_batch(traces: list[DeviceTrace], rows, stream=None) -> SimBatch:
 def set_sim_options(segment_events: int = 0, state_entries: int = 0) -> None:
     """tlru_set_sim_options (0 = automatic); results never depend on these."""
     check(lib.tlru_set_sim_options(segment_events, state_entries))
+
+
+def set_etlru_model(mu_tick: float, ln_surv) -> None:
+    """tlru_set_etlru_model: ET-LRU's belief decay mu per time tick (ticks are the trace's
+    microsecond times) and ln P(Q >= k) for k = 0..K (Def. 1; Reading #27)."""
+    import numpy as np
+    tab = np.ascontiguousarray(ln_surv, dtype=np.float64)
+    check(lib.tlru_set_etlru_model(float(mu_tick), tab.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                                   tab.shape[0] - 1))
 
 
 def set_sim_engine(engine: int) -> None:
