@@ -34,17 +34,20 @@ from functools import lru_cache
 from itertools import product
 
 
-def tlru_step(X, L, ages, theta, C, xi, q_hat, policy, budget="strict"):
+def tlru_step(X, L, ages, theta, C, xi, q_hat, policy, budget="strict", forced=False):
     """One Alg. 1 decision after serving `theta` (whose X/L are already updated
     per P:206: X_theta = L_theta).  X, L, ages: lists (ages: larger = older).
     policy 'lru' skips Phase 1.  budget 'strict' trims to (L + Q_hat - xi)^+
     (Reading #2); 'weak' is the literal `X_i >= L_i + Q_hat - xi` test that
-    trims one block below the budget.  Returns the new X (list)."""
+    trims one block below the budget.  forced (App. C): theta (an index) keeps its
+    whole history unless it alone exceeds C.  Returns the new X (list)."""
     X = list(X)
     over = sum(X) - C
     order = sorted(range(len(X)), key=lambda i: -ages[i])  # ascending tau = oldest first
     if over > 0 and policy == "tlru":
         for i in order:  # Phase 1 (P:208-213), bulk, oldest first, theta last (Readings #1, #3, #5)
+            if forced and i == theta:
+                continue
             budget_i = max(L[i] + q_hat - xi, 0)
             if budget == "weak":
                 budget_i = max(budget_i - 1, 0) if X[i] >= L[i] + q_hat - xi else X[i]
@@ -55,11 +58,15 @@ def tlru_step(X, L, ages, theta, C, xi, q_hat, policy, budget="strict"):
                 break
     if over > 0:
         for i in order:  # Phase 2
+            if forced and i == theta:
+                continue
             k = min(X[i], over)
             X[i] -= k
             over -= k
             if over == 0:
                 break
+    if over > 0 and forced:  # theta alone exceeds C
+        X[theta] -= over
     return X
 
 
@@ -106,8 +113,9 @@ def etlru_objective_min(X, L, lam, C, xi, q_pmf):
 
 
 # ----------------------------------------------------------------------------- Thm 1 / Eq. 5
-def hindsight_opt(conv, q, a, C: int, xi: int) -> int:
-    """min sum_t (J_t - x_{theta,t} - xi)^+ over cache schedules obeying (2)-(4)."""
+def hindsight_opt(conv, q, a, C: int, xi: int, forced: bool = False) -> int:
+    """min sum_t (J_t - x_{theta,t} - xi)^+ over cache schedules obeying (2)-(4); forced: (3) with
+    equality (App. C), capped by the capacity (Reading #28)."""
     ids = sorted(set(int(c) for c in conv))
     idx = {c: i for i, c in enumerate(ids)}
     n = len(ids)
@@ -128,6 +136,8 @@ def hindsight_opt(conv, q, a, C: int, xi: int) -> int:
         for Y in product(*[range(u + 1) for u in ub]):
             if sum(Y) != target:
                 continue
+            if forced and Y[th] != min(L2[th], C):
+                continue
             v = V(t + 1, tuple(Y), tuple(L2))
             if best is None or v < best:
                 best = v
@@ -137,7 +147,8 @@ def hindsight_opt(conv, q, a, C: int, xi: int) -> int:
 
 
 # ----------------------------------------------------------------------------- Thm 2 belief MDP
-def belief_mdp_value(C, xi, Q, A_set, rho, w_new, n_max, M, policy=None, budget="strict", q_pmf=None):
+def belief_mdp_value(C, xi, Q, A_set, rho, w_new, n_max, M, policy=None, budget="strict", q_pmf=None,
+                     forced=False):
     """Expected TEL (in blocks) over M arrivals from an empty system.
 
     policy: None (optimal), 'tlru' (Alg. 1 with Q_hat = Q), 'lru' or 'etlru' (Alg. 2 with the
@@ -186,6 +197,8 @@ def belief_mdp_value(C, xi, Q, A_set, rho, w_new, n_max, M, policy=None, budget=
                         for Y in product(*[range(u + 1) for u in ub]):
                             if sum(Y) != target:
                                 continue
+                            if forced and Y[0] != min(L_new, C):  # App. C: theta kept whole
+                                continue
                             nxt = canon(tuple((Ls[i], Y[i], ages[i]) for i in range(len(Y))))
                             v = V(k + 1, nxt)
                             if best is None or v < best:
@@ -195,7 +208,7 @@ def belief_mdp_value(C, xi, Q, A_set, rho, w_new, n_max, M, policy=None, budget=
                         if policy == "etlru":  # belief lam = rho**age, older = larger age
                             Y = etlru_step(Xs, Ls, [rho ** g for g in ages], C, xi, q_pmf, [-g for g in ages])
                         else:
-                            Y = tlru_step(Xs, Ls, ages, 0, C, xi, Q, policy, budget)
+                            Y = tlru_step(Xs, Ls, ages, 0, C, xi, Q, policy, budget, forced)
                         nxt = canon(tuple((Ls[i], Y[i], ages[i]) for i in range(len(Y))))
                         cont = V(k + 1, nxt)
                     ev += p * pQ * pA * (cost + cont)

@@ -467,7 +467,8 @@ static int replay_tail_belady(const uint32_t* dense, int64_t n, const uint32_t* 
    uncached blocks of each request (u64).  counters_out[3] = {evicted_trim,
    evicted_lru, max_occupancy}; released blocks are not evictions.  5 = Tail-Optimized
    Belady (Thm 1, replay_tail_belady above; evicted_lru counts its Phase-2
-   furthest-in-future evictions).  Returns 0, or -1 on allocation failure. */
+   furthest-in-future evictions).  7 = T-LRU under forced caching (App. C, Reading #28).
+   Returns 0, or -1 on allocation failure. */
 int oracle_replay(const uint32_t* conv, const uint32_t* q, const uint32_t* a, uint64_t E,
                   int policy, uint64_t C, uint64_t xi, uint64_t q_hat, uint64_t threshold,
                   uint64_t* b_out, uint64_t* counters_out) {
@@ -499,7 +500,11 @@ int oracle_replay(const uint32_t* conv, const uint32_t* q, const uint32_t* a, ui
        of the history beyond the TEL-safe budget L + Q_hat - xi (P:56, P:62
        footnote; Readings #2, #4, #6).  LRU has no free blocks. */
     uint64_t D = 0;
-    if ((policy == 1 || policy == 3) && xi > q_hat) D = xi - q_hat;
+    if ((policy == 1 || policy == 3 || policy == 7) && xi > q_hat) D = xi - q_hat;
+    /* policy 7: T-LRU under forced caching (App. C; Reading #28): the post-decision
+       state must hold theta's whole history (constraint (3) with equality), so Phases 1 and 2
+       skip theta; only if theta alone exceeds C does it lose tail blocks (capacity first). */
+    const int forced = policy == 7;
     uint64_t used = 0, ev_trim = 0, ev_lru = 0, max_occ = 0;
     for (uint64_t t = 0; t < E; ++t) {
         int64_t c = dense[t];
@@ -548,6 +553,7 @@ int oracle_replay(const uint32_t* conv, const uint32_t* q, const uint32_t* a, ui
             int64_t i = fre.head;
             while (over > 0 && i >= 0) {
                 int64_t nx = s[i].fre_next;
+                if (forced && i == c) { i = nx; continue; }   /* theta is kept whole */
                 uint64_t k = s[i].surplus < over ? s[i].surplus : over;
                 s[i].X -= k; s[i].surplus -= k; used -= k; over -= k; ev_trim += k;
                 if (s[i].surplus == 0) list_remove(s, &fre, FRE, i);
@@ -559,10 +565,20 @@ int oracle_replay(const uint32_t* conv, const uint32_t* q, const uint32_t* a, ui
             i = res.head;
             while (over > 0 && i >= 0) {
                 int64_t nx = s[i].res_next;
+                if (forced && i == c) { i = nx; continue; }
                 uint64_t k = s[i].X < over ? s[i].X : over;
                 s[i].X -= k; used -= k; over -= k; ev_lru += k;
                 if (s[i].X == 0) list_remove(s, &res, RES, i);
                 i = nx;
+            }
+            if (forced && over > 0) {
+                /* theta alone exceeds C: its tail blocks go (free ones first, they are the tail) */
+                uint64_t k = over;
+                s[c].X -= k; used -= k; over = 0; ev_lru += k;
+                uint64_t ks = s[c].surplus < k ? s[c].surplus : k;
+                s[c].surplus -= ks;
+                if (s[c].surplus == 0 && s[c].in_fre) list_remove(s, &fre, FRE, c);
+                if (s[c].X == 0) list_remove(s, &res, RES, c);
             }
         }
         if (used > max_occ) max_occ = used;
