@@ -189,6 +189,14 @@ def workload(name: str, rank: int):
             "ET-LRU per GPU (Def. 1 / Alg. 2, P:261-275): 10 seeds x 10^6-conversation traces x 25 capacities x "
             "xi in {4, 8, 16, 24} = 1000 instances, belief mu = 1/90 s, the preset's prompt law (one warp per "
             "instance)")
+    if name == "forced":
+        from paper_2510_15152_b200.inputs import CAPS_CONFIG5, Q_HAT, SLO_BLOCKS
+        seeds = [SEEDS_CONFIG5 * rank + k for k in range(SEEDS_CONFIG5)]
+        rows = [(t, 7, C, xi, Q_HAT, SLO_BLOCKS) for t in range(len(seeds)) for C in CAPS_CONFIG5
+                for xi in (4, 8, 16, 24)]
+        return seeds, rows, (
+            "T-LRU under forced caching per GPU (App. C): 10 seeds x 10^6-conversation traces x 25 capacities x "
+            "xi in {4, 8, 16, 24} = 1000 instances (replay engine, burn-in segments verified by the fix-up)")
     if name == "config5x3":
         seeds = [SEEDS_CONFIG5 * rank + k for k in range(SEEDS_CONFIG5)]
         return seeds, config5_rows(len(seeds), threshold_lru=True), (
@@ -517,7 +525,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-replay", action="store_true", help="skip timing the replay engine")
     ap.add_argument("--replay-instances", type=int, default=0, help="limit the replay-engine sample (0 = all of seed 0)")
-    ap.add_argument("--config", choices=("config5", "config5x3", "spectrum", "etlru", "config4"), default="config5")
+    ap.add_argument("--config", choices=("config5", "config5x3", "spectrum", "etlru", "forced", "config4"), default="config5")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

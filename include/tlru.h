@@ -42,7 +42,7 @@ typedef enum {
   TLRU_EINVAL = 1,       /* bad argument or configuration (block_tokens == 0, rate <= 0, q == 0, ...) */
   TLRU_ERANGE = 2,       /* buffer / workspace too small, or a value exceeds its field width (J > 65535) */
   TLRU_ECUDA = 3,        /* CUDA runtime error; tlru_last_error() carries cudaGetErrorString */
-  TLRU_EUNSUPPORTED = 4, /* policy family not built (policy > TLRU_POLICY_ET_LRU) */
+  TLRU_EUNSUPPORTED = 4, /* policy family not built (policy > TLRU_POLICY_TLRU_FORCED) */
   TLRU_ESTATE = 5        /* internal per-chain state pool exhausted with no fallback left */
 } tlru_status;
 
@@ -182,6 +182,10 @@ tlru_status tlru_trace_from_turns(const uint32_t* conv, const uint16_t* q, const
  *   comes from tlru_set_etlru_model; the trace must carry time_ticks.  evicted_trim
  *   counts blocks with P = 0 (TEL-safe), evicted_lru the rest.  q_hat is ignored.
  *   One warp per instance (replay engine only).
+ * T-LRU under forced caching (App. C; Reading #28): Alg. 1 where the
+ *   post-decision state must hold theta's whole history -- Phases 1 and 2 skip
+ *   theta; only if theta alone exceeds C does it lose tail blocks (counted in
+ *   evicted_lru).  With xi <= q_hat it equals LRU.  Replay engine only.
  * ------------------------------------------------------------------------ */
 enum {
   TLRU_POLICY_LRU = 0,
@@ -190,7 +194,8 @@ enum {
   TLRU_POLICY_END_AWARE = 3,
   TLRU_POLICY_LENGTH_AWARE = 4,
   TLRU_POLICY_TAIL_BELADY = 5,
-  TLRU_POLICY_ET_LRU = 6 /* > 6 -> TLRU_EUNSUPPORTED (forced caching: not built) */
+  TLRU_POLICY_ET_LRU = 6,
+  TLRU_POLICY_TLRU_FORCED = 7 /* > 7 -> TLRU_EUNSUPPORTED */
 };
 
 typedef struct {

@@ -21,6 +21,7 @@ POLICY_END_AWARE = 3
 POLICY_LENGTH_AWARE = 4
 POLICY_TAIL_BELADY = 5
 POLICY_ET_LRU = 6
+POLICY_TLRU_FORCED = 7
 ENGINE_REPLAY = 0
 ENGINE_STACK = 1
 

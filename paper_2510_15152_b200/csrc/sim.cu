@@ -249,9 +249,11 @@ __global__ void __launch_bounds__(32) sim_kernel(const ItemDev* __restrict__ ite
             if (c.overflow) active = false;
           }
         } else if (active) {
-          const bool last = qn == 0xFFFFFFFFu;
+          const bool forced = lp.policy == TLRU_POLICY_TLRU_FORCED;  // no release, D = xi - Q_hat
+          const bool last = !forced && qn == 0xFFFFFFFFu;
           const uint32_t Dcur = lp.policy == TLRU_POLICY_LENGTH_AWARE ? (lp.xi > qn ? lp.xi - qn : 0u) : lp.D;
-          const uint32_t b = chain_request_aware(c, st, base + k, sim_prev(ev), sim_J(ev), sim_La(ev), last, Dcur);
+          const uint32_t b =
+              chain_request_aware(c, st, base + k, sim_prev(ev), sim_J(ev), sim_La(ev), last, Dcur, forced);
           bst[lane * BST_STRIDE + k] = static_cast<uint16_t>(b);
           if (c.overflow) active = false;
         }
@@ -400,8 +402,9 @@ __global__ void aware_fix_kernel(const LaneDev* __restrict__ lanes, const uint32
           continue;
         }
         const uint32_t Dcur = lp.policy == TLRU_POLICY_LENGTH_AWARE ? (lp.xi > qn ? lp.xi - qn : 0u) : lp.D;
-        bout[lp.boff + e] = static_cast<uint16_t>(
-            chain_request_aware(c, st, e, sim_prev(ev), sim_J(ev), sim_La(ev), nx == TLRU_NONE, Dcur));
+        const bool forced = lp.policy == TLRU_POLICY_TLRU_FORCED;
+        bout[lp.boff + e] = static_cast<uint16_t>(chain_request_aware(c, st, e, sim_prev(ev), sim_J(ev), sim_La(ev),
+                                                                      !forced && nx == TLRU_NONE, Dcur, forced));
       }
       if (c.overflow) {
         failed = true;
@@ -517,9 +520,9 @@ static tlru_status make_plan(const tlru_trace* traces, uint32_t nt, const tlru_i
   for (uint32_t i = 0; i < ni; ++i) {
     const tlru_instance& in = inst[i];
     if (in.trace >= nt) TLRU_FAIL(TLRU_EINVAL, "instance %u: trace index %u out of range", i, in.trace);
-    if (in.policy > TLRU_POLICY_ET_LRU)
-      TLRU_FAIL(TLRU_EUNSUPPORTED, "instance %u: policy %u is not built (0..6: LRU, T-LRU, Threshold-LRU, "
-                "End-Aware, Length-Aware, Tail-Optimized Belady, ET-LRU)", i, in.policy);
+    if (in.policy > TLRU_POLICY_TLRU_FORCED)
+      TLRU_FAIL(TLRU_EUNSUPPORTED, "instance %u: policy %u is not built (0..7: LRU, T-LRU, Threshold-LRU, "
+                "End-Aware, Length-Aware, Tail-Optimized Belady, ET-LRU, forced-caching T-LRU)", i, in.policy);
     if (in.policy == TLRU_POLICY_ET_LRU) {
       if (g_et_mu < 0.0) TLRU_FAIL(TLRU_EINVAL, "instance %u: ET-LRU needs tlru_set_etlru_model first", i);
       if (traces[in.trace].num_events > 0 && !traces[in.trace].time_ticks)
@@ -599,7 +602,8 @@ static tlru_status make_plan(const tlru_trace* traces, uint32_t nt, const tlru_i
       LaneDev l;
       l.inst = order[k];
       l.C = std::min<uint32_t>(in.capacity, 0x7FFF0000u);
-      l.D = ((in.policy == TLRU_POLICY_TLRU || in.policy == TLRU_POLICY_END_AWARE) && in.xi > in.q_hat)
+      l.D = ((in.policy == TLRU_POLICY_TLRU || in.policy == TLRU_POLICY_END_AWARE ||
+              in.policy == TLRU_POLICY_TLRU_FORCED) && in.xi > in.q_hat)
                 ? in.xi - in.q_hat
                 : 0u;  // free tail
       l.policy = in.policy;

@@ -253,7 +253,8 @@ __device__ __forceinline__ uint32_t chain_request(ChainRegs& c, const St& st, ui
 // insertion, so its surplus is S).
 template <class St>
 __device__ __forceinline__ uint32_t chain_request_aware(ChainRegs& c, const St& st, uint32_t e, uint32_t prev,
-                                                        uint32_t J, uint32_t La, bool last, uint32_t Dcur) {
+                                                        uint32_t J, uint32_t La, bool last, uint32_t Dcur,
+                                                        bool forced = false) {
   uint32_t x_old = 0;
   if (prev != TLRU_NONE) {
     uint32_t lo = c.head, n = c.tail - c.head;
@@ -293,7 +294,9 @@ __device__ __forceinline__ uint32_t chain_request_aware(ChainRegs& c, const St& 
   c.used += La - x_old;
   if (c.used > c.C) {
     uint32_t over = c.used - c.C;
-    while (over > 0 && c.fh < c.tail) {  // Phase 1, oldest surplus first, theta last
+    // forced caching (App. C, Reading #28): theta (the tail entry) is skipped by both phases
+    const uint32_t lim = forced ? c.tail - 1 : c.tail;
+    while (over > 0 && c.fh < lim) {  // Phase 1, oldest surplus first, theta last
       uint32_t take = min(c.frem, over);
       if (take > 0) {
         st.Xr(c.fh) = static_cast<uint16_t>(st.Xr(c.fh) - take);
@@ -306,13 +309,19 @@ __device__ __forceinline__ uint32_t chain_request_aware(ChainRegs& c, const St& 
         c.frem = (c.fh < c.tail) ? min(static_cast<uint32_t>(st.Xr(c.fh)), static_cast<uint32_t>(st.Sr(c.fh))) : 0u;
       }
     }
-    while (over > 0) {  // Phase 2, LRU
+    while (over > 0 && c.head < lim) {  // Phase 2, LRU
       uint32_t x = st.Xr(c.head);
       uint32_t take = min(x, over);
       st.Xr(c.head) = static_cast<uint16_t>(x - take);
       over -= take;
       c.ev_lru += take;
       if (x == take) ++c.head;
+    }
+    if (over > 0) {  // forced: theta alone exceeds C -- its tail blocks (free ones first) go
+      const uint32_t t = c.tail - 1;
+      st.Xr(t) = static_cast<uint16_t>(st.Xr(t) - over);
+      if (c.fh == t) c.frem -= min(c.frem, over);
+      c.ev_lru += over;
     }
     c.used = c.C;
   }
