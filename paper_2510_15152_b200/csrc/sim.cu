@@ -39,6 +39,7 @@ struct LaneDev {
 // re-runs the others from the exact F_{k-1}, in order, so every output is exact.
 struct AwareDev {
   uint32_t seg_len, burn, nseg_max, wsnap;
+  uint32_t burn_long;        // forced-caching groups: fragments kept only by Phase 2 can be old
   uint32_t* snap;            // [aware lane][seg][2] snapshots of 4 + 2 * wsnap words
   unsigned long long* segc;  // [aware lane][seg][2] evicted_trim, evicted_lru of the segment
   uint32_t* segm;            // [aware lane][seg] max occupancy in the segment
@@ -65,6 +66,8 @@ __device__ void snap_write(uint32_t* out, uint32_t wsnap, const ChainRegs& c, co
         frem = eff;
       }
       s = 0;
+    } else {
+      s = min(x, s);  // the effective surplus: identical whether S is stored or the constant D
     }
     if (n < wsnap) {
       tau[n] = st.T(k);
@@ -107,8 +110,10 @@ __device__ bool snap_equal(const uint32_t* a, const uint32_t* b, uint32_t wsnap)
   return true;
 }
 
-constexpr uint32_t kAwareTLRU = 1;    // End-/Length-Aware T-LRU lanes
+constexpr uint32_t kAwareTLRU = 1;    // Length-Aware T-LRU lanes (per-entry surplus)
 constexpr uint32_t kAwareBelady = 2;  // Tail-Optimized Belady lanes
+constexpr uint32_t kAwareNoS = 3;     // End-Aware lanes (surplus = constant D: no surplus array)
+constexpr uint32_t kAwareForced = 4;  // forced-caching T-LRU lanes (no surplus array, long burn-in)
 
 struct GroupDev {
   uint32_t trace, lane0, nlanes, W;
@@ -157,7 +162,7 @@ __device__ __forceinline__ void acc_commit(AccDev* acc, uint32_t inst, const Cha
 // One warp per (lane group, segment).  W = state entries per lane (compile-time).
 // AWARE: End-/Length-Aware groups: the segment is the whole trace (their cache is not the
 // top-C of the universe, so no exact warm start exists) and the state keeps per-entry surplus.
-template <int W, bool AWARE>
+template <int W, bool AWARE, bool NOS = false>
 __global__ void __launch_bounds__(32) sim_kernel(const ItemDev* __restrict__ items, const GroupDev* __restrict__ groups,
                                                  const LaneDev* __restrict__ lanes, const TraceDev* __restrict__ traces,
                                                  uint32_t seg_len, uint16_t* __restrict__ bout, AccDev* acc,
@@ -166,7 +171,7 @@ __global__ void __launch_bounds__(32) sim_kernel(const ItemDev* __restrict__ ite
   uint32_t* tau_s = reinterpret_cast<uint32_t*>(smem);
   uint16_t* X_s = reinterpret_cast<uint16_t*>(tau_s + W * 32);
   uint16_t* S_s = X_s + W * 32;
-  uint16_t* bst = AWARE ? S_s + W * 32 : S_s;
+  uint16_t* bst = (AWARE && !NOS) ? S_s + W * 32 : S_s;
   const int lane = threadIdx.x;
   const ItemDev it = items[blockIdx.x];
   const GroupDev g = groups[it.group];
@@ -174,7 +179,8 @@ __global__ void __launch_bounds__(32) sim_kernel(const ItemDev* __restrict__ ite
   const uint32_t sl = AWARE ? aw.seg_len : seg_len;
   const uint32_t s = it.seg * sl;
   const uint32_t s_end = static_cast<uint32_t>(min(uint64_t(s) + sl, tr.E));
-  const uint32_t s0 = AWARE ? (s > aw.burn ? s - aw.burn : 0u) : s;  // aware: burn-in from an empty cache
+  const uint32_t burn = g.aware == kAwareForced ? aw.burn_long : aw.burn;
+  const uint32_t s0 = AWARE ? (s > burn ? s - burn : 0u) : s;  // aware: burn-in from an empty cache
   LaneDev lp;
   lp.inst = 0xFFFFFFFFu;
   lp.C = lp.D = lp.T = 0;
@@ -182,7 +188,7 @@ __global__ void __launch_bounds__(32) sim_kernel(const ItemDev* __restrict__ ite
   lp.policy = lp.xi = 0;
   if (lane < static_cast<int>(g.nlanes)) lp = lanes[g.lane0 + lane];
   bool active = lp.inst != 0xFFFFFFFFu;
-  SmemState st{tau_s, X_s, S_s, lane};
+  SmemStateT<NOS> st{tau_s, X_s, S_s, lane, static_cast<uint16_t>(min(lp.D, 65535u))};
   ChainRegs c;
   chain_init(c, lp.C, lp.D, lp.T, W, active && s > 0);
   const bool bel = AWARE && g.aware == kAwareBelady;  // warp-uniform
@@ -470,17 +476,22 @@ static int w_class(uint32_t C, uint32_t nconv) {
 
 static bool is_aware(const tlru_instance& in) { return in.policy >= TLRU_POLICY_END_AWARE; }
 static uint32_t aware_kind(const tlru_instance& in) {
-  return in.policy == TLRU_POLICY_TAIL_BELADY ? kAwareBelady : (is_aware(in) ? kAwareTLRU : 0u);
+  if (in.policy == TLRU_POLICY_TAIL_BELADY) return kAwareBelady;
+  if (in.policy == TLRU_POLICY_END_AWARE) return kAwareNoS;
+  if (in.policy == TLRU_POLICY_TLRU_FORCED) return kAwareForced;
+  return is_aware(in) ? kAwareTLRU : 0u;
 }
 
 struct Plan {
   std::vector<LaneDev> lanes;
   std::vector<GroupDev> groups;
   std::vector<ItemDev> items[kNumW];
-  std::vector<ItemDev> items_aware[kNumW];  // End-/Length-Aware segments (burn-in + fix-up)
+  std::vector<ItemDev> items_aware[kNumW];  // Length-Aware / Belady segments (burn-in + fix-up)
+  std::vector<ItemDev> items_nos[kNumW];    // End-Aware / forced-caching segments (no surplus array)
   bool any_aware = false;
   std::vector<uint32_t> alane, atrace;       // aware lane -> global lane index, trace
-  uint32_t aseg = 8192, aburn = 4096, anseg_max = 1, awsnap = 32;
+  uint32_t aseg = 8192, aburn = 4096, aburn_long = 16384, anseg_max = 1, awsnap = 32;
+  bool any_forced = false;
   std::vector<EtItem> et_items;              // ET-LRU instances (etlru.cuh)
   std::vector<EtSeg> et_segs[kNumW];         // their (instance, segment) warps per state class
   uint32_t n_et = 0, et_seg_len = 8192, et_burn = 4096, et_nseg_max = 1, et_wsnap = 32;
@@ -535,7 +546,12 @@ static tlru_status make_plan(const tlru_trace* traces, uint32_t nt, const tlru_i
     const uint32_t C = std::min<uint32_t>(in.capacity, 0x7FFF0000u);
     wc[i] = g_opt_w >= 0 ? g_opt_w : w_class(C, traces[in.trace].num_conversations);
     // aware chains keep 8 B per entry: 1024 x 32 lanes would exceed shared memory (spill covers the rest)
-    if (is_aware(in)) wc[i] = std::min(wc[i], kNumW - 2);
+    // End-/Length-Aware chains release terminated conversations, so their entries are bounded by
+    // the live conversations (<= ~91 on the preset), not by C: 128 entries (more -> the fix-up);
+    // forced-caching chains keep LRU-like state (up to 1024 entries of 6 B, no surplus array)
+    if ((in.policy == TLRU_POLICY_END_AWARE || in.policy == TLRU_POLICY_LENGTH_AWARE) && g_opt_w < 0)
+      wc[i] = std::min(wc[i], 2);
+    if (is_aware(in) && aware_kind(in) == kAwareTLRU) wc[i] = std::min(wc[i], kNumW - 2);
     if (in.policy == TLRU_POLICY_TAIL_BELADY && g_opt_w < 0) {
       // entries hold X >= 1 (tombstones are compacted before the state counts as full), so
       // W > C never overflows; the live conversations of a trace bound it too (<= ~91 on the
@@ -636,10 +652,14 @@ static tlru_status make_plan(const tlru_trace* traces, uint32_t nt, const tlru_i
   P->seg_len = static_cast<uint32_t>(seg);
   {  // aware segments: enough warps to fill the GPU, but >= 2x the burn-in
     uint64_t ag = 0;
-    for (const GroupDev& g : P->groups) ag += g.aware ? 1u : 0u;
+    for (const GroupDev& g : P->groups) {
+      ag += g.aware ? 1u : 0u;
+      P->any_forced = P->any_forced || g.aware == kAwareForced;
+    }
     const uint64_t pa = ag ? (148ull * 8ull + ag - 1) / ag : 1;
     uint64_t sa = Emax ? (Emax + pa - 1) / pa : 8192;
-    sa = std::min<uint64_t>(std::max<uint64_t>(sa, 2ull * P->aburn), 1ull << 20);
+    sa = std::min<uint64_t>(std::max<uint64_t>(sa, P->any_forced ? P->aburn_long : 2ull * P->aburn), 1ull << 20);
+    if (g_opt_seg) sa = std::max<uint32_t>(g_opt_seg, 64);  // tests: short segments exercise the fix-up
     P->aseg = static_cast<uint32_t>((sa + 31) & ~31ull);
   }
   uint64_t nitems = 0;
@@ -648,7 +668,8 @@ static tlru_status make_plan(const tlru_trace* traces, uint32_t nt, const tlru_i
     const uint64_t E = P->traces[g.trace].E;
     if (g.aware) {  // segments of aseg events, each with an aburn-event burn-in
       const uint64_t nsa = (E + P->aseg - 1) / P->aseg;
-      for (uint64_t sgi = 0; sgi < nsa; ++sgi) P->items_aware[g.W].push_back(ItemDev{gi, static_cast<uint32_t>(sgi)});
+      auto& dst = (g.aware == kAwareNoS || g.aware == kAwareForced) ? P->items_nos[g.W] : P->items_aware[g.W];
+      for (uint64_t sgi = 0; sgi < nsa; ++sgi) dst.push_back(ItemDev{gi, static_cast<uint32_t>(sgi)});
       P->anseg_max = std::max<uint32_t>(P->anseg_max, static_cast<uint32_t>(nsa));
       nitems += nsa;
       continue;
@@ -698,7 +719,7 @@ struct SimWs {
 
 static void carve_sim(Carver& cv, const Plan& P, uint32_t ni, SimWs* w) {
   uint64_t nitems = 0;
-  for (int k = 0; k < kNumW; ++k) nitems += P.items[k].size() + P.items_aware[k].size();
+  for (int k = 0; k < kNumW; ++k) nitems += P.items[k].size() + P.items_aware[k].size() + P.items_nos[k].size();
   w->lanes = cv.take<LaneDev>(P.lanes.size() + 1);
   w->groups = cv.take<GroupDev>(P.groups.size() + 1);
   w->items = cv.take<ItemDev>(nitems + 1);
@@ -716,6 +737,7 @@ static void carve_sim(Carver& cv, const Plan& P, uint32_t ni, SimWs* w) {
   const uint64_t nsl = std::max<uint64_t>(nal, 1) * P.anseg_max;
   w->aw.seg_len = P.aseg;
   w->aw.burn = P.aburn;
+  w->aw.burn_long = P.aburn_long;
   w->aw.nseg_max = P.anseg_max;
   w->aw.wsnap = P.awsnap;
   w->aw.snap = cv.take<uint32_t>(nal ? nsl * 2 * snap_words(P.awsnap) : 1);
@@ -757,15 +779,15 @@ static tlru_status record(int k, cudaStream_t st) {
   return TLRU_OK;
 }
 
-template <int W, bool AWARE>
+template <int W, bool AWARE, bool NOS = false>
 static tlru_status launch_w(const std::vector<ItemDev>& items, const ItemDev* d_items, const SimWs& w,
                             uint32_t seg_len, uint16_t* bout, cudaStream_t st) {
   if (items.empty()) return TLRU_OK;
-  const size_t smem = size_t(W) * 32 * (sizeof(uint32_t) + (AWARE ? 2 : 1) * sizeof(uint16_t)) +
+  const size_t smem = size_t(W) * 32 * (sizeof(uint32_t) + ((AWARE && !NOS) ? 2 : 1) * sizeof(uint16_t)) +
                       32 * BST_STRIDE * sizeof(uint16_t);
-  TLRU_CUDA(cudaFuncSetAttribute(sim_kernel<W, AWARE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  TLRU_CUDA(cudaFuncSetAttribute(sim_kernel<W, AWARE, NOS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(smem)));
-  sim_kernel<W, AWARE><<<static_cast<unsigned>(items.size()), 32, smem, st>>>(d_items, w.groups, w.lanes, w.traces,
+  sim_kernel<W, AWARE, NOS><<<static_cast<unsigned>(items.size()), 32, smem, st>>>(d_items, w.groups, w.lanes, w.traces,
                                                                               seg_len, bout, w.acc, w.spill,
                                                                               w.counters, w.aw);
   TLRU_CHECK_LAUNCH();
@@ -858,7 +880,7 @@ extern "C" tlru_status tlru_simulate_batch(const tlru_trace* traces, uint32_t nt
   TLRU_TRY(check_ws(cv, ws, ws_bytes));
   // tables -> device (pageable copies complete before the call returns)
   std::vector<ItemDev> all_items;
-  size_t item_off[kNumW + 1], aware_off[kNumW];
+  size_t item_off[kNumW + 1], aware_off[kNumW], nos_off[kNumW];
   for (int k = 0; k < kNumW; ++k) {
     item_off[k] = all_items.size();
     all_items.insert(all_items.end(), P.items[k].begin(), P.items[k].end());
@@ -867,6 +889,10 @@ extern "C" tlru_status tlru_simulate_batch(const tlru_trace* traces, uint32_t nt
   for (int k = 0; k < kNumW; ++k) {
     aware_off[k] = all_items.size();
     all_items.insert(all_items.end(), P.items_aware[k].begin(), P.items_aware[k].end());
+  }
+  for (int k = 0; k < kNumW; ++k) {
+    nos_off[k] = all_items.size();
+    all_items.insert(all_items.end(), P.items_nos[k].begin(), P.items_nos[k].end());
   }
   TLRU_CUDA(cudaMemcpyAsync(w.lanes, P.lanes.data(), P.lanes.size() * sizeof(LaneDev), cudaMemcpyHostToDevice, st));
   TLRU_CUDA(cudaMemcpyAsync(w.groups, P.groups.data(), P.groups.size() * sizeof(GroupDev), cudaMemcpyHostToDevice, st));
@@ -900,19 +926,26 @@ extern "C" tlru_status tlru_simulate_batch(const tlru_trace* traces, uint32_t nt
     const ItemDev* d = w.items + item_off[k];
     const ItemDev* da = w.items + aware_off[k];
     const std::vector<ItemDev>& ia = P.items_aware[k];
+    const ItemDev* dn = w.items + nos_off[k];
+    const std::vector<ItemDev>& in_ = P.items_nos[k];
     switch (k) {
       case 0: TLRU_TRY((launch_w<32, false>(P.items[k], d, w, P.seg_len, uncached, st)));
-              TLRU_TRY((launch_w<32, true>(ia, da, w, P.seg_len, uncached, st))); break;
+              TLRU_TRY((launch_w<32, true>(ia, da, w, P.seg_len, uncached, st)));
+              TLRU_TRY((launch_w<32, true, true>(in_, dn, w, P.seg_len, uncached, st))); break;
       case 1: TLRU_TRY((launch_w<64, false>(P.items[k], d, w, P.seg_len, uncached, st)));
-              TLRU_TRY((launch_w<64, true>(ia, da, w, P.seg_len, uncached, st))); break;
+              TLRU_TRY((launch_w<64, true>(ia, da, w, P.seg_len, uncached, st)));
+              TLRU_TRY((launch_w<64, true, true>(in_, dn, w, P.seg_len, uncached, st))); break;
       case 2: TLRU_TRY((launch_w<128, false>(P.items[k], d, w, P.seg_len, uncached, st)));
-              TLRU_TRY((launch_w<128, true>(ia, da, w, P.seg_len, uncached, st))); break;
+              TLRU_TRY((launch_w<128, true>(ia, da, w, P.seg_len, uncached, st)));
+              TLRU_TRY((launch_w<128, true, true>(in_, dn, w, P.seg_len, uncached, st))); break;
       case 3: TLRU_TRY((launch_w<256, false>(P.items[k], d, w, P.seg_len, uncached, st)));
-              TLRU_TRY((launch_w<256, true>(ia, da, w, P.seg_len, uncached, st))); break;
+              TLRU_TRY((launch_w<256, true>(ia, da, w, P.seg_len, uncached, st)));
+              TLRU_TRY((launch_w<256, true, true>(in_, dn, w, P.seg_len, uncached, st))); break;
       case 4: TLRU_TRY((launch_w<512, false>(P.items[k], d, w, P.seg_len, uncached, st)));
-              TLRU_TRY((launch_w<512, true>(ia, da, w, P.seg_len, uncached, st))); break;
+              TLRU_TRY((launch_w<512, true>(ia, da, w, P.seg_len, uncached, st)));
+              TLRU_TRY((launch_w<512, true, true>(in_, dn, w, P.seg_len, uncached, st))); break;
       case 5: TLRU_TRY((launch_w<1024, false>(P.items[k], d, w, P.seg_len, uncached, st)));
-              TLRU_TRY((launch_w<1024, true>(ia, da, w, P.seg_len, uncached, st))); break;
+              TLRU_TRY((launch_w<1024, true, true>(in_, dn, w, P.seg_len, uncached, st))); break;
     }
   }
   if (P.n_et) {  // ET-LRU: one warp per (instance, segment), shared-memory state per class
@@ -959,10 +992,11 @@ extern "C" tlru_status tlru_simulate_batch(const tlru_trace* traces, uint32_t nt
   g_stats.kernels += 3;
   g_stats.chains = 0;
   for (int k = 0; k < kNumW; ++k)
-    g_stats.chains += (P.items[k].size() + P.items_aware[k].size()) * 32 + P.et_segs[k].size();
+    g_stats.chains += (P.items[k].size() + P.items_aware[k].size() + P.items_nos[k].size()) * 32 +
+                      P.et_segs[k].size();
   g_stats.segment_events = P.seg_len;
   for (int k = kNumW - 1; k >= 0; --k)
-    if (!P.items[k].empty() || !P.items_aware[k].empty()) {
+    if (!P.items[k].empty() || !P.items_aware[k].empty() || !P.items_nos[k].empty()) {
       g_stats.state_entries = kWClasses[k];
       break;
     }

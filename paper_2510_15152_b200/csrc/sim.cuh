@@ -33,17 +33,33 @@
 
 namespace tlru {
 
+// A per-entry surplus that is the chain's constant D (End-Aware and forced-caching T-LRU: the
+// surplus at insertion is min(L_after, D) and every read takes min(X, S) with X <= L_after, so
+// S = D reads the same): reads give D, writes are dropped -- no shared-memory array.
+struct SConstD {
+  uint16_t d;
+  __device__ __forceinline__ operator uint16_t() const { return d; }
+  __device__ __forceinline__ SConstD& operator=(uint16_t) { return *this; }
+};
+
 // Lane-interleaved shared-memory state: entry k of lane l at [k * 32 + l]
 // (4-byte tau and 2-byte X arrays: conflict-free for any per-lane k).
-struct SmemState {
+// NOS: no surplus array (S reads as the constant D, see SConstD).
+template <bool NOS>
+struct SmemStateT {
   uint32_t* tau;
   uint16_t* X;
-  uint16_t* S;  // End-/Length-Aware chains only: surplus of the entry at insertion
+  uint16_t* S;  // End-/Length-Aware / Belady chains only: surplus of the entry
   int lane;
+  uint16_t D;   // NOS: the constant surplus bound
   __device__ __forceinline__ uint32_t& T(uint32_t k) const { return tau[k * 32u + lane]; }
   __device__ __forceinline__ uint16_t& Xr(uint32_t k) const { return X[k * 32u + lane]; }
-  __device__ __forceinline__ uint16_t& Sr(uint32_t k) const { return S[k * 32u + lane]; }
+  __device__ __forceinline__ decltype(auto) Sr(uint32_t k) const {
+    if constexpr (NOS) return SConstD{D};
+    else return (S[k * 32u + lane]);
+  }
 };
+using SmemState = SmemStateT<false>;
 
 // Chain-contiguous global-memory state (spill path).
 struct GlobalState {
