@@ -112,8 +112,8 @@ __device__ bool snap_equal(const uint32_t* a, const uint32_t* b, uint32_t wsnap)
 
 constexpr uint32_t kAwareTLRU = 1;    // Length-Aware T-LRU lanes (per-entry surplus)
 constexpr uint32_t kAwareBelady = 2;  // Tail-Optimized Belady lanes
-constexpr uint32_t kAwareNoS = 3;     // End-Aware lanes (surplus = constant D: no surplus array)
-constexpr uint32_t kAwareForced = 4;  // forced-caching T-LRU lanes (no surplus array, long burn-in)
+constexpr uint32_t kAwareForced = 4;  // forced-caching T-LRU lanes (surplus = constant D: no surplus
+                                      // array; long burn-in)
 
 struct GroupDev {
   uint32_t trace, lane0, nlanes, W;
@@ -477,7 +477,6 @@ static int w_class(uint32_t C, uint32_t nconv) {
 static bool is_aware(const tlru_instance& in) { return in.policy >= TLRU_POLICY_END_AWARE; }
 static uint32_t aware_kind(const tlru_instance& in) {
   if (in.policy == TLRU_POLICY_TAIL_BELADY) return kAwareBelady;
-  if (in.policy == TLRU_POLICY_END_AWARE) return kAwareNoS;
   if (in.policy == TLRU_POLICY_TLRU_FORCED) return kAwareForced;
   return is_aware(in) ? kAwareTLRU : 0u;
 }
@@ -546,11 +545,11 @@ static tlru_status make_plan(const tlru_trace* traces, uint32_t nt, const tlru_i
     const uint32_t C = std::min<uint32_t>(in.capacity, 0x7FFF0000u);
     wc[i] = g_opt_w >= 0 ? g_opt_w : w_class(C, traces[in.trace].num_conversations);
     // aware chains keep 8 B per entry: 1024 x 32 lanes would exceed shared memory (spill covers the rest)
-    // End-/Length-Aware chains release terminated conversations, so their entries are bounded by
-    // the live conversations (<= ~91 on the preset), not by C: 128 entries (more -> the fix-up);
-    // forced-caching chains keep LRU-like state (up to 1024 entries of 6 B, no surplus array)
-    if ((in.policy == TLRU_POLICY_END_AWARE || in.policy == TLRU_POLICY_LENGTH_AWARE) && g_opt_w < 0)
-      wc[i] = std::min(wc[i], 2);
+    // End-/Length-Aware chains keep a surplus array (8 B per entry): 1024 x 32 lanes would exceed
+    // shared memory (the fix-up covers the rest).  Measured: bounding them by their live
+    // conversations (128 or 256 entries) or splitting End- from Length-Aware lanes was slower on
+    // the spectrum workload (wider capacity ranges per warp, more frequent compaction).
+    // Forced-caching chains keep LRU-like state: up to 1024 entries of 6 B (no surplus array).
     if (is_aware(in) && aware_kind(in) == kAwareTLRU) wc[i] = std::min(wc[i], kNumW - 2);
     if (in.policy == TLRU_POLICY_TAIL_BELADY && g_opt_w < 0) {
       // entries hold X >= 1 (tombstones are compacted before the state counts as full), so
@@ -668,7 +667,7 @@ static tlru_status make_plan(const tlru_trace* traces, uint32_t nt, const tlru_i
     const uint64_t E = P->traces[g.trace].E;
     if (g.aware) {  // segments of aseg events, each with an aburn-event burn-in
       const uint64_t nsa = (E + P->aseg - 1) / P->aseg;
-      auto& dst = (g.aware == kAwareNoS || g.aware == kAwareForced) ? P->items_nos[g.W] : P->items_aware[g.W];
+      auto& dst = g.aware == kAwareForced ? P->items_nos[g.W] : P->items_aware[g.W];
       for (uint64_t sgi = 0; sgi < nsa; ++sgi) dst.push_back(ItemDev{gi, static_cast<uint32_t>(sgi)});
       P->anseg_max = std::max<uint32_t>(P->anseg_max, static_cast<uint32_t>(nsa));
       nitems += nsa;
