@@ -64,3 +64,23 @@ def test_generated_preset_and_short_segments(T):
     assert bt2.results_numpy().tobytes() == bt.results_numpy().tobytes()
     for i in range(len(rows)):
         assert np.array_equal(bt2.b(i), bt.b(i))
+
+
+def test_full_size_sampled(T):
+    """BASELINE trace size (10^6 conversations) in the launch configuration of
+    `bench.py --config forced` (one trace, its 100 rows in one batch): sampled instances against
+    the oracle element by element, and no failed chains."""
+    from paper_2510_15152_b200.inputs import CAPS_CONFIG5
+    p = preset("wildchat", 4, 1_000_000)
+    tr = T.generate_traces([p], exports=False)[0]
+    rows = [(0, FORCED, C, xi, Q_HAT, SLO_BLOCKS) for C in CAPS_CONFIG5 for xi in (4, 8, 16, 24)]
+    bt = T.simulate_batch([tr], rows)
+    assert T.last_sim_stats()["failed_chains"] == 0
+    o = O.generate(p)
+    res = bt.results_numpy()
+    for C, xi in ((16, 4), (256, 24), (CAPS_CONFIG5[24], 16)):
+        i = rows.index((0, FORCED, C, xi, Q_HAT, SLO_BLOCKS))
+        r = O.replay(o.conv, o.q, o.a, FORCED, C, xi, Q_HAT)
+        assert np.array_equal(bt.b(i).astype(np.uint64), r.b), (C, xi)
+        assert (res[i]["evicted_trim"], res[i]["evicted_lru"], res[i]["max_occupancy"]) == (
+            r.evicted_trim, r.evicted_lru, r.max_occupancy)
