@@ -72,3 +72,29 @@ def test_one_event_and_single_conversation(T):
 def test_ragged_lengths_and_extreme_parameters(T, E):
     conv, q, a = random_trace(6000 + E, E, 12, q_max=5, a_max=5, locality=0.5)
     run_and_check(T, conv, q, a, rows_for((0, 1, 7, 64, 70000, 0x7FFFFFFF), (0, 1, 6, 40000)))
+
+
+def test_tiny_traces_grid_every_policy(T):
+    """BASELINE config 2 (<= 4 conversations, <= 3 turns) for the policy families beyond
+    LRU / T-LRU (those have the full grid in test_gpu_parity): every C in [0, 8], xi in [0, 5],
+    Q_hat in [0, 3] on 60 traces, GPU against the oracle."""
+    from paper_2510_15152_b200.inputs import tiny_trace
+    traces, otr, rows = [], [], []
+    for seed in range(60):
+        conv, q, a = tiny_trace(seed)
+        traces.append(upload(T, conv, q, a))
+        otr.append((conv, q, a))
+        for pol in (2, 3, 4, 5, 6, 7):
+            for C in range(9):
+                for xi in range(6):
+                    for qh in (range(4) if pol in (3, 4, 7) else (0,)):
+                        rows.append((seed, pol, C, xi, qh, 2) + ((2,) if pol == 2 else ()))
+    bt = T.simulate_batch(traces, rows)
+    assert T.last_sim_stats()["failed_chains"] == 0
+    res = bt.results_numpy()
+    for i, r in enumerate(rows):
+        conv, q, a = otr[r[0]]
+        o = oracle_b(r[1], conv, q, a, r[2], r[3], r[4], r[6] if len(r) > 6 else 0)
+        assert np.array_equal(bt.b(i).astype(np.uint64), o.b), r
+        assert (res[i]["evicted_trim"], res[i]["evicted_lru"], res[i]["max_occupancy"]) == (
+            o.evicted_trim, o.evicted_lru, o.max_occupancy), r
