@@ -139,46 +139,48 @@ typedef struct {
     uint32_t max_turns;
 } oracle_gen_params;
 
-enum { F_BIRTH = 0, F_DEATH = 1, F_TURN_GAP = 2, F_PROMPT = 3, F_RESPONSE = 4 };
 static const uint64_t KEY_TAG = 0x544C52552D474E31ull; /* "TLRU-GN1" */
 
-static void draw(uint64_t seed, uint64_t conv, uint64_t turn, uint64_t field, uint64_t attempt,
-                 uint64_t out[4]) {
-    uint64_t ctr[4] = {conv, turn, field | (attempt << 8), 0};
+/* The random numbers of turn `turn` of conversation `conv` (Reading #16): Philox4x64-10 with
+   counter (conv, turn, attempt, 0).  Attempt 0: o[0] = the gap before the turn (turn 0: the
+   birth gap), o[1], o[2] = the first polar pair, o[3] = the death clock (turn 0); a rejected
+   polar pair retries with attempt 1, 2, ... */
+static void draw(uint64_t seed, uint64_t conv, uint64_t turn, uint64_t attempt, uint64_t out[4]) {
+    uint64_t ctr[4] = {conv, turn, attempt, 0};
     uint64_t key[2] = {seed, KEY_TAG};
     oracle_philox4x64(ctr, key, out);
 }
 
-/* Exponential(rate) gap, returned in integer microsecond ticks: floor(-ln(u) * (1e6/rate)). */
-static uint64_t exp_ticks(uint64_t seed, uint64_t conv, uint64_t turn, uint64_t field, double rate) {
-    uint64_t o[4];
-    draw(seed, conv, turn, field, 0, o);
-    double u = oracle_u01(o[0]);
+/* Exponential(rate) gap from one 64-bit draw, in integer microsecond ticks:
+   floor(-ln(u) * (1e6/rate)). */
+static uint64_t exp_ticks(uint64_t x, double rate) {
+    double u = oracle_u01(x);
     double scale = 1000000.0 / rate;
     double g = (0.0 - oracle_det_ln(u)) * scale;
     return (uint64_t)floor(g);
 }
 
-/* Standard normal by the Marsaglia polar method; attempt a uses counter (.., field|a<<8). */
-static double std_normal(uint64_t seed, uint64_t conv, uint64_t turn, uint64_t field) {
+/* Two standard normals by the Marsaglia polar method (one accepted pair gives both):
+   the prompt's z1 = v1 f and the response's z2 = v2 f. */
+static void std_normal_pair(uint64_t seed, uint64_t conv, uint64_t turn, double* z1, double* z2) {
     for (uint64_t a = 0; a < 64; ++a) {
         uint64_t o[4];
-        draw(seed, conv, turn, field, a, o);
-        double v1 = 2.0 * oracle_u01(o[0]) - 1.0;
-        double v2 = 2.0 * oracle_u01(o[1]) - 1.0;
+        draw(seed, conv, turn, a, o);
+        double v1 = 2.0 * oracle_u01(o[1]) - 1.0;
+        double v2 = 2.0 * oracle_u01(o[2]) - 1.0;
         double s = v1 * v1 + v2 * v2;
         if (s < 1.0 && s > 0.0) {
             double f = sqrt((-2.0 * oracle_det_ln(s)) / s);
-            return v1 * f;
+            *z1 = v1 * f;
+            *z2 = v2 * f;
+            return;
         }
     }
-    return 0.0;
+    *z1 = *z2 = 0.0;
 }
 
 /* Lognormal token count with the given mean, clipped to [lo, hi], rounded half-up. */
-static uint32_t lognormal_tokens(uint64_t seed, uint64_t conv, uint64_t turn, uint64_t field,
-                                 double mean, double sigma, uint32_t lo, uint32_t hi) {
-    double z = std_normal(seed, conv, turn, field);
+static uint32_t lognormal_tokens(double z, double mean, double sigma, uint32_t lo, uint32_t hi) {
     double mu = oracle_det_ln(mean) - 0.5 * (sigma * sigma);
     double x = oracle_det_exp(mu + sigma * z);
     double t = floor(x + 0.5);
@@ -216,27 +218,31 @@ int64_t oracle_generate(const oracle_gen_params* p, uint64_t** ticks_out, uint32
     if (!ev) return -1;
     uint64_t birth = 0;
     for (uint32_t c = 0; c < p->num_conversations; ++c) {
+        uint64_t o0[4];
+        draw(p->seed, c, 0, 0, o0);
         /* Births: Poisson(lambda_conv) process, gaps Exp(lambda_conv). */
-        birth += exp_ticks(p->seed, c, 0, F_BIRTH, p->birth_rate);
+        birth += exp_ticks(o0[0], p->birth_rate);
         /* Death clock Exp(mu). */
-        uint64_t life = exp_ticks(p->seed, c, 0, F_DEATH, p->death_rate);
+        uint64_t life = exp_ticks(o0[3], p->death_rate);
         uint64_t t = birth, elapsed = 0;
         uint32_t L = 0;
         for (uint32_t k = 0; k < p->max_turns; ++k) {
             if (k > 0) {
                 /* While active, turns follow a Poisson(lambda_turn) process. */
-                uint64_t gap = exp_ticks(p->seed, c, k, F_TURN_GAP, p->turn_rate);
+                uint64_t o[4];
+                draw(p->seed, c, k, 0, o);
+                uint64_t gap = exp_ticks(o[0], p->turn_rate);
                 elapsed += gap;
                 if (elapsed >= life) break;
                 t += gap;
             }
             /* Random prompt length Q and response length A per turn. */
-            uint32_t ptok = lognormal_tokens(p->seed, c, k, F_PROMPT, p->prompt_mean_tokens,
-                                             p->prompt_sigma_ln, p->prompt_min_tokens,
-                                             p->prompt_max_tokens);
-            uint32_t rtok = lognormal_tokens(p->seed, c, k, F_RESPONSE, p->response_mean_tokens,
-                                             p->response_sigma_ln, p->response_min_tokens,
-                                             p->response_max_tokens);
+            double zp, zr;
+            std_normal_pair(p->seed, c, k, &zp, &zr);
+            uint32_t ptok = lognormal_tokens(zp, p->prompt_mean_tokens, p->prompt_sigma_ln,
+                                             p->prompt_min_tokens, p->prompt_max_tokens);
+            uint32_t rtok = lognormal_tokens(zr, p->response_mean_tokens, p->response_sigma_ln,
+                                             p->response_min_tokens, p->response_max_tokens);
             uint32_t q = (ptok + B - 1) / B;
             if (q < 1) q = 1;
             uint32_t a = (rtok + B - 1) / B;

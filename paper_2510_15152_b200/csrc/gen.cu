@@ -32,17 +32,21 @@ struct GenDev {  // per-trace constants, by value to the kernels
 // Exact turn count of conversation c: death/turn clocks plus the context-window rule,
 // which needs the lengths.  Used only for conversations that may reach L_max.
 __device__ __forceinline__ uint32_t conv_count_exact(const GenDev& g, uint32_t c) {
-  const uint64_t life = exp_gap_ticks(g.seed, c, 0, FIELD_DEATH, g.us_death);  // Exp(mu) lifetime
+  const U64x4 d00 = turn_draw(g.seed, c, 0, 0);
+  const uint64_t life = exp_ticks_of(d00.v[3], g.us_death);  // Exp(mu) lifetime
   const double p_mu = lognormal_mu(g.p_mean, g.p_sigma), r_mu = lognormal_mu(g.r_mean, g.r_sigma);
   uint64_t elapsed = 0;
   uint32_t L = 0, n = 0;
   for (uint32_t k = 0; k < g.max_turns; ++k) {
+    const U64x4 d = k ? turn_draw(g.seed, c, k, 0) : d00;
     if (k > 0) {  // Poisson(lambda_turn) turns while alive
-      elapsed += exp_gap_ticks(g.seed, c, k, FIELD_TURN_GAP, g.us_turn);
+      elapsed += exp_ticks_of(d.v[0], g.us_turn);
       if (elapsed >= life) break;
     }
-    const uint32_t pt = lognormal_tokens(g.seed, c, k, FIELD_PROMPT, p_mu, g.p_sigma, g.p_lo, g.p_hi);
-    const uint32_t rt = lognormal_tokens(g.seed, c, k, FIELD_RESPONSE, r_mu, g.r_sigma, g.r_lo, g.r_hi);
+    double zp, zr;
+    polar_pair(g.seed, c, k, d, zp, zr);
+    const uint32_t pt = lognormal_tokens(zp, p_mu, g.p_sigma, g.p_lo, g.p_hi);
+    const uint32_t rt = lognormal_tokens(zr, r_mu, g.r_sigma, g.r_lo, g.r_hi);
     uint32_t q = (pt + g.B - 1) / g.B;
     if (q < 1) q = 1;
     const uint32_t a = (rt + g.B - 1) / g.B;
@@ -54,12 +58,11 @@ __device__ __forceinline__ uint32_t conv_count_exact(const GenDev& g, uint32_t c
 }
 
 // Turns allowed by the death clock and max_turns alone (no lengths drawn).
-__device__ __forceinline__ uint32_t clock_turns(const GenDev& g, uint32_t c, uint64_t* last_elapsed) {
-  const uint64_t life = exp_gap_ticks(g.seed, c, 0, FIELD_DEATH, g.us_death);
+__device__ __forceinline__ uint32_t clock_turns(const GenDev& g, uint32_t c, uint64_t life, uint64_t* last_elapsed) {
   uint64_t elapsed = 0, kept = 0;
   uint32_t n = 1;
   for (uint32_t k = 1; k < g.max_turns; ++k) {
-    elapsed += exp_gap_ticks(g.seed, c, k, FIELD_TURN_GAP, g.us_turn);
+    elapsed += exp_ticks_of(turn_draw(g.seed, c, k, 0).v[0], g.us_turn);
     if (elapsed >= life) break;
     kept = elapsed;
     ++n;
@@ -79,9 +82,10 @@ __global__ void gen_count_kernel(GenDev g, uint64_t* gaps, uint32_t* counts, uns
   for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < Npad; c += stride) {
     uint32_t n = 0;
     if (c < g.N) {
-      gaps[c] = exp_gap_ticks(g.seed, c, 0, FIELD_BIRTH, g.us_birth);  // Poisson(lambda_conv) births
+      const U64x4 d00 = turn_draw(g.seed, c, 0, 0);
+      gaps[c] = exp_ticks_of(d00.v[0], g.us_birth);  // Poisson(lambda_conv) births
       uint64_t el;
-      n = clock_turns(g, c, &el);
+      n = clock_turns(g, c, exp_ticks_of(d00.v[3], g.us_death), &el);  // Exp(mu) lifetime
       counts[c] = n;
       mel = el > mel ? el : mel;
     }
@@ -119,9 +123,12 @@ __global__ void gen_draw_kernel(GenDev g, uint32_t E, const uint32_t* cid, const
   const double p_mu = lognormal_mu(g.p_mean, g.p_sigma), r_mu = lognormal_mu(g.r_mean, g.r_sigma);
   for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < E; j += gridDim.x * blockDim.x) {
     const uint32_t c = cid[j], k = turn[j];
-    gapt[j] = k ? exp_gap_ticks(g.seed, c, k, FIELD_TURN_GAP, g.us_turn) : 0ull;
-    const uint32_t pt = lognormal_tokens(g.seed, c, k, FIELD_PROMPT, p_mu, g.p_sigma, g.p_lo, g.p_hi);
-    const uint32_t rt = lognormal_tokens(g.seed, c, k, FIELD_RESPONSE, r_mu, g.r_sigma, g.r_lo, g.r_hi);
+    const U64x4 d = turn_draw(g.seed, c, k, 0);  // one draw: the gap and the first polar pair
+    gapt[j] = k ? exp_ticks_of(d.v[0], g.us_turn) : 0ull;
+    double zp, zr;
+    polar_pair(g.seed, c, k, d, zp, zr);
+    const uint32_t pt = lognormal_tokens(zp, p_mu, g.p_sigma, g.p_lo, g.p_hi);
+    const uint32_t rt = lognormal_tokens(zr, r_mu, g.r_sigma, g.r_lo, g.r_hi);
     uint32_t q = (pt + g.B - 1) / g.B;
     if (q < 1) q = 1;
     q16[j] = static_cast<uint16_t>(q);

@@ -1,9 +1,12 @@
 // rng.cuh -- counter-based sampling for the synthetic-trace generator (K1).
 //
 // The generator spec (Reading #16) fixes every random
-// value as a pure function of (seed, conversation, turn, field, attempt):
+// value as a pure function of (seed, conversation, turn, attempt, lane):
 //   Philox4x64-10, key = (seed, 0x544C52552D474E31 "TLRU-GN1"),
-//   counter = (conv, turn, field | attempt << 8, 0);
+//   counter = (conv, turn, attempt, 0) -> four 64-bit lanes; attempt 0 of a turn gives
+//   lane 0: the gap before the turn (turn 0: the birth gap), lanes 1, 2: the first polar pair,
+//   lane 3: the death clock (turn 0); a rejected polar pair retries with attempt 1, 2, ...;
+//   one accepted pair (v1, v2) gives both normals: prompt z = v1 f, response z = v2 f;
 //   u = ((x >> 11) + 1) * 2^-53 in (0, 1];
 //   ln / exp evaluated with a fixed sequence of correctly rounded IEEE double
 //   operations (explicit __d*_rn intrinsics: no FMA contraction), so the
@@ -44,11 +47,8 @@ __device__ __forceinline__ U64x4 philox4x64_10(uint64_t c0, uint64_t c1, uint64_
   return out;
 }
 
-enum : uint64_t { FIELD_BIRTH = 0, FIELD_DEATH = 1, FIELD_TURN_GAP = 2, FIELD_PROMPT = 3, FIELD_RESPONSE = 4 };
-
-__device__ __forceinline__ U64x4 gen_draw(uint64_t seed, uint64_t conv, uint64_t turn, uint64_t field,
-                                          uint64_t attempt) {
-  return philox4x64_10(conv, turn, field | (attempt << 8), 0, seed, 0x544C52552D474E31ull);
+__device__ __forceinline__ U64x4 turn_draw(uint64_t seed, uint64_t conv, uint64_t turn, uint64_t attempt) {
+  return philox4x64_10(conv, turn, attempt, 0, seed, 0x544C52552D474E31ull);
 }
 
 __device__ __forceinline__ double unit_open0(uint64_t x) {  // (0, 1]
@@ -105,33 +105,34 @@ __device__ __forceinline__ double dexp(double y) {
   return ldexp(p, static_cast<int>(k));
 }
 
-// Exp(rate) waiting time in integer microsecond ticks.
-__device__ __forceinline__ uint64_t exp_gap_ticks(uint64_t seed, uint64_t conv, uint64_t turn, uint64_t field,
-                                                  double us_per_unit /* = 1e6 / rate */) {
-  U64x4 d = gen_draw(seed, conv, turn, field, 0);
-  double u = unit_open0(d.v[0]);
+// Exp(rate) waiting time in integer microsecond ticks from one 64-bit lane.
+__device__ __forceinline__ uint64_t exp_ticks_of(uint64_t x, double us_per_unit /* = 1e6 / rate */) {
+  double u = unit_open0(x);
   double g = __dmul_rn(__dsub_rn(0.0, dln(u)), us_per_unit);
   return static_cast<uint64_t>(floor(g));
 }
 
-__device__ __forceinline__ double polar_normal(uint64_t seed, uint64_t conv, uint64_t turn, uint64_t field) {
+// Two standard normals of turn (conv, turn) by the Marsaglia polar method: lanes 1, 2 of the
+// attempt-0 draw d0, then of attempts 1, 2, ... until accepted.
+__device__ __forceinline__ void polar_pair(uint64_t seed, uint64_t conv, uint64_t turn, const U64x4& d0, double& z1,
+                                           double& z2) {
   for (uint64_t att = 0; att < 64; ++att) {
-    U64x4 d = gen_draw(seed, conv, turn, field, att);
-    double v1 = __dsub_rn(__dmul_rn(2.0, unit_open0(d.v[0])), 1.0);
-    double v2 = __dsub_rn(__dmul_rn(2.0, unit_open0(d.v[1])), 1.0);
+    const U64x4 d = att == 0 ? d0 : turn_draw(seed, conv, turn, att);
+    double v1 = __dsub_rn(__dmul_rn(2.0, unit_open0(d.v[1])), 1.0);
+    double v2 = __dsub_rn(__dmul_rn(2.0, unit_open0(d.v[2])), 1.0);
     double s = __dadd_rn(__dmul_rn(v1, v1), __dmul_rn(v2, v2));
     if (s < 1.0 && s > 0.0) {
       double f = __dsqrt_rn(__ddiv_rn(__dmul_rn(-2.0, dln(s)), s));
-      return __dmul_rn(v1, f);
+      z1 = __dmul_rn(v1, f);
+      z2 = __dmul_rn(v2, f);
+      return;
     }
   }
-  return 0.0;
+  z1 = z2 = 0.0;
 }
 
-__device__ __forceinline__ uint32_t lognormal_tokens(uint64_t seed, uint64_t conv, uint64_t turn, uint64_t field,
-                                                     double ln_mean_minus_half_var, double sigma, uint32_t lo,
-                                                     uint32_t hi) {
-  double z = polar_normal(seed, conv, turn, field);
+__device__ __forceinline__ uint32_t lognormal_tokens(double z, double ln_mean_minus_half_var, double sigma,
+                                                     uint32_t lo, uint32_t hi) {
   double x = dexp(__dadd_rn(ln_mean_minus_half_var, __dmul_rn(sigma, z)));
   double t = floor(__dadd_rn(x, 0.5));
   if (t < static_cast<double>(lo)) t = static_cast<double>(lo);
