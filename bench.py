@@ -508,7 +508,7 @@ def run_ours(args, rank, world, local_rank):
                          "frac": rep_achieved / peak, "kernel": "sim_kernel<W> (K2 replay)"},
             "note": "Alg. 1 replayed request by request (one lane per instance) on seed 0's instances; "
                     "result bytes identical to the stack engine"}
-    if not args.no_cpu_baseline:
+    if not args.no_cpu_baseline and world == 1:  # the CPU oracle baseline: rank 0 at N = 1 only
         n, dt, cores, sample = cpu_oracle_sample(seed=0, n_conv=args.conversations)
         line["cpu_baseline"] = {"value": n / dt, "unit": "requests/s", "cores": cores, "kind": "oracle",
                                 "sample": sample}
