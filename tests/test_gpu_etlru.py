@@ -165,3 +165,18 @@ def test_short_segments_verified(T):
         T.set_sim_options(0, 0)
     assert st["failed_chains"] == 0
     check_et(bt, rows, [(conv, q, a, ticks)], 0.02, tab)
+
+
+def test_long_prompt_law_table(T):
+    """A prompt law with K = 700 > the 256 table entries kept in shared memory: the kernel reads
+    the tail of ln P(Q >= k) from global memory.  Large xi makes k = X - L + xi reach it."""
+    K = 700
+    tab = [0.0, 0.0] + [math.log(max(1e-300, (1.0 - k / (K + 1.0)) ** 3)) for k in range(2, K + 1)]
+    tab = list(np.minimum.accumulate(np.array(tab)))
+    T.set_etlru_model(0.03, tab)
+    conv, q, a = random_trace(4300, 4000, 40, q_max=30, a_max=30, locality=0.6)
+    ticks = np.cumsum(np.random.default_rng(7).integers(0, 3, size=conv.size)).astype(np.uint64)
+    tr = with_ticks(T, upload(T, conv, q, a), ticks)
+    rows = [(0, ET, C, xi, 0, 8) for C in (50, 300, 1500) for xi in (200, 450, 690)]
+    bt = T.simulate_batch([tr], rows)
+    check_et(bt, rows, [(conv, q, a, ticks)], 0.03, tab)
