@@ -1,21 +1,22 @@
 #!/usr/bin/env python
 """Benchmark of the T-LRU hot path (BASELINE.json metric: simulated requests/s + HBM roofline %).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--scaling strong|weak]
 
-One step = the whole hot path of SURVEY 8(a) over one batch of synthetic input
-(BASELINE config 4 per GPU): generate 4 WildChat-shaped traces of 10^6
-conversations (a1-a3, K1), simulate 384 instances = 4 seeds x 8 capacities x 6 xi
-x {LRU, T-LRU} (a4-a8, K2), tail metrics per instance (a9, K3) and, for N > 1,
-an NCCL all_gather of the per-instance results (a10).  Weak scaling: rank r
-simulates seeds 4r..4r+3, so per-GPU work is fixed as N grows.
+One step = the whole hot path of SURVEY 8(a) over the BASELINE config-5 sweep (configs[4]):
+generate 10 WildChat-shaped traces of 10^6 conversations (a1-a3, K1), simulate 10^4 instances =
+10 seeds x 25 capacities x 20 xi x {LRU, T-LRU} (a4-a8), per-instance tail metrics (a9, fused
+into the engine), and (a10) the NCCL all_gather of the per-instance results plus the all_reduce
+of the pooled (policy, C, xi) histograms over seeds, with pooled P50/P90/P95/P99, TEL and SLO.
+Strong scaling (default): the same 10^4 instances are sharded over the N ranks at sub-trace
+granularity (sweep.plan_strong); each rank regenerates only the traces its instances use.
 
 `value` = requests simulated by all ranks / max-over-ranks device time per step.
-`e2e` = the same metric through the public API from pinned host buffers: H2D of
-each trace's (conv, q, a) turns, tlru_trace_from_turns, tlru_simulate_batch and a
-D2H read of the results, all inside the timed region.
-`--impl reference` times the CPU oracle (oracle/, test infrastructure) on a
-bounded sample of the same workload on the host cores; rank 0 only.
+`e2e` = the same metric through the public API from pinned host buffers: H2D of each trace's
+(conv, q, a) turns, tlru_trace_from_turns, tlru_simulate_batch_ex, pooling, the collectives and
+a D2H read of the result table and pooled metrics, all inside the timed region.
+`--impl reference` times the CPU oracle (oracle/, test infrastructure) on a bounded sample of
+the same workload on the host cores; rank 0 only.
 """
 from __future__ import annotations
 
@@ -33,23 +34,12 @@ sys.path.insert(0, ROOT)
 
 # Algorithmic HBM bytes:
 #  * replay engine (SURVEY 8(d) model): 8-byte event record read per request + 2-byte b written = 10 B/request;
-#  * stack engine: 2-byte b written per request + each trace pass reads the 8-byte sim view and 4-byte next
-#    link and writes/reads the 8-byte scan record once per event (20 B/event/pass), shared by all instances.
 ALGO_BYTES_PER_REQUEST = 10
-STACK_B_BYTES = 2
-STACK_PASS_BYTES_PER_EVENT = 20
 #  * s2_out (the dominant kernel): 2-byte b written per request; 4-byte (L_before | J) read per event and
 #    one 2-byte A_nf per (event, distinct D) read, shared by the instances of a group.
 OUT_B_BYTES = 2
 OUT_EVENT_BYTES = 4
 OUT_ROW_BYTES = 2
-SEEDS_PER_RANK = 4
-
-
-def workload_rows(n_traces: int):
-    from paper_2510_15152_b200.inputs import CAPS_CONFIG4, Q_HAT, SLO_BLOCKS, XI_BLOCKS
-    return [(t, pol, C, xi, Q_HAT, SLO_BLOCKS) for t in range(n_traces) for pol in (0, 1) for C in CAPS_CONFIG4
-            for xi in XI_BLOCKS]
 
 
 def peaks():
@@ -115,19 +105,32 @@ class ClockSampler:
         return out
 
 
-# ----------------------------------------------------------------------------- reference (CPU oracle)
-def cpu_oracle_sample(seed: int = 0, n_conv: int = 1_000_000):
-    """Oracle as it stands, on a bounded sample of the config-5 sweep: generate one trace
-    (seed 0), replay 9 instances (capacities 16, 32, ..., 4096 from the sweep's grid,
-    alternating LRU / T-LRU(xi=16)) on host threads, tail metrics for each."""
+# ----------------------------------------------------------------------------- CPU oracle baseline
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def oracle_trace(seed: int, n_conv: int):
+    """The oracle's own generation of one config-5 trace (untimed: the baseline times the replay loop)."""
+    import oracle as O
+    from paper_2510_15152_b200.inputs import preset
+    return O.generate(preset("wildchat", seed, n_conv))
+
+
+def cpu_replay_sample(tr, insts, threads: int, pin_core: int | None = None):
+    """Replays `insts` = [(policy, C, xi)] of the config-5 grid on trace `tr` with the plain oracle
+    (Alg. 1, oracle/tlru_oracle.c) plus its tail metrics, one instance per host thread; returns
+    (requests, seconds).  pin_core: run on that one core (sched_setaffinity of this thread)."""
     from concurrent.futures import ThreadPoolExecutor
 
     import oracle as O
-    from paper_2510_15152_b200.inputs import ALPHA_MS, CAPS_CONFIG5, Q_HAT, SLO_BLOCKS, preset
-    t0 = time.perf_counter()
-    tr = O.generate(preset("wildchat", seed, n_conv))
-    insts = [(i % 2, C, 16) for i, C in enumerate(CAPS_CONFIG5[::3])]
-    cores = min(len(insts), os.cpu_count() or 1)
+    from paper_2510_15152_b200.inputs import ALPHA_MS, Q_HAT, SLO_BLOCKS
 
     def one(x):
         pol, C, xi = x
@@ -135,82 +138,118 @@ def cpu_oracle_sample(seed: int = 0, n_conv: int = 1_000_000):
         O.tail(r.b, xi, ALPHA_MS * xi, SLO_BLOCKS, ALPHA_MS)
         return tr.E
 
-    with ThreadPoolExecutor(max_workers=cores) as ex:
-        n = sum(ex.map(one, insts))
-    dt = time.perf_counter() - t0
-    return n, dt, cores, (f"config-5 sample: oracle generation of seed {seed} ({n_conv} conversations, {tr.E} "
-                          f"requests) + {len(insts)} instances (C = 16, 32, ..., 4096; LRU / T-LRU xi=16) "
-                          f"on {cores} threads, incl. tail metrics")
+    old = os.sched_getaffinity(0)
+    try:
+        if pin_core is not None:
+            os.sched_setaffinity(0, {pin_core})
+        t0 = time.perf_counter()
+        if threads == 1:
+            n = sum(one(x) for x in insts)
+        else:
+            with ThreadPoolExecutor(max_workers=threads) as ex:
+                n = sum(ex.map(one, insts))
+        dt = time.perf_counter() - t0
+    finally:
+        os.sched_setaffinity(0, old)
+    return n, dt
+
+
+def cpu_sample_instances(k: int):
+    """k instances spread over the config-5 grid: capacities 16..4096, alternating LRU / T-LRU(xi)."""
+    from paper_2510_15152_b200.inputs import CAPS_CONFIG5, XI_CONFIG5
+    out = []
+    for j in range(k):
+        C = CAPS_CONFIG5[(j * 7) % len(CAPS_CONFIG5)]
+        xi = XI_CONFIG5[(j * 3) % len(XI_CONFIG5)]
+        out.append((j % 2, C, xi))
+    return out
+
+
+def cpu_oracle_baseline(n_conv: int, seed: int = 0):
+    """the oracle as it stands on the GPU box's host cores -- one pinned core, then all
+    cores (one instance per thread) -- timing the replay loop only (generation outside the timer)."""
+    tr = oracle_trace(seed, n_conv)
+    ncores = len(os.sched_getaffinity(0))
+    core0 = min(os.sched_getaffinity(0))
+    n1, dt1 = cpu_replay_sample(tr, [(0, 256, 16), (1, 1024, 16)], 1, pin_core=core0)
+    insts = cpu_sample_instances(ncores)
+    na, dta = cpu_replay_sample(tr, insts, ncores)
+    return {
+        "value": na / dta, "unit": "requests/s", "cores": ncores, "kind": "oracle",
+        "sample": (f"config-5 seed {seed} trace ({n_conv} conversations, {tr.E} requests, oracle-generated outside "
+                   f"the timer); replay loop + tail metrics of {len(insts)} instances spread over C = 16..4096, "
+                   f"LRU / T-LRU, one per host thread on all {ncores} cores"),
+        "single_core": {"value": n1 / dt1, "unit": "requests/s", "cores": 1, "pinned_core": core0,
+                        "sample": "LRU C=256 and T-LRU C=1024 xi=16 on the same trace, one pinned core"},
+        "cpu_model": cpu_model(), "nproc": os.cpu_count(),
+    }
 
 
 def run_reference(args, rank, world):
+    """--impl reference: the CPU oracle (test infrastructure) timed on the host cores, rank 0 only.
+    Each step replays one instance per core of the config-5 grid on one oracle-generated trace."""
     if rank != 0:
         return
     import oracle
     oracle.build()
-    times, n_req, cores, sample = [], 0, 1, ""
+    tr = oracle_trace(0, args.conversations)  # untimed
+    ncores = len(os.sched_getaffinity(0))
+    insts = cpu_sample_instances(ncores)
+    times, n_req = [], 0
     for i in range(args.warmup + args.steps):
-        n, dt, cores, sample = cpu_oracle_sample(seed=0)
+        n, dt = cpu_replay_sample(tr, insts, ncores)
         if i >= args.warmup:
             times.append(dt)
             n_req = n
     ms = 1000.0 * statistics.mean(times)
     value = n_req / (ms / 1000.0)
+    sample = (f"config-5 seed 0 trace ({args.conversations} conversations, {tr.E} requests): replay loop + tail "
+              f"metrics of {len(insts)} instances (C = 16..4096, LRU / T-LRU), one per thread on {ncores} cores")
     line = {"impl": "reference", "metric": "simulated requests/sec", "value": value, "unit": "requests/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "u32",
+            "data": "synthetic",
             "config": {"workload": "config5 sample (CPU oracle, see cpu_baseline.sample)", "requests_per_step": n_req},
-            "cpu_baseline": {"value": value, "unit": "requests/s", "cores": cores, "kind": "oracle",
-                             "sample": sample},
+            "cpu_baseline": {"value": value, "unit": "requests/s", "cores": ncores, "kind": "oracle", "sample": sample,
+                             "cpu_model": cpu_model()},
             "e2e": {"value": value, "unit": "requests/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
 # ----------------------------------------------------------------------------- ours
-def workload(name: str, rank: int):
-    """(seeds, rows, description) of one GPU's share.  Weak scaling: rank r takes the seeds
-    after rank r-1's, so per-GPU work is fixed as N grows."""
-    from paper_2510_15152_b200.inputs import SEEDS_CONFIG5, config5_rows
+def workload_global(name: str):
+    """(rows, n_traces, description) of the whole job: rows = (trace, policy, C, xi, Q_hat, slo[, T])
+    with trace = seed index.  Strong scaling shards these rows over the ranks (sweep.plan_strong);
+    weak scaling gives every rank all of them on its own seeds."""
+    from paper_2510_15152_b200.inputs import CAPS_CONFIG4, CAPS_CONFIG5, Q_HAT, SEEDS_CONFIG5, SLO_BLOCKS, XI_BLOCKS
+    from paper_2510_15152_b200.inputs import config5_rows
+    n = SEEDS_CONFIG5
     if name == "spectrum":
-        from paper_2510_15152_b200.inputs import CAPS_CONFIG5, Q_HAT, SLO_BLOCKS
-        seeds = [SEEDS_CONFIG5 * rank + k for k in range(SEEDS_CONFIG5)]
-        rows = [(t, pol, C, xi, Q_HAT, SLO_BLOCKS) for t in range(len(seeds)) for pol in (3, 4, 5)
-                for C in CAPS_CONFIG5 for xi in (4, 8, 16, 24)]
-        return seeds, rows, (
-            "predictability spectrum per GPU (P:389-395, Thm 1): 10 seeds x 10^6-conversation traces x 25 "
-            "capacities x xi in {4, 8, 16, 24} x {End-Aware, Length-Aware T-LRU, Tail-Optimized Belady} = 3000 "
-            "instances (replay engine, burn-in segments verified by the fix-up)")
+        rows = [(t, pol, C, xi, Q_HAT, SLO_BLOCKS) for t in range(n) for pol in (3, 4, 5) for C in CAPS_CONFIG5
+                for xi in (4, 8, 16, 24)]
+        return rows, n, ("predictability spectrum (P:389-395, Thm 1): 10 seeds x 10^6-conversation traces x 25 "
+                         "capacities x xi in {4, 8, 16, 24} x {End-Aware, Length-Aware T-LRU, Tail-Optimized Belady} "
+                         "= 3000 instances (replay engine, burn-in segments verified by the fix-up)")
     if name == "etlru":
-        from paper_2510_15152_b200.inputs import CAPS_CONFIG5, Q_HAT, SLO_BLOCKS
-        seeds = [SEEDS_CONFIG5 * rank + k for k in range(SEEDS_CONFIG5)]
-        rows = [(t, 6, C, xi, Q_HAT, SLO_BLOCKS) for t in range(len(seeds)) for C in CAPS_CONFIG5
-                for xi in (4, 8, 16, 24)]
-        return seeds, rows, (
-            "ET-LRU per GPU (Def. 1 / Alg. 2, P:261-275): 10 seeds x 10^6-conversation traces x 25 capacities x "
-            "xi in {4, 8, 16, 24} = 1000 instances, belief mu = 1/90 s, the preset's prompt law (one warp per "
-            "instance)")
+        rows = [(t, 6, C, xi, Q_HAT, SLO_BLOCKS) for t in range(n) for C in CAPS_CONFIG5 for xi in (4, 8, 16, 24)]
+        return rows, n, ("ET-LRU (Def. 1 / Alg. 2, P:261-275): 10 seeds x 10^6-conversation traces x 25 capacities "
+                         "x xi in {4, 8, 16, 24} = 1000 instances, belief mu = 1/90 s, the preset's prompt law")
     if name == "forced":
-        from paper_2510_15152_b200.inputs import CAPS_CONFIG5, Q_HAT, SLO_BLOCKS
-        seeds = [SEEDS_CONFIG5 * rank + k for k in range(SEEDS_CONFIG5)]
-        rows = [(t, 7, C, xi, Q_HAT, SLO_BLOCKS) for t in range(len(seeds)) for C in CAPS_CONFIG5
-                for xi in (4, 8, 16, 24)]
-        return seeds, rows, (
-            "T-LRU under forced caching per GPU (App. C): 10 seeds x 10^6-conversation traces x 25 capacities x "
-            "xi in {4, 8, 16, 24} = 1000 instances (replay engine, burn-in segments verified by the fix-up)")
+        rows = [(t, 7, C, xi, Q_HAT, SLO_BLOCKS) for t in range(n) for C in CAPS_CONFIG5 for xi in (4, 8, 16, 24)]
+        return rows, n, ("T-LRU under forced caching (App. C): 10 seeds x 10^6-conversation traces x 25 capacities "
+                         "x xi in {4, 8, 16, 24} = 1000 instances (replay engine)")
     if name == "config5x3":
-        seeds = [SEEDS_CONFIG5 * rank + k for k in range(SEEDS_CONFIG5)]
-        return seeds, config5_rows(len(seeds), threshold_lru=True), (
-            "config5 sweep per GPU with the paper's three policies: 10 seeds x 10^6-conversation traces x 25 "
-            "capacities x 20 xi x {LRU, T-LRU, Threshold-LRU (1024 tokens = 8 blocks)} = 1.5x10^4 instances")
-    if name == "config5":
-        seeds = [SEEDS_CONFIG5 * rank + k for k in range(SEEDS_CONFIG5)]
-        return seeds, config5_rows(len(seeds)), (
-            "config5 sweep per GPU: 10 seeds x 10^6-conversation WildChat-shaped traces (generated each step) x "
-            "25 capacities (16..4096 blocks, geometric) x 20 xi (2..40 blocks) x {LRU, T-LRU} = 10^4 instances")
-    seeds = [SEEDS_PER_RANK * rank + k for k in range(SEEDS_PER_RANK)]
-    return seeds, workload_rows(len(seeds)), (
-        "config4 per GPU: 4 seeds x 10^6-conversation WildChat-shaped traces (generated each step), "
-        "C in {64..4096} x xi in {4..40} x {LRU, T-LRU} = 384 instances")
+        return config5_rows(n, threshold_lru=True), n, (
+            "config5 sweep with the paper's three policies: 10 seeds x 10^6-conversation traces x 25 capacities x "
+            "20 xi x {LRU, T-LRU, Threshold-LRU (1024 tokens = 8 blocks)} = 1.5x10^4 instances")
+    if name == "config4":
+        rows = [(t, pol, C, xi, Q_HAT, SLO_BLOCKS) for t in range(4) for pol in (0, 1) for C in CAPS_CONFIG4
+                for xi in XI_BLOCKS]
+        return rows, 4, ("config4: 4 seeds x 10^6-conversation traces, C in {64..4096} x xi in {4..40} x "
+                         "{LRU, T-LRU} = 384 instances")
+    return config5_rows(n), n, (
+        "config5 sweep (BASELINE configs[4]): 10 seeds x 10^6-conversation WildChat-shaped traces (generated each "
+        "step) x 25 capacities (16..4096 blocks, geometric) x 20 xi (2..40 blocks) x {LRU, T-LRU} = 10^4 instances")
 
 
 def run_ours(args, rank, world, local_rank):
@@ -222,38 +261,23 @@ def run_ours(args, rank, world, local_rank):
     import paper_2510_15152_b200.tlru as T
     from paper_2510_15152_b200 import _abi
     from paper_2510_15152_b200.inputs import preset
+    from paper_2510_15152_b200.sweep import Sweep, gather_results, shard_cost
 
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
     stream = torch.cuda.current_stream()
-    seeds, rows, wl_desc = workload(args.config, rank)
-    params = [preset("wildchat", s, args.conversations) for s in seeds]
-    if any(r[1] == T.POLICY_ET_LRU for r in rows):  # ET-LRU model: belief decay per µs tick, prompt law
+    rows_all, n_traces, wl_desc = workload_global(args.config)
+    n_total = len(rows_all)
+    strong = args.scaling == "strong"
+    if any(r[1] == T.POLICY_ET_LRU for r in rows_all):  # ET-LRU model: belief decay per µs tick, prompt law
         from paper_2510_15152_b200.inputs import WILDCHAT, prompt_law_ln_surv
-        T.set_etlru_model(params[0]["death_rate"] * 1e-6, prompt_law_ln_surv(WILDCHAT))
+        T.set_etlru_model(WILDCHAT["death_rate"] * 1e-6, prompt_law_ln_surv(WILDCHAT))
 
-    # ---- setup (untimed): traces at their exact size, one batch per trace, workspaces, streams
-    traces = T.generate_traces(params, device=dev, exports=True)
-    nt = len(traces)
-    trace_rows = [[(0,) + tuple(r[1:]) for r in rows if r[0] == t] for t in range(nt)]
-    assert [r[0] for r in rows] == sorted(r[0] for r in rows)  # rows are trace-major
-    batches = [T.prepare_batch([traces[t]], trace_rows[t]) for t in range(nt)]
-    ni = len(rows)
-    E_tot = sum(traces[r[0]].num_events for r in rows)
-    results_all = torch.empty(ni * _abi.RESULT_DTYPE.itemsize, dtype=torch.uint8, device=dev)
-    slices, o = [], 0
-    for bt in batches:
-        n = bt.ni * _abi.RESULT_DTYPE.itemsize
-        slices.append(slice(o, o + n))
-        o += n
-    gstructs = [T._gen_struct(p) for p in params]
-    gws = []
-    for g, tr in zip(gstructs, traces):
-        sz = ctypes.c_size_t()
-        _abi.check(_abi.lib.tlru_gen_workspace_size(ctypes.byref(g), tr.sim.numel(), ctypes.byref(sz)))
-        gws.append(torch.empty(max(sz.value, 1), dtype=torch.uint8, device=dev))
-    tstructs = [tr.struct() for tr in traces]
-    gathered = torch.empty(world * results_all.numel(), dtype=torch.uint8, device=dev) if world > 1 else None
+    # ---- setup (untimed): this rank's traces at their exact size, one batch per trace, pools
+    sw = Sweep(rows_all, world, rank, lambda seed: preset("wildchat", seed, args.conversations), dev,
+               scaling=args.scaling, backend="nccl")
+    shards, traces, batches, ids_by_trace = sw.shards, sw.traces, sw.batches, sw.ids_by_trace
+    E_loc, RS, HB, npool = sw.requests_local, sw.RS, sw.HB, sw.npool
     # generation (compute-bound) on a higher-priority stream: its CTAs take SM slots as the
     # memory-bound simulation kernels' CTAs retire
     prio = int(os.environ.get("BENCH_GEN_PRIO", "-1"))
@@ -261,53 +285,26 @@ def run_ours(args, rank, world, local_rank):
     nsim = int(os.environ.get("BENCH_SIM_STREAMS", "2"))
     sBs = [torch.cuda.Stream(device=dev) for _ in range(nsim)]
 
-    def gen_one(t, st):  # a1-a3: K1 re-generates trace t in place (host waits on `st` only)
-        _abi.check(_abi.lib.tlru_generate_traces(ctypes.byref(gstructs[t]), 1, ctypes.byref(tstructs[t]),
-                                                 T._ptr(gws[t]), gws[t].numel(), T._stream(st)))
-
-    def gather():  # a10: NCCL all_gather of the per-instance results
-        if world > 1:
-            dist.all_gather_into_tensor(gathered, results_all)
+    def step():
+        sw.step(stream, sA, sBs)
 
     def step_seq():
-        """One stream, no overlap; returns the summed engine / K3 device times of the step."""
-        for t in range(nt):
-            gen_one(t, stream)
+        """One stream, no overlap; returns the summed engine / K3 / s2_out device times of the step."""
+        with torch.cuda.stream(stream):
+            sw.pooled.zero_()
+        for j in range(len(batches)):
+            sw.gen(j, stream)
         k2 = k3 = out_ms = 0.0
         out_n = 0
-        for t, bt in enumerate(batches):
-            bt.run(stream)  # a4-a9: simulation engine + K3
+        for j in range(len(batches)):
+            sw.simulate(j, stream)  # a4-a9: simulation engine + K3, results, pooling
             st = T.last_sim_stats()
             k2 += st["k2_ms"]
             k3 += st["k3_ms"]
             out_ms += st["out_ms"]
             out_n += st["out_launches"]
-            results_all[slices[t]].copy_(bt.results)
-        gather()
+        sw.combine(stream)
         return k2, k3, out_ms, out_n
-
-    def step():
-        """Pipelined: trace t+1 is generated on stream A while traces are simulated on the
-        simulation streams (alternating, so one trace's compute-bound phase overlaps the
-        previous trace's memory-bound output phase; every batch has its own workspace)."""
-        ev0 = torch.cuda.Event()
-        ev0.record(stream)
-        sA.wait_event(ev0)
-        for sB in sBs:
-            sB.wait_event(ev0)
-        for t, bt in enumerate(batches):
-            sB = sBs[t % len(sBs)]
-            gen_one(t, sA)
-            ev = torch.cuda.Event()
-            ev.record(sA)
-            sB.wait_event(ev)
-            bt.run(sB)
-            with torch.cuda.stream(sB):
-                results_all[slices[t]].copy_(bt.results)
-        stream.wait_stream(sA)
-        for sB in sBs:
-            stream.wait_stream(sB)
-        gather()
 
     def barrier():
         if world > 1:
@@ -342,33 +339,50 @@ def run_ours(args, rank, world, local_rank):
     main["out_n"] = seq["out"][-1][3]
     stats = T.last_sim_stats()
     assert stats["failed_chains"] == 0
-    res = results_all.cpu().numpy().view(_abi.RESULT_DTYPE)
-    assert np.all(res["requests"][:ni] > 0)
+    tab = sw.table.cpu().numpy().tobytes()
+    ptails = sw.pooled_tails_numpy()
     step()
     torch.cuda.synchronize()
-    assert results_all.cpu().numpy().tobytes() == res.tobytes()  # pipelined == sequential, byte for byte
+    assert sw.table.cpu().numpy().tobytes() == tab  # pipelined == sequential, byte for byte
+    res = np.frombuffer(tab, dtype=_abi.RESULT_DTYPE)
+    if strong or world == 1:
+        assert np.all(res["requests"] > 0)
+        # the pooled histograms hold every request of their pool's instances (all ranks reduced)
+        preq = np.zeros(npool, np.uint64)
+        np.add.at(preq, [sw.pidx[tuple(r[1:])] for r in sw.rows], res["requests"])
+        assert np.array_equal(ptails["n"], preq)
+    if world > 1 and strong:  # the host-side gather (duplicate / missing detection) agrees with the device one
+        loc = sw.results_local.view(-1, RS)[: len(sw.local_ids)].cpu().numpy().copy().view(_abi.RESULT_DTYPE)
+        host_table = gather_results(loc, sw.local_ids, n_total, device=dev)
+        if rank == 0:
+            assert host_table.tobytes() == tab
 
-    # ---- replay engine (Alg. 1 request by request) on seed 0's instances; must give identical bytes
+    # ---- replay engine (Alg. 1 request by request) on the first local trace: identical b bytes
     rep = None
-    if not args.no_replay and stats["engine"] == 1:  # replay workloads already ran on the replay engine
-        sub = trace_rows[0]
+    if not args.no_replay and stats["engine"] == T.ENGINE_STACK and batches:
+        sub = [(0,) + tuple(rows_all[i][1:]) for i in ids_by_trace[0]]
         if args.replay_instances:
             sub = sub[:args.replay_instances]
-        rbatch = T.prepare_batch(traces[:1], sub)
+        rbatch = T.prepare_batch(traces[:1], sub, hist_bins=HB)
+        rbatch.uncached.zero_()
         T.set_sim_engine(T.ENGINE_REPLAY)
         r = timed(lambda: (rbatch.run(), T.last_sim_stats()["k2_ms"])[1], 1, 1)
         rst = T.last_sim_stats()
         T.set_sim_engine(T.ENGINE_STACK)
-        assert rbatch.results_numpy().tobytes() == res[:len(sub)].tobytes(), "engines disagree"
+        nb = int(rbatch.offsets[len(sub) - 1]) + traces[0].num_events
+        assert rbatch.results_numpy()[: len(sub)].tobytes() == \
+            batches[0].results_numpy()[: len(sub)].tobytes(), "engines disagree (results)"
+        assert torch.equal(rbatch.uncached[:nb], batches[0].uncached[:nb]), "engines disagree (b bytes)"
+        assert torch.equal(rbatch.hist[: len(sub) * HB], batches[0].hist[: len(sub) * HB]), "engines disagree (hist)"
         rep = dict(r, k2=statistics.mean(r["out"]), requests=traces[0].num_events * len(sub), instances=len(sub),
                    stats=rst)
         del rbatch
 
-    # ---- e2e: same batches through the public API from pinned host buffers (H2D on stream A,
-    # upload + simulation on stream B, pipelined across traces), results read back to the host
-    host_turns = []
-    need_ticks = any(r[1] == T.POLICY_ET_LRU for r in rows)  # ET-LRU beliefs read the event times
-    host_ticks = []
+    # ---- e2e: the same step through the public API from pinned host buffers (H2D of each trace's
+    # turns on stream A, upload + simulation + pooling on the simulation streams, the collectives),
+    # the result table and the pooled metrics read back to the host
+    need_ticks = any(r[1] == T.POLICY_ET_LRU for r in rows_all)  # ET-LRU beliefs read the event times
+    host_turns, host_ticks = [], []
     for tr in traces:
         E = tr.num_events
         host_turns.append((tr.conv[:E].cpu().pin_memory(), tr.prompt[:E].view(torch.int16).cpu().pin_memory(),
@@ -376,95 +390,114 @@ def run_ours(args, rank, world, local_rank):
         host_ticks.append(tr.time_ticks[:E].cpu().pin_memory() if need_ticks else None)
     dev_turns = [(torch.empty_like(c, device=dev), torch.empty_like(q, device=dev), torch.empty_like(a, device=dev))
                  for c, q, a in host_turns]
+    dev_ticks = [torch.empty_like(h, device=dev) if h is not None else None for h in host_ticks]
     up_ws = []
     for tr in traces:
         sz = ctypes.c_size_t()
         _abi.check(_abi.lib.tlru_upload_workspace_size(tr.num_events, ctypes.byref(sz)))
         up_ws.append(torch.empty(max(sz.value, 1), dtype=torch.uint8, device=dev))
-    host_results = torch.empty(results_all.numel(), dtype=torch.uint8).pin_memory()
+    host_table = torch.empty(sw.table.numel(), dtype=torch.uint8).pin_memory()
+    host_ptails = torch.empty(sw.pooled_tails.numel(), dtype=torch.uint8).pin_memory()
     h2d_bytes = sum(c.numel() * 4 + q.numel() * 2 + a.numel() * 2 for c, q, a in host_turns)
     h2d_bytes += sum(h.numel() * 8 for h in host_ticks if h is not None)
-    d2h_bytes = host_results.numel()
+    d2h_bytes = host_table.numel() + host_ptails.numel()
 
     def e2e_step():
+        with torch.cuda.stream(stream):
+            sw.pooled.zero_()
         ev0 = torch.cuda.Event()
         ev0.record(stream)
         sA.wait_event(ev0)
         for sB in sBs:
             sB.wait_event(ev0)
-        for t, ((hc, hq, ha), (dc, dq, da), tr, ts, w, bt) in enumerate(
-                zip(host_turns, dev_turns, traces, tstructs, up_ws, batches)):
-            sB = sBs[t % len(sBs)]
+        for j, ((hc, hq, ha), (dc, dq, da), tr, ts, w) in enumerate(
+                zip(host_turns, dev_turns, traces, sw.tstructs, up_ws)):
+            sB = sBs[j % len(sBs)]
             with torch.cuda.stream(sA):
                 dc.copy_(hc, non_blocking=True)
                 dq.copy_(hq, non_blocking=True)
                 da.copy_(ha, non_blocking=True)
+                if dev_ticks[j] is not None:
+                    dev_ticks[j].copy_(host_ticks[j], non_blocking=True)
             ev = torch.cuda.Event()
             ev.record(sA)
             sB.wait_event(ev)
-            _abi.check(_abi.lib.tlru_trace_from_turns(T._ptr(dc), T._ptr(dq), T._ptr(da), tr.num_events,
-                                                      ctypes.byref(ts), T._ptr(w), w.numel(), T._stream(sB)))
-            if host_ticks[t] is not None:  # the upload numbers events; ET-LRU needs the real times
-                with torch.cuda.stream(sB):
-                    tr.time_ticks[:tr.num_events].copy_(host_ticks[t], non_blocking=True)
-            bt.run(sB)
-            with torch.cuda.stream(sB):
-                results_all[slices[t]].copy_(bt.results)
+            _abi.check(_abi.lib.tlru_trace_from_turns(T._ptr(dc), T._ptr(dq), T._ptr(da), T._ptr(dev_ticks[j]),
+                                                      tr.num_events, ctypes.byref(ts), T._ptr(w), w.numel(),
+                                                      T._stream(sB)))
+            sw.simulate(j, sB)
         stream.wait_stream(sA)
         for sB in sBs:
             stream.wait_stream(sB)
-        host_results.copy_(results_all, non_blocking=True)
+        sw.combine(stream)
+        host_table.copy_(sw.table, non_blocking=True)
+        host_ptails.copy_(sw.pooled_tails, non_blocking=True)
         stream.synchronize()
 
     e2e = timed(e2e_step, args.steps, max(1, min(args.warmup, 2)))
-    assert host_results.numpy().tobytes() == res.tobytes()
+    assert host_table.numpy().tobytes() == tab
 
-    # ---- max over ranks
+    # ---- max over ranks; exact request totals over ranks
     loc = torch.tensor([main["ms"], e2e["ms"], main["k2"], main["k3"], rep["ms"] if rep else 0.0,
                         rep["k2"] if rep else 0.0, seq["ms"], main["out_ms"]], dtype=torch.float64, device=dev)
+    req = torch.tensor([float(E_loc)], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(loc, op=dist.ReduceOp.MAX)
+        dist.all_reduce(req)
     ms, e2e_ms, k2, k3, rep_ms, rep_k2, seq_ms, out_ms = [float(x) for x in loc.tolist()]
+    req_all = int(req.item())
     if rank != 0:
         return
-    req_all = E_tot * world
     value = req_all / (ms / 1000.0)
     peak, peak_src = peaks()
+    # dominant kernel s2_out (rank 0's launches): the irreducible HBM traffic is the 2-byte b it
+    # writes per request; its per-event inputs (4 B L_before|J + 2 B A_nf per D) are listed beside
+    out_n = max(int(main["out_n"]), 1)
     nd_per_trace = {}
-    for r in rows:
-        D = (r[3] - r[4]) if (r[1] == 1 and r[3] > r[4]) else 0
-        Tk = r[6] if (r[1] == 2 and len(r) > 6) else 0  # Threshold-LRU rows: (D = 0, T)
-        nd_per_trace.setdefault(r[0], set()).add((D, Tk))
-    ev_tot = sum(traces[t].num_events for t in nd_per_trace)
-    ev_rows = sum(traces[t].num_events * len(v) for t, v in nd_per_trace.items())  # (event, D) pairs
-    # dominant kernel s2_out: writes b (2 B/request) and reads, once per event, the packed
-    # (L_before | J) word and one 2-byte A_nf per (event, D)
-    out_bytes = OUT_B_BYTES * E_tot + OUT_EVENT_BYTES * ev_tot + OUT_ROW_BYTES * ev_rows
-    out_n = max(int(main["out_n"]), 1)  # s2_out launches per step (one per trace here)
-    achieved = (out_bytes / out_n) / (out_ms / out_n / 1000.0) / 1e9 if out_ms > 0 else None
-    # whole engine (all simulation kernels of the step, sequential stream)
-    eng_bytes = STACK_B_BYTES * E_tot + STACK_PASS_BYTES_PER_EVENT * ev_tot
+    for j, ids in enumerate(ids_by_trace):
+        for i in ids:
+            r = rows_all[i]
+            D = (r[3] - r[4]) if (r[1] == 1 and r[3] > r[4]) else 0
+            Tk = r[6] if (r[1] == 2 and len(r) > 6) else 0  # Threshold-LRU rows: (D = 0, T)
+            nd_per_trace.setdefault(j, set()).add((D, Tk))
+    ev_tot = sum(traces[j].num_events for j in nd_per_trace)
+    ev_rows = sum(traces[j].num_events * len(v) for j, v in nd_per_trace.items())
+    b_bytes = OUT_B_BYTES * E_loc
+    in_bytes = OUT_EVENT_BYTES * ev_tot + OUT_ROW_BYTES * ev_rows
+    achieved = (b_bytes / out_n) / (out_ms / out_n / 1000.0) / 1e9 if out_ms > 0 else None
+    achieved_in = ((b_bytes + in_bytes) / out_n) / (out_ms / out_n / 1000.0) / 1e9 if out_ms > 0 else None
+    step_achieved = b_bytes / (ms / 1000.0) / 1e9  # rank 0's b bytes over the (max-over-ranks) step
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
         t = json.load(open(tpath))
         if "s2_out_dram_bytes_per_request" in t:
-            traffic = float(t["s2_out_dram_bytes_per_request"]) * E_tot / out_n
+            traffic = float(t["s2_out_dram_bytes_per_request"]) * E_loc / out_n
+    shard_info = {"instances": [len(s_) for s_ in shards], "traces": [len({int(rows_all[i][0]) for i in s_})
+                                                                       for s_ in shards],
+                  "modelled_ms": [round(shard_cost(rows_all, s_), 3) for s_ in shards]} if strong else None
     line = {
         "metric": "simulated requests/sec", "value": value, "unit": "requests/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "u32", "data": "synthetic",
         "config": {
-            "workload": wl_desc, "instances_per_gpu": ni, "requests_per_gpu_step": E_tot,
-            "conversations": args.conversations,
-            "parallelism": f"dp{world} (instances sharded by seed, NCCL all_gather of results)",
-            "l2": f"inputs larger than L2: {2 * E_tot / 1e9:.1f} GB of b written per GPU-step",
+            "workload": wl_desc, "instances": n_total if strong else n_total * world,
+            "requests_per_step": req_all, "conversations": args.conversations,
+            "parallelism": (f"dp{world}: the sweep's instances sharded over {world} GPU(s) at sub-trace granularity "
+                            "(sweep.plan_strong; each rank regenerates its traces), NCCL all_gather of the results "
+                            "+ all_reduce of the pooled histograms" if strong else
+                            f"dp{world}: every rank runs the whole sweep on its own seeds; NCCL all_gather / "
+                            "all_reduce as in strong mode"),
+            "shards": shard_info,
+            "l2": f"inputs larger than L2: {2 * E_loc / 1e9:.1f} GB of b written per GPU-step (rank 0)",
             "engine": ("stack (closed form of Alg. 1 from the stack property, all capacities of a trace per pass; "
                        "bit-identical to the replay engine and the oracle); no dedup of identical instances")
-            if stats["engine"] == 1 else
-            "replay (Alg. 1 / Thm 1 request by request, one lane per instance; End-/Length-Aware and "
-            "Tail-Optimized Belady: burn-in segments verified by the fix-up)",
+            if stats["engine"] == T.ENGINE_STACK else
+            "replay (Alg. 1 / Thm 1 request by request; aware / Belady / forced / ET-LRU: burn-in segments verified "
+            "by the fix-up)" if stats["engine"] == T.ENGINE_REPLAY else "mixed (stack + replay engines)",
             "engine_ms": k2, "k3_ms": k3, "sequential_ms_per_step": seq_ms,
+            "pooled": {"pools": npool, "bins": HB, "what": "per (policy, C, xi) over seeds: u64 b-histograms "
+                       "summed per GPU (tlru_pool_histograms), all_reduce over GPUs, tlru_tail_from_histograms"},
             "pipelining": "traces generated on a high-priority stream A while earlier traces are simulated on "
                           "two alternating streams; engine_ms / k3_ms / roofline.launch_ms from the sequential "
                           "(single-stream) step",
@@ -475,26 +508,29 @@ def run_ours(args, rank, world, local_rank):
                      "frac": achieved / peak if achieved else None, "traffic": traffic,
                      "kernel": "s2_out_kernel (b output + per-group histograms), per launch",
                      "launch_ms": out_ms / out_n, "launches_per_step": out_n,
-                     "algorithmic_bytes_per_launch": out_bytes / out_n,
-                     "algorithmic_bytes": f"{OUT_B_BYTES} B/request (b written) + {OUT_EVENT_BYTES} B/event + "
-                                          f"{OUT_ROW_BYTES} B/(event, D) read",
+                     "algorithmic_bytes_per_launch": b_bytes / out_n,
+                     "algorithmic_bytes": f"{OUT_B_BYTES} B/request: the b row written (irreducible output)",
+                     "with_inputs": {"achieved": achieved_in, "frac": achieved_in / peak if achieved_in else None,
+                                     "bytes": f"+ {OUT_EVENT_BYTES} B/event + {OUT_ROW_BYTES} B/(event, D) read"},
+                     "step_frac": step_achieved / peak, "step_achieved": step_achieved,
+                     "step_note": "the 2 B/request b write over the whole pipelined step (generation, window "
+                                  "sums, s2_out, pooling, collectives)",
                      "peak_source": peak_src,
-                     "engine": {"achieved": eng_bytes / (k2 / 1000.0) / 1e9,
-                                "frac": eng_bytes / (k2 / 1000.0) / 1e9 / peak, "ms": k2,
-                                "algorithmic_bytes": f"{STACK_B_BYTES} B/request + "
-                                                     f"{STACK_PASS_BYTES_PER_EVENT} B/event"},
-                     "survey_model_frac": ALGO_BYTES_PER_REQUEST * E_tot / (k2 / 1000.0) / 1e9 / peak},
+                     "survey_model_10B": {"frac": ALGO_BYTES_PER_REQUEST * E_loc / (k2 / 1000.0) / 1e9 / peak,
+                                          "note": "SURVEY 8(d)'s 8 B event read + 2 B write per request is the "
+                                                  "replay engine's model; the stack engine reads per-event inputs "
+                                                  "once per instance group, never per request, so this figure "
+                                                  "exceeds 1 and does not apply"}},
         "gpu_launches": int(main["launches"] // max(args.steps, 1)),
         "clocks": main["clocks"],
     }
-    if stats["engine"] != 1:
-        # replay-engine workload (End-/Length-Aware, Belady): the dominant kernels are K2's (sim_kernel
-        # + fix-up), SURVEY 8(d)'s model: one 8-byte event read + one 2-byte b write per request
-        ach = ALGO_BYTES_PER_REQUEST * E_tot / (k2 / 1000.0) / 1e9
+    if stats["engine"] != T.ENGINE_STACK:
+        # replay-engine workload: the dominant kernels are K2's (sim_kernel + fix-up), SURVEY 8(d)'s model
+        ach = ALGO_BYTES_PER_REQUEST * E_loc / (k2 / 1000.0) / 1e9
         line["roofline"] = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
-                            "traffic": None, "kernel": "sim_kernel<W, AWARE> + aware_fix_kernel (K2 replay), "
+                            "traffic": None, "kernel": "sim_kernel<W, AWARE> + fix-up / etlru_seg_kernel (K2 replay), "
                                                        "per step (sequential stream)",
-                            "launch_ms": k2, "algorithmic_bytes_per_launch": ALGO_BYTES_PER_REQUEST * E_tot,
+                            "launch_ms": k2, "algorithmic_bytes_per_launch": ALGO_BYTES_PER_REQUEST * E_loc,
                             "algorithmic_bytes": f"{ALGO_BYTES_PER_REQUEST} B/request (8 B event read + 2 B b "
                                                  "written)", "peak_source": peak_src,
                             "note": "issue/shared-memory-latency bound state machine, not HBM (DESIGN.md 6)"}
@@ -506,12 +542,10 @@ def run_ours(args, rank, world, local_rank):
             "segment_events": rep["stats"]["segment_events"], "spilled_chains": rep["stats"]["spilled_chains"],
             "roofline": {"bound": "hbm", "achieved": rep_achieved, "peak": peak, "unit": "GB/s",
                          "frac": rep_achieved / peak, "kernel": "sim_kernel<W> (K2 replay)"},
-            "note": "Alg. 1 replayed request by request (one lane per instance) on seed 0's instances; "
-                    "result bytes identical to the stack engine"}
+            "note": "Alg. 1 replayed request by request (one lane per instance) on the first trace's instances; "
+                    "b bytes, histograms and results identical to the stack engine"}
     if not args.no_cpu_baseline and world == 1:  # the CPU oracle baseline: rank 0 at N = 1 only
-        n, dt, cores, sample = cpu_oracle_sample(seed=0, n_conv=args.conversations)
-        line["cpu_baseline"] = {"value": n / dt, "unit": "requests/s", "cores": cores, "kind": "oracle",
-                                "sample": sample}
+        line["cpu_baseline"] = cpu_oracle_baseline(args.conversations)
     print(json.dumps(line), flush=True)
 
 
@@ -525,7 +559,10 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-replay", action="store_true", help="skip timing the replay engine")
     ap.add_argument("--replay-instances", type=int, default=0, help="limit the replay-engine sample (0 = all of seed 0)")
-    ap.add_argument("--config", choices=("config5", "config5x3", "spectrum", "etlru", "forced", "config4"), default="config5")
+    ap.add_argument("--config", choices=("config5", "config5x3", "spectrum", "etlru", "forced", "config4"),
+                    default="config5")
+    ap.add_argument("--scaling", choices=("strong", "weak"), default="strong",
+                    help="strong: the one sweep sharded over the ranks (default); weak: every rank its own seeds")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

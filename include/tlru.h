@@ -67,9 +67,11 @@ uint64_t tlru_launch_count(void);
  *   - a turn whose history would exceed max_history_blocks ends the
  *     conversation (context window), as does max_turns.
  * App. E's recipe is the ShareGPT preset.  Random numbers come from
- * Philox4x64-10 keyed by (seed, tag) with counter (conv, turn, field|attempt<<8, 0),
- * so a trace is a pure function of its parameters (Reading #16).  Time is kept
- * in integer microsecond ticks; events are ordered by (tick, conv, turn).
+ * Philox4x64-10 keyed by the seed with counter (conv, turn, attempt, 0): attempt 0
+ * of a turn gives the gap before it (turn 0: the birth gap), the first Marsaglia
+ * polar pair and (turn 0) the death clock; a rejected pair retries with attempt
+ * 1, 2, ...; so a trace is a pure function of its parameters (Reading #16).  Time
+ * is kept in integer microsecond ticks; events are ordered by (tick, conv, turn).
  * ------------------------------------------------------------------------ */
 typedef struct {
   uint64_t seed;
@@ -97,6 +99,10 @@ typedef struct {
   uint64_t num_events;  /* out: E */
   uint32_t max_history; /* out: max over events of L_after (bounds every J and every b) */
   uint32_t num_conversations; /* out: number of distinct conversation ids */
+  uint64_t universe_blocks;   /* out: sum over conversations of their final L_after (the "universe" of
+                                 the stack engine's window sums) */
+  uint32_t flags;             /* out: TLRU_TRACE_* bits below */
+  uint32_t reserved;
   uint64_t* sim;        /* [E] required.  Simulation view, 8 B per request:
                              bits  0..31 prev = event index of the same conversation's previous
                                          turn, or TLRU_NONE for a first turn
@@ -107,9 +113,15 @@ typedef struct {
   uint32_t* conv;       /* [E] nullable export: conversation id (dense, birth order for generated traces) */
   uint16_t* prompt;     /* [E] nullable export: q blocks >= 1 */
   uint16_t* response;   /* [E] nullable export: a blocks >= 0 */
-  uint64_t* time_ticks; /* [E] nullable export: arrival time in microseconds (generated traces) */
+  uint64_t* time_ticks; /* [E] nullable export: arrival time in microseconds (generated traces; the
+                             caller's ticks on upload, else event indices and TLRU_TRACE_SYNTHETIC_TICKS) */
   uint8_t* is_last;     /* [E] nullable export: 1 on a conversation's last turn */
 } tlru_trace;
+
+/* tlru_trace.flags: time_ticks holds event indices, not arrival times (an upload without
+ * ticks).  ET-LRU's beliefs decay with time, so ET-LRU instances on such a trace are
+ * TLRU_EINVAL. */
+#define TLRU_TRACE_SYNTHETIC_TICKS 1u
 
 /* Host: upper bound N * max_turns on the events of a generated trace. */
 tlru_status tlru_trace_max_events(const tlru_gen_params* p /*host*/, uint64_t* out /*host*/);
@@ -135,11 +147,16 @@ tlru_status tlru_upload_workspace_size(uint64_t E, size_t* bytes /*host*/);
 
 /* Build the simulation view of an uploaded trace.  conv/q/a are DEVICE arrays
  * in event (time) order; conversation ids are arbitrary u32 except TLRU_NONE.
- * The library derives prev, next, J = L_before + q and L_after = J + a
- * and fills out->sim / out->next, copying the non-NULL export arrays.
- * q == 0 -> TLRU_EINVAL; J or L_after > 65535 -> TLRU_ERANGE (offending event index
- * in tlru_last_error()).  E == 0 is valid.  Synchronizes `stream`. */
-tlru_status tlru_trace_from_turns(const uint32_t* conv, const uint16_t* q, const uint16_t* a, uint64_t E,
+ * ticks (DEVICE u64[E], nullable) are the arrival times, non-decreasing, in the unit
+ * ET-LRU's mu_per_tick uses; they are copied to out->time_ticks.  Without ticks,
+ * out->time_ticks (if non-NULL) receives event indices and out->flags gets
+ * TLRU_TRACE_SYNTHETIC_TICKS.  The library derives prev, next, J = L_before + q and
+ * L_after = J + a and fills out->sim / out->next, copying the non-NULL
+ * export arrays, and out->max_history, num_conversations, universe_blocks, flags.
+ * q == 0 or decreasing ticks -> TLRU_EINVAL; J or L_after > 65535 -> TLRU_ERANGE
+ * (offending event index in tlru_last_error()).  E == 0 is valid.  Synchronizes `stream`. */
+tlru_status tlru_trace_from_turns(const uint32_t* conv, const uint16_t* q, const uint16_t* a,
+                                  const uint64_t* ticks, uint64_t E,
                                   tlru_trace* out /*host struct, device arrays*/, void* ws,
                                   size_t ws_bytes, cudaStream_t stream);
 
@@ -164,8 +181,11 @@ tlru_status tlru_trace_from_turns(const uint32_t* conv, const uint16_t* q, const
  *   conversation releases theta's blocks (not counted as evictions) and caches
  *   nothing; Length-Aware budgets each cached history with the true next prompt,
  *   surplus = min(L_after, max(xi - q_next, 0)).  Their cache is not the top-C of
- *   the universe, so they always run on the replay engine as whole-trace chains;
- *   a batch that contains them runs entirely on the replay engine.
+ *   the universe, so they always run on the replay engine, as time segments that
+ *   start with a burn-in from an empty cache and are verified against their
+ *   predecessor's end state (a fix-up kernel re-runs any segment whose start state
+ *   was not exact).  In a batch that also holds LRU / T-LRU / Threshold-LRU
+ *   instances, those still run on the stack engine (stats.engine = MIXED).
  * Tail-Optimized Belady (Thm 1; proof App. A; Reading
  *   #26): the hindsight policy, clairvoyant through the trace's next links.
  *   theta caches its whole history; on overflow Phase 1 trims blocks above the
@@ -226,17 +246,40 @@ tlru_status tlru_sim_workspace_size(const tlru_trace* traces /*host[nt]*/, uint3
                                     size_t* bytes /*host*/);
 
 /* Simulate ni instances.  inst is a HOST array (the launch planner groups
- * instances by trace and capacity class).  uncached (device, u16) receives
- * instance i's per-request b at uncached[offsets[i] .. offsets[i] + E_i);
+ * instances by trace, engine and capacity class on the host).  uncached (device,
+ * u16) receives instance i's per-request b at uncached[offsets[i] .. offsets[i] + E_i);
  * offsets is a host array, or NULL for packed offsets (prefix sums of E_i).
  * results (device[ni]) receives one tlru_result per instance.
- * Unknown policy -> TLRU_EUNSUPPORTED; trace index out of range -> TLRU_EINVAL.
- * Does not synchronize unless a chain overflows its on-chip state, in which case
- * the library re-runs that chain from global memory (counted, never truncated). */
+ * Engine per instance: LRU / T-LRU / Threshold-LRU instances run on the engine
+ * tlru_set_sim_engine selects (stack by default) -- except on a trace whose
+ * universe_blocks >= 2^32 - 2^16 (the stack engine's 32-bit window sums), which runs
+ * on the replay engine; every other policy runs on the replay engine.  A batch
+ * that needs both engines runs both, each on its own instances (stats.engine =
+ * TLRU_ENGINE_MIXED); the outputs are identical either way.
+ * Unknown policy -> TLRU_EUNSUPPORTED; trace index out of range -> TLRU_EINVAL;
+ * ET-LRU on a trace without real ticks (TLRU_TRACE_SYNTHETIC_TICKS) -> TLRU_EINVAL.
+ * Does not synchronize.  A replay chain that outgrows its on-chip state is re-run
+ * from global memory (counted in spilled_chains, never truncated); one that
+ * outgrows even that is counted in failed_chains (its b rows are then invalid):
+ * callers that cannot rule this out poll tlru_last_sim_stats (the Python binding's
+ * simulate_batch does). */
 tlru_status tlru_simulate_batch(const tlru_trace* traces /*host[nt]*/, uint32_t nt,
                                 const tlru_instance* inst /*host[ni]*/, uint32_t ni, uint16_t* uncached,
                                 const uint64_t* offsets /*host[ni] or NULL*/, tlru_result* results, void* ws,
                                 size_t ws_bytes, cudaStream_t stream);
+
+/* tlru_simulate_batch that also exports each instance's histogram of b (the one
+ * the tail metrics of its tlru_result are computed from): hist (device,
+ * nullable) receives row i = #{requests of instance i with b = v} for v = 0 ..
+ * hist_bins - 1 at hist[i * hist_bins + v].  hist_bins must exceed every trace's
+ * max_history (b <= J <= L_after), else TLRU_ERANGE; bins above the batch's
+ * largest max_history are written as 0.  The workspace size is the same as
+ * tlru_simulate_batch's.  Row sums fit u32 because E < 2^32. */
+tlru_status tlru_simulate_batch_ex(const tlru_trace* traces /*host[nt]*/, uint32_t nt,
+                                   const tlru_instance* inst /*host[ni]*/, uint32_t ni, uint16_t* uncached,
+                                   const uint64_t* offsets /*host[ni] or NULL*/, tlru_result* results,
+                                   uint32_t* hist /*device[ni][hist_bins] or NULL*/, uint32_t hist_bins,
+                                   void* ws, size_t ws_bytes, cudaStream_t stream);
 
 /* Tuning / test knobs for tlru_simulate_batch on this thread (host; 0 = automatic).
  * segment_events: events per segment (rounded up to a multiple of 32; the cache
@@ -260,7 +303,7 @@ tlru_status tlru_set_etlru_model(double mu_per_tick, const double* ln_surv /*hos
  *   TLRU_ENGINE_STACK: closed form of Alg. 1 from the stack property:
  *     per (trace, D) window sums, every capacity of a trace in one pass; the
  *     eviction counters by telescoping.  Default. */
-enum { TLRU_ENGINE_REPLAY = 0, TLRU_ENGINE_STACK = 1 };
+enum { TLRU_ENGINE_REPLAY = 0, TLRU_ENGINE_STACK = 1, TLRU_ENGINE_MIXED = 2 /* stats only */ };
 tlru_status tlru_set_sim_engine(uint32_t engine);
 
 /* Statistics of the last tlru_simulate_batch on this thread.  Reads two device
@@ -276,8 +319,9 @@ typedef struct {
   uint32_t state_entries;   /* largest on-chip W used (replay engine) */
   uint32_t engine;          /* TLRU_ENGINE_* used */
   uint32_t reserved;
-  float k2_ms;              /* device time of the simulation kernels (K2 + spill, or the stack engine) */
-  float k3_ms;              /* device time of the tail-metric kernels (K3) */
+  float k2_ms;              /* device time of the simulation kernels (K2 + spill, or the stack engine;
+                               MIXED: both engines and their K3) */
+  float k3_ms;              /* device time of the tail-metric kernels (K3; 0 for MIXED) */
   float out_ms;             /* stack engine, fused path: device time from the first to the last
                                s2_out launch (b output + histograms, the dominant kernel); else 0 */
   uint32_t out_launches;    /* s2_out launches in that interval */
@@ -291,13 +335,16 @@ tlru_status tlru_last_sim_stats(tlru_sim_stats* out /*host*/);
  *   over b in ascending order, double); SLO = #{b > slo};
  *   p-th percentile: nearest rank k = max(1, ceil(p * n / 100)) on sorted b
  *   (integer arithmetic, p in {50, 90, 95, 99}; Reading #11); *_ms = alpha * b_(k).
- * An empty segment yields n = 0 and zero fields.  Values of b above max_b are
- * clamped to max_b and counted in n_clamped (max_b <= 65535).
+ * An empty segment yields n = 0 and zero fields.  max_b (<= 65535) bounds the
+ * histogram: a value of b above it makes the call return TLRU_ERANGE (the count
+ * of such values is in n_clamped of the affected segments, whose other fields are
+ * then unspecified) -- percentiles are never computed from truncated data.  For
+ * that check tlru_tail_metrics synchronizes `stream`.
  * ------------------------------------------------------------------------ */
 typedef struct {
   uint64_t n, tel_blocks, slo_violations, sum_b;
   uint32_t p50, p90, p95, p99;
-  uint32_t max_b, n_clamped;
+  uint32_t max_b, n_clamped; /* n_clamped: values above max_b (0 whenever the call returns TLRU_OK) */
   double tel_ms, p50_ms, p90_ms, p95_ms, p99_ms, mean_ms;
 } tlru_tail;
 
@@ -308,6 +355,34 @@ tlru_status tlru_tail_metrics(const uint16_t* b, const uint64_t* seg_offsets /*d
                               const uint32_t* slo /*device[ns]*/, double alpha_ms_per_block,
                               uint32_t max_b, tlru_tail* out /*device[ns]*/, void* ws, size_t ws_bytes,
                               cudaStream_t stream);
+
+/* ------------------------------------------------------------------------
+ * Pooled metrics (row a10; the paper reports percentiles of TTFT pooled over
+ * the requests of a configuration): histograms of b are summed per
+ * pool -- e.g. one pool per (C, xi, policy) over seeds -- on each GPU, summed
+ * across GPUs by the caller's collective (NCCL all_reduce of the u64 counts), and
+ * turned into tail metrics.  Sums of histograms are exact, so the pooled metrics
+ * equal tlru_tail_metrics over the concatenated b of the pool's instances.
+ * ------------------------------------------------------------------------ */
+
+/* Host: workspace bytes of tlru_pool_histograms for ni instances. */
+tlru_status tlru_pool_workspace_size(uint32_t ni, size_t* bytes /*host*/);
+
+/* pooled[pool[i] * bins + v] += hist[i * bins + v] for every instance i with
+ * pool[i] != TLRU_NONE (TLRU_NONE skips the instance).  pooled is accumulated into
+ * (zero it first).  pool[i] >= npool (other than TLRU_NONE) -> TLRU_EINVAL. */
+tlru_status tlru_pool_histograms(const uint32_t* hist /*device[ni][bins]*/, uint32_t ni, uint32_t bins,
+                                 const uint32_t* pool /*host[ni]*/, uint32_t npool,
+                                 uint64_t* pooled /*device[npool][bins]*/, void* ws, size_t ws_bytes,
+                                 cudaStream_t stream);
+
+/* Tail metrics of ns histograms (u64 counts, hist[s * bins + v] = #{b = v}) with the
+ * definitions of tlru_tail_metrics (xi, xi_ms, slo nullable: 0, 0.0, "no SLO").
+ * bins in 1..65536; n_clamped = 0.  No workspace; does not synchronize. */
+tlru_status tlru_tail_from_histograms(const uint64_t* hist /*device[ns][bins]*/, uint32_t ns, uint32_t bins,
+                                      const uint32_t* xi /*device[ns]*/, const double* xi_ms /*device[ns]*/,
+                                      const uint32_t* slo /*device[ns]*/, double alpha_ms_per_block,
+                                      tlru_tail* out /*device[ns]*/, cudaStream_t stream);
 
 #ifdef __cplusplus
 }

@@ -24,6 +24,8 @@ POLICY_ET_LRU = 6
 POLICY_TLRU_FORCED = 7
 ENGINE_REPLAY = 0
 ENGINE_STACK = 1
+ENGINE_MIXED = 2
+TRACE_SYNTHETIC_TICKS = 1
 
 STATUS = {0: "TLRU_OK", 1: "TLRU_EINVAL", 2: "TLRU_ERANGE", 3: "TLRU_ECUDA", 4: "TLRU_EUNSUPPORTED",
           5: "TLRU_ESTATE"}
@@ -62,6 +64,9 @@ class Trace(ctypes.Structure):
         ("num_events", ctypes.c_uint64),
         ("max_history", ctypes.c_uint32),
         ("num_conversations", ctypes.c_uint32),
+        ("universe_blocks", ctypes.c_uint64),
+        ("flags", ctypes.c_uint32),
+        ("reserved", ctypes.c_uint32),
         ("sim", ctypes.c_void_p),
         ("next", ctypes.c_void_p),
         ("conv", ctypes.c_void_p),
@@ -89,7 +94,9 @@ class SimStats(ctypes.Structure):
 EXPORTS = (
     "tlru_last_error", "tlru_version", "tlru_launch_count", "tlru_trace_max_events", "tlru_gen_workspace_size", "tlru_count_events",
     "tlru_generate_traces", "tlru_upload_workspace_size", "tlru_trace_from_turns", "tlru_sim_workspace_size",
-    "tlru_simulate_batch", "tlru_set_sim_options", "tlru_set_sim_engine", "tlru_set_etlru_model", "tlru_last_sim_stats", "tlru_tail_workspace_size", "tlru_tail_metrics",
+    "tlru_simulate_batch", "tlru_simulate_batch_ex", "tlru_set_sim_options", "tlru_set_sim_engine",
+    "tlru_set_etlru_model", "tlru_last_sim_stats", "tlru_tail_workspace_size", "tlru_tail_metrics",
+    "tlru_pool_workspace_size", "tlru_pool_histograms", "tlru_tail_from_histograms",
 )
 
 
@@ -109,15 +116,19 @@ def _load():
         "tlru_count_events": ([P(GenParams), P(u64), vp, sz, vp], st),
         "tlru_generate_traces": ([P(GenParams), u32, P(Trace), vp, sz, vp], st),
         "tlru_upload_workspace_size": ([u64, P(sz)], st),
-        "tlru_trace_from_turns": ([vp, vp, vp, u64, P(Trace), vp, sz, vp], st),
+        "tlru_trace_from_turns": ([vp, vp, vp, vp, u64, P(Trace), vp, sz, vp], st),
         "tlru_sim_workspace_size": ([P(Trace), u32, P(Instance), u32, P(sz)], st),
         "tlru_simulate_batch": ([P(Trace), u32, P(Instance), u32, vp, P(u64), vp, vp, sz, vp], st),
+        "tlru_simulate_batch_ex": ([P(Trace), u32, P(Instance), u32, vp, P(u64), vp, vp, u32, vp, sz, vp], st),
         "tlru_set_sim_options": ([u32, u32], st),
         "tlru_set_sim_engine": ([u32], st),
         "tlru_set_etlru_model": ([ctypes.c_double, P(ctypes.c_double), u32], st),
         "tlru_last_sim_stats": ([P(SimStats)], st),
         "tlru_tail_workspace_size": ([u32, u32, P(sz)], st),
         "tlru_tail_metrics": ([vp, vp, u32, vp, vp, vp, ctypes.c_double, u32, vp, vp, sz, vp], st),
+        "tlru_pool_workspace_size": ([u32, P(sz)], st),
+        "tlru_pool_histograms": ([vp, u32, u32, P(u32), u32, vp, vp, sz, vp], st),
+        "tlru_tail_from_histograms": ([vp, u32, u32, vp, vp, vp, ctypes.c_double, vp, vp], st),
     }
     for name, (args, res) in sigs.items():
         fn = getattr(L, name)

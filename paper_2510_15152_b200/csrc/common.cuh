@@ -97,6 +97,12 @@ __device__ __forceinline__ void warp_atomic_max_u32(uint32_t* dst, uint32_t v) {
   if ((threadIdx.x & 31) == 0 && v) atomicMax(dst, v);
 }
 
+__device__ __forceinline__ void warp_atomic_add_u64(unsigned long long* dst, unsigned long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+  if ((threadIdx.x & 31) == 0 && v) atomicAdd(dst, v);
+}
+
 __device__ __forceinline__ void warp_atomic_add_u32(uint32_t* dst, uint32_t v) {
   v = __reduce_add_sync(0xFFFFFFFFu, v);
   if ((threadIdx.x & 31) == 0 && v) atomicAdd(dst, v);

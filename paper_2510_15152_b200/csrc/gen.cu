@@ -143,8 +143,9 @@ __global__ void gen_draw_kernel(GenDev g, uint32_t E, const uint32_t* cid, const
 __global__ void gen_emit_kernel(GenDev g, const uint64_t* birth, const uint32_t* off, const uint64_t* gapt,
                                 const uint16_t* q16, const uint16_t* a16, uint64_t sentinel, uint64_t* key,
                                 uint32_t* val, uint16_t* J16, uint16_t* La16, uint8_t* last8, uint32_t* max_L,
-                                uint32_t* nconv, uint32_t* nvalid) {
+                                uint32_t* nconv, uint32_t* nvalid, unsigned long long* universe) {
   uint32_t maxL = 0, nc = 0, nv = 0;
+  unsigned long long U = 0;  // sum of final histories (the universe)
   for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < g.N; c += gridDim.x * blockDim.x) {
     const uint32_t b = off[c], n = off[c + 1] - b;
     uint64_t t = birth[c];
@@ -170,10 +171,12 @@ __global__ void gen_emit_kernel(GenDev g, const uint64_t* birth, const uint32_t*
     maxL = L > maxL ? L : maxL;
     nc += k > 0;
     nv += k;
+    U += L;
   }
   warp_atomic_max_u32(max_L, maxL);
   warp_atomic_add_u32(nconv, nc);
   warp_atomic_add_u32(nvalid, nv);
+  warp_atomic_add_u64(universe, U);
 }
 
 // ---- time order: bucket sort on the arrival tick (buckets of 2^sh ticks, ~2 events each),
@@ -301,6 +304,7 @@ struct GenWs {
   uint32_t* queue;   // [N] conversations needing an exact length replay in the count pass
   uint32_t* nqueue;
   uint32_t* nvalid;
+  unsigned long long* universe;
   uint16_t* turn;    // [E] turn index of each event slot
   uint64_t* gapt;    // [E] gap ticks to the previous turn
   uint64_t* key[2];
@@ -326,6 +330,7 @@ static tlru_status carve_gen(Carver& cv, uint32_t N, uint64_t cap, GenWs* w) {
   w->queue = cv.take<uint32_t>(N);
   w->nqueue = cv.take<uint32_t>(1);
   w->nvalid = cv.take<uint32_t>(1);
+  w->universe = cv.take<unsigned long long>(1);
   w->turn = cv.take<uint16_t>(cap);
   w->gapt = cv.take<uint64_t>(cap);
   for (int i = 0; i < 2; ++i) {
@@ -412,11 +417,12 @@ __global__ void up_weight_kernel(uint64_t E, const uint32_t* sval, const uint16_
 // In conversation-major order (stable, so time order within a conversation):
 // L_after = running sum of q + a, J = L_after - a, prev/next = neighbours.
 __global__ void up_link_kernel(uint64_t E, const uint32_t* skey, const uint32_t* sval, const uint32_t* cum,
-                               const uint16_t* a, uint64_t* sim, uint32_t* next, uint8_t* is_last,
-                               uint64_t* time_ticks, unsigned long long* bad_range, uint32_t* max_L,
-                               uint32_t* nconv) {
+                               const uint16_t* a, const uint64_t* ticks, uint64_t* sim, uint32_t* next,
+                               uint8_t* is_last, uint64_t* time_ticks, unsigned long long* bad_range,
+                               unsigned long long* bad_ticks, uint32_t* max_L, uint32_t* nconv,
+                               unsigned long long* universe) {
   uint32_t maxL = 0, nc = 0;
-  unsigned long long bad = ~0ull;
+  unsigned long long bad = ~0ull, badt = ~0ull, U = 0;
   for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < E; i += uint64_t(gridDim.x) * blockDim.x) {
     uint32_t e = sval[i];
     uint32_t La = cum[i];
@@ -429,13 +435,19 @@ __global__ void up_link_kernel(uint64_t E, const uint32_t* skey, const uint32_t*
     sim[e] = pack_sim(prev, J, La);
     next[e] = nx;
     if (is_last) is_last[e] = last ? 1 : 0;
-    if (time_ticks) time_ticks[e] = e;
+    if (time_ticks) time_ticks[e] = ticks ? ticks[e] : e;
+    if (ticks && e > 0 && ticks[e - 1] > ticks[e] && e < badt) badt = e;
     nc += first;
-    if (last) maxL = max(maxL, La > 65535u ? 65535u : La);
+    if (last) {
+      maxL = max(maxL, La > 65535u ? 65535u : La);
+      U += La;
+    }
   }
   warp_atomic_max_u32(max_L, maxL);
   warp_atomic_add_u32(nconv, nc);
+  warp_atomic_add_u64(universe, U);
   if (bad != ~0ull) atomicMin(bad_range, bad);
+  if (badt != ~0ull) atomicMin(bad_ticks, badt);
 }
 
 struct UpWs {
@@ -443,7 +455,7 @@ struct UpWs {
   uint32_t* val[2];
   uint32_t* w;
   uint32_t* cum;
-  unsigned long long* flags;  // bad_q, bad_conv, bad_range
+  unsigned long long* flags;  // bad_q, bad_conv, bad_range, bad_ticks, universe
   uint32_t* stats;            // max_L, nconv
   void* cub_tmp;
   size_t cub_bytes;
@@ -457,7 +469,7 @@ static tlru_status carve_up(Carver& cv, uint64_t E, UpWs* w) {
   }
   w->w = cv.take<uint32_t>(n);
   w->cum = cv.take<uint32_t>(n);
-  w->flags = cv.take<unsigned long long>(3);
+  w->flags = cv.take<unsigned long long>(5);
   w->stats = cv.take<uint32_t>(2);
   size_t s1 = 0, s2 = 0;
   cub::DoubleBuffer<uint32_t> kb(nullptr, nullptr), vb(nullptr, nullptr);
@@ -534,6 +546,7 @@ extern "C" tlru_status tlru_generate_traces(const tlru_gen_params* params, uint3
     TLRU_CUDA(cudaMemsetAsync(w.max_L, 0, sizeof(uint32_t), st));
     TLRU_CUDA(cudaMemsetAsync(w.nconv, 0, sizeof(uint32_t), st));
     TLRU_CUDA(cudaMemsetAsync(w.nvalid, 0, sizeof(uint32_t), st));
+    TLRU_CUDA(cudaMemsetAsync(w.universe, 0, sizeof(unsigned long long), st));
     gen_slot_kernel<<<grid_for(g.N, 128), 128, 0, st>>>(g, w.off, w.cid, w.turn);
     TLRU_CHECK_LAUNCH();
     if (E > 0) {
@@ -543,12 +556,14 @@ extern "C" tlru_status tlru_generate_traces(const tlru_gen_params* params, uint3
     }
     gen_emit_kernel<<<grid_for(g.N, 128), 128, 0, st>>>(g, w.birth, w.off, w.gapt, w.q16, w.a16, sentinel, w.key[0],
                                                          w.val[0], w.J16, w.La16, w.last8, w.max_L, w.nconv,
-                                                         w.nvalid);
+                                                         w.nvalid, w.universe);
     TLRU_CHECK_LAUNCH();
     uint32_t stats[3];
+    unsigned long long universe = 0;
     TLRU_CUDA(cudaMemcpyAsync(&stats[0], w.max_L, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
     TLRU_CUDA(cudaMemcpyAsync(&stats[1], w.nconv, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
     TLRU_CUDA(cudaMemcpyAsync(&stats[2], w.nvalid, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    TLRU_CUDA(cudaMemcpyAsync(&universe, w.universe, sizeof(universe), cudaMemcpyDeviceToHost, st));
     TLRU_CUDA(cudaStreamSynchronize(st));
     const uint64_t slots = E;
     E = stats[2];  // events that survive the context cap
@@ -580,6 +595,8 @@ extern "C" tlru_status tlru_generate_traces(const tlru_gen_params* params, uint3
     tr->num_events = E;  // known since the stats copy: the rest of the generation stays asynchronous
     tr->max_history = stats[0];
     tr->num_conversations = stats[1];
+    tr->universe_blocks = universe;
+    tr->flags = 0;
   }
   return TLRU_OK;
 }
@@ -595,8 +612,9 @@ extern "C" tlru_status tlru_upload_workspace_size(uint64_t E, size_t* bytes) {
   return TLRU_OK;
 }
 
-extern "C" tlru_status tlru_trace_from_turns(const uint32_t* conv, const uint16_t* q, const uint16_t* a, uint64_t E,
-                                             tlru_trace* out, void* ws, size_t ws_bytes, cudaStream_t st) {
+extern "C" tlru_status tlru_trace_from_turns(const uint32_t* conv, const uint16_t* q, const uint16_t* a,
+                                             const uint64_t* ticks, uint64_t E, tlru_trace* out, void* ws,
+                                             size_t ws_bytes, cudaStream_t st) {
   clear_error();
   if (!out) TLRU_FAIL(TLRU_EINVAL, "out is NULL");
   if (E >= 0xFFFFFFFFull) TLRU_FAIL(TLRU_ERANGE, "E must be < 2^32 - 1");
@@ -611,8 +629,10 @@ extern "C" tlru_status tlru_trace_from_turns(const uint32_t* conv, const uint16_
   out->num_events = E;
   out->max_history = 0;
   out->num_conversations = 0;
+  out->universe_blocks = 0;
+  out->flags = ticks ? 0u : TLRU_TRACE_SYNTHETIC_TICKS;
   if (E == 0) return TLRU_OK;
-  const unsigned long long init[3] = {~0ull, ~0ull, ~0ull};
+  const unsigned long long init[5] = {~0ull, ~0ull, ~0ull, ~0ull, 0ull};
   TLRU_CUDA(cudaMemcpyAsync(w.flags, init, sizeof(init), cudaMemcpyHostToDevice, st));
   TLRU_CUDA(cudaMemsetAsync(w.stats, 0, 2 * sizeof(uint32_t), st));
   up_init_kernel<<<grid_for(E, 256), 256, 0, st>>>(E, conv, q, w.key[0], w.val[0], w.flags, w.flags + 1);
@@ -625,14 +645,14 @@ extern "C" tlru_status tlru_trace_from_turns(const uint32_t* conv, const uint16_
   b = w.cub_bytes;
   TLRU_CUDA(cub::DeviceScan::InclusiveSumByKey(w.cub_tmp, b, kb.Current(), w.w, w.cum, static_cast<int>(E),
                                                cub::Equality(), st));
-  up_link_kernel<<<grid_for(E, 256), 256, 0, st>>>(E, kb.Current(), vb.Current(), w.cum, a, out->sim, out->next,
-                                                   out->is_last, out->time_ticks, w.flags + 2, w.stats,
-                                                   w.stats + 1);
+  up_link_kernel<<<grid_for(E, 256), 256, 0, st>>>(E, kb.Current(), vb.Current(), w.cum, a, ticks, out->sim,
+                                                   out->next, out->is_last, out->time_ticks, w.flags + 2,
+                                                   w.flags + 3, w.stats, w.stats + 1, w.flags + 4);
   TLRU_CHECK_LAUNCH();
   if (out->conv) TLRU_CUDA(cudaMemcpyAsync(out->conv, conv, E * 4, cudaMemcpyDeviceToDevice, st));
   if (out->prompt) TLRU_CUDA(cudaMemcpyAsync(out->prompt, q, E * 2, cudaMemcpyDeviceToDevice, st));
   if (out->response) TLRU_CUDA(cudaMemcpyAsync(out->response, a, E * 2, cudaMemcpyDeviceToDevice, st));
-  unsigned long long flags[3];
+  unsigned long long flags[5];
   uint32_t stats[2];
   TLRU_CUDA(cudaMemcpyAsync(flags, w.flags, sizeof(flags), cudaMemcpyDeviceToHost, st));
   TLRU_CUDA(cudaMemcpyAsync(stats, w.stats, sizeof(stats), cudaMemcpyDeviceToHost, st));
@@ -640,7 +660,10 @@ extern "C" tlru_status tlru_trace_from_turns(const uint32_t* conv, const uint16_
   if (flags[1] != ~0ull) TLRU_FAIL(TLRU_EINVAL, "conv[%llu] == TLRU_NONE is reserved", flags[1]);
   if (flags[0] != ~0ull) TLRU_FAIL(TLRU_EINVAL, "q[%llu] == 0: every prompt has at least one block", flags[0]);
   if (flags[2] != ~0ull) TLRU_FAIL(TLRU_ERANGE, "event %llu: L_after exceeds 65535 blocks", flags[2]);
+  if (flags[3] != ~0ull) TLRU_FAIL(TLRU_EINVAL, "ticks[%llu] < ticks[%llu]: arrival times must be non-decreasing",
+                                   flags[3], flags[3] - 1);
   out->max_history = stats[0];
   out->num_conversations = stats[1];
+  out->universe_blocks = flags[4];
   return TLRU_OK;
 }

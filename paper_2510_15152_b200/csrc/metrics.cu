@@ -10,6 +10,8 @@
 //           per-thread partials are added in thread order (deterministic).
 #include <cub/cub.cuh>
 
+#include <algorithm>
+
 #include "metrics.cuh"
 
 namespace tlru {
@@ -88,14 +90,38 @@ __global__ void hist_global_kernel(const uint16_t* __restrict__ b, const SegDev*
 
 constexpr int FIN_THREADS = 256;
 
-__global__ void __launch_bounds__(FIN_THREADS) finalize_kernel(const SegDev* segs, uint32_t bins,
-                                                                const uint32_t* hist,
+// Thresholds of one segment: the SegDev of a b segment, or (xi, xi_ms, slo) arrays for
+// tlru_tail_from_histograms (NULL -> 0, 0.0, no SLO).
+struct FinParams {
+  const SegDev* segs;
+  const uint32_t* xi;
+  const double* xi_ms;
+  const uint32_t* slo;
+  __device__ void get(uint32_t s, uint32_t& x, double& xm, uint32_t& sl) const {
+    if (segs) {
+      x = segs[s].xi;
+      xm = segs[s].xi_ms;
+      sl = segs[s].slo;
+    } else {
+      x = xi ? xi[s] : 0u;
+      xm = xi_ms ? xi_ms[s] : 0.0;
+      sl = slo ? slo[s] : 0xFFFFFFFFu;
+    }
+  }
+};
+
+// One CTA per histogram row: exact integer ranks / TEL / SLO / sums from the counts (CountT =
+// u32 for per-instance rows, u64 for pooled rows).
+template <typename CountT>
+__global__ void __launch_bounds__(FIN_THREADS) finalize_kernel(FinParams prm, uint32_t bins, const CountT* hist,
                                                                 const unsigned long long* clamped, double alpha,
                                                                 tlru_tail* tails, tlru_result* results) {
   const uint32_t s = blockIdx.x;
-  const SegDev sg = segs[s];
+  uint32_t sg_xi, sg_slo;
+  double sg_xi_ms;
+  prm.get(s, sg_xi, sg_xi_ms, sg_slo);
   const uint32_t tid = threadIdx.x;
-  const uint32_t* H = hist + uint64_t(s) * bins;
+  const CountT* H = hist + uint64_t(s) * bins;
   const uint32_t per = (bins + FIN_THREADS - 1) / FIN_THREADS;
   const uint32_t lo = min(bins, tid * per), hi = min(bins, lo + per);
   unsigned long long cnt = 0, sum = 0, tel = 0, slo = 0;
@@ -106,10 +132,10 @@ __global__ void __launch_bounds__(FIN_THREADS) finalize_kernel(const SegDev* seg
     if (!c) continue;
     cnt += c;
     sum += c * v;
-    if (v > sg.xi) tel += c * (v - sg.xi);  // (b - xi)^+  (Eq. 3)
-    if (v > sg.slo) slo += c;               // b > slo, strict
+    if (v > sg_xi) tel += c * (v - sg_xi);  // (b - xi)^+  (Eq. 3)
+    if (v > sg_slo) slo += c;               // b > slo, strict
     vmax = v;
-    const double term = alpha * static_cast<double>(v) - sg.xi_ms;
+    const double term = alpha * static_cast<double>(v) - sg_xi_ms;
     if (term > 0.0) tel_ms += static_cast<double>(c) * term;  // (alpha b - xi_s)^+  (Eq. 1)
   }
   typedef cub::BlockScan<unsigned long long, FIN_THREADS> BS;
@@ -170,7 +196,7 @@ __global__ void __launch_bounds__(FIN_THREADS) finalize_kernel(const SegDev* seg
       o.p95 = pv[2];
       o.p99 = pv[3];
       o.max_b = n ? max_all : 0;
-      o.n_clamped = static_cast<uint32_t>(clamped[s]);
+      o.n_clamped = clamped ? static_cast<uint32_t>(clamped[s]) : 0u;
       o.tel_ms = tms;
       o.p50_ms = alpha * static_cast<double>(pv[0]);
       o.p90_ms = alpha * static_cast<double>(pv[1]);
@@ -192,6 +218,41 @@ __global__ void __launch_bounds__(FIN_THREADS) finalize_kernel(const SegDev* seg
       r.max_uncached = n ? max_all : 0;
     }
   }
+}
+
+// hist_out[row(i)][v] = hist[i][v] for v < bins, 0 for bins <= v < out_bins (row(i) = map[i] or i)
+__global__ void hist_export_kernel(const uint32_t* __restrict__ hist, uint32_t ni, uint32_t bins,
+                                   const uint32_t* __restrict__ map, uint32_t* __restrict__ out, uint32_t out_bins) {
+  const uint32_t i = blockIdx.y;
+  const uint32_t row = map ? map[i] : i;
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < out_bins; v += gridDim.x * blockDim.x)
+    out[uint64_t(row) * out_bins + v] = v < bins ? hist[uint64_t(i) * bins + v] : 0u;
+}
+
+// pooled[pool[i]][v] += hist[i][v]
+__global__ void pool_kernel(const uint32_t* __restrict__ hist, uint32_t bins, const uint32_t* __restrict__ pool,
+                            unsigned long long* __restrict__ pooled) {
+  const uint32_t i = blockIdx.y;
+  const uint32_t p = pool[i];
+  if (p == TLRU_NONE) return;
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < bins; v += gridDim.x * blockDim.x) {
+    const uint32_t c = hist[uint64_t(i) * bins + v];
+    if (c) atomicAdd(pooled + uint64_t(p) * bins + v, static_cast<unsigned long long>(c));
+  }
+}
+
+tlru_status launch_hist_export(const uint32_t* hist, uint32_t ni, uint32_t bins, const uint32_t* map, uint32_t* out,
+                               uint32_t out_bins, cudaStream_t st) {
+  if (ni == 0 || !out) return TLRU_OK;
+  for (uint32_t i0 = 0; i0 < ni; i0 += 65535u) {
+    const uint32_t n = std::min(65535u, ni - i0);
+    hist_export_kernel<<<dim3((out_bins + 255) / 256, n), 256, 0, st>>>(hist + uint64_t(i0) * bins, n, bins,
+                                                                        map ? map + i0 : nullptr,
+                                                                        map ? out : out + uint64_t(i0) * out_bins,
+                                                                        out_bins);
+    TLRU_CHECK_LAUNCH();
+  }
+  return TLRU_OK;
 }
 
 tlru_status launch_hist(const uint16_t* b, const SegDev* segs, uint32_t ns, uint32_t bins, uint32_t* hist,
@@ -223,7 +284,8 @@ tlru_status launch_finalize(const SegDev* segs, uint32_t ns, uint32_t bins, cons
                             const unsigned long long* clamped, double alpha, tlru_tail* tails,
                             tlru_result* results, cudaStream_t st) {
   if (ns == 0) return TLRU_OK;
-  finalize_kernel<<<ns, FIN_THREADS, 0, st>>>(segs, bins, hist, clamped, alpha, tails, results);
+  finalize_kernel<uint32_t><<<ns, FIN_THREADS, 0, st>>>(FinParams{segs, nullptr, nullptr, nullptr}, bins, hist, clamped,
+                                                        alpha, tails, results);
   TLRU_CHECK_LAUNCH();
   return TLRU_OK;
 }
@@ -251,7 +313,13 @@ struct TailWs {
 static void carve_tail(Carver& cv, uint32_t ns, uint32_t bins, TailWs* w) {
   w->segs = cv.take<SegDev>(ns ? ns : 1);
   w->hist = cv.take<uint32_t>(uint64_t(ns ? ns : 1) * bins);
-  w->clamped = cv.take<unsigned long long>(ns ? ns : 1);
+  w->clamped = cv.take<unsigned long long>(ns + 1);  // + the total over segments
+}
+
+__global__ void sum_u64_kernel(const unsigned long long* v, uint32_t n, unsigned long long* out) {
+  unsigned long long s = 0;
+  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) s += v[i];
+  warp_atomic_add_u64(out, s);
 }
 
 }  // namespace tlru
@@ -288,5 +356,62 @@ extern "C" tlru_status tlru_tail_metrics(const uint16_t* b, const uint64_t* seg_
   tail_segs_kernel<<<grid_for(ns, 128), 128, 0, st>>>(seg_offsets, ns, xi, xi_ms, slo, w.segs);
   TLRU_CHECK_LAUNCH();
   TLRU_TRY(launch_hist(b, w.segs, ns, bins, w.hist, w.clamped, st));
-  return launch_finalize(w.segs, ns, bins, w.hist, w.clamped, alpha, out, nullptr, st);
+  TLRU_TRY(launch_finalize(w.segs, ns, bins, w.hist, w.clamped, alpha, out, nullptr, st));
+  // never report percentiles of truncated data: any b > max_b is an error
+  unsigned long long* nbad = w.clamped + ns;
+  TLRU_CUDA(cudaMemsetAsync(nbad, 0, sizeof(unsigned long long), st));
+  sum_u64_kernel<<<1, 256, 0, st>>>(w.clamped, ns, nbad);
+  TLRU_CHECK_LAUNCH();
+  unsigned long long bad = 0;
+  TLRU_CUDA(cudaMemcpyAsync(&bad, nbad, sizeof(bad), cudaMemcpyDeviceToHost, st));
+  TLRU_CUDA(cudaStreamSynchronize(st));
+  if (bad) TLRU_FAIL(TLRU_ERANGE, "%llu values of b exceed max_b = %u (see tlru_tail.n_clamped)", bad, max_b);
+  return TLRU_OK;
+}
+
+extern "C" tlru_status tlru_pool_workspace_size(uint32_t ni, size_t* bytes) {
+  clear_error();
+  if (!bytes) TLRU_FAIL(TLRU_EINVAL, "bytes is NULL");
+  Carver cv(nullptr);
+  cv.take<uint32_t>(ni ? ni : 1);
+  *bytes = cv.used;
+  return TLRU_OK;
+}
+
+extern "C" tlru_status tlru_pool_histograms(const uint32_t* hist, uint32_t ni, uint32_t bins, const uint32_t* pool,
+                                            uint32_t npool, uint64_t* pooled, void* ws, size_t ws_bytes,
+                                            cudaStream_t st) {
+  clear_error();
+  if (ni == 0) return TLRU_OK;
+  if (!hist || !pool || !pooled) TLRU_FAIL(TLRU_EINVAL, "hist/pool/pooled is NULL");
+  if (bins == 0 || bins > 65536) TLRU_FAIL(TLRU_EINVAL, "bins must be in 1..65536");
+  for (uint32_t i = 0; i < ni; ++i)
+    if (pool[i] != TLRU_NONE && pool[i] >= npool) TLRU_FAIL(TLRU_EINVAL, "pool[%u] = %u >= npool = %u", i, pool[i], npool);
+  Carver cv(ws);
+  uint32_t* dpool = cv.take<uint32_t>(ni);
+  TLRU_TRY(check_ws(cv, ws, ws_bytes));
+  TLRU_CUDA(cudaMemcpyAsync(dpool, pool, size_t(ni) * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
+  for (uint32_t i0 = 0; i0 < ni; i0 += 65535u) {
+    const uint32_t n = std::min(65535u, ni - i0);
+    pool_kernel<<<dim3((bins + 255) / 256, n), 256, 0, st>>>(hist + uint64_t(i0) * bins, bins, dpool + i0,
+                                                             reinterpret_cast<unsigned long long*>(pooled));
+    TLRU_CHECK_LAUNCH();
+  }
+  // the pool map is copied from pageable host memory: it is staged before the call returns
+  return TLRU_OK;
+}
+
+extern "C" tlru_status tlru_tail_from_histograms(const uint64_t* hist, uint32_t ns, uint32_t bins, const uint32_t* xi,
+                                                 const double* xi_ms, const uint32_t* slo, double alpha,
+                                                 tlru_tail* out, cudaStream_t st) {
+  clear_error();
+  if (ns == 0) return TLRU_OK;
+  if (!hist || !out) TLRU_FAIL(TLRU_EINVAL, "hist/out is NULL");
+  if (bins == 0 || bins > 65536) TLRU_FAIL(TLRU_EINVAL, "bins must be in 1..65536");
+  if (!(alpha >= 0.0)) TLRU_FAIL(TLRU_EINVAL, "alpha must be >= 0");
+  finalize_kernel<unsigned long long><<<ns, FIN_THREADS, 0, st>>>(
+      FinParams{nullptr, xi, xi_ms, slo}, bins, reinterpret_cast<const unsigned long long*>(hist), nullptr, alpha, out,
+      nullptr);
+  TLRU_CHECK_LAUNCH();
+  return TLRU_OK;
 }

@@ -26,4 +26,9 @@ tlru_status launch_finalize(const SegDev* segs, uint32_t ns, uint32_t bins, cons
                             const unsigned long long* clamped, double alpha, tlru_tail* tails,
                             tlru_result* results, cudaStream_t st);
 
+// Copy per-instance histogram rows [ni][bins] to out[row][out_bins] (row = map[i], or i if map is
+// NULL), zero-filling bins >= bins.
+tlru_status launch_hist_export(const uint32_t* hist, uint32_t ni, uint32_t bins, const uint32_t* map, uint32_t* out,
+                               uint32_t out_bins, cudaStream_t st);
+
 }  // namespace tlru

@@ -537,6 +537,9 @@ static tlru_status make_plan(const tlru_trace* traces, uint32_t nt, const tlru_i
       if (g_et_mu < 0.0) TLRU_FAIL(TLRU_EINVAL, "instance %u: ET-LRU needs tlru_set_etlru_model first", i);
       if (traces[in.trace].num_events > 0 && !traces[in.trace].time_ticks)
         TLRU_FAIL(TLRU_EINVAL, "instance %u: ET-LRU needs the trace's time_ticks (beliefs, P:255)", i);
+      if (traces[in.trace].num_events > 0 && (traces[in.trace].flags & TLRU_TRACE_SYNTHETIC_TICKS))
+        TLRU_FAIL(TLRU_EINVAL, "instance %u: ET-LRU needs real arrival times, but trace %u was uploaded without "
+                  "ticks (time_ticks holds event indices; beliefs decay with time, P:255)", i, in.trace);
     }
     if (in.policy >= TLRU_POLICY_END_AWARE) P->any_aware = true;
     if (in.policy == TLRU_POLICY_THRESHOLD && in.threshold > 65535)
@@ -550,7 +553,6 @@ static tlru_status make_plan(const tlru_trace* traces, uint32_t nt, const tlru_i
     // conversations (128 or 256 entries) or splitting End- from Length-Aware lanes was slower on
     // the spectrum workload (wider capacity ranges per warp, more frequent compaction).
     // Forced-caching chains keep LRU-like state: up to 1024 entries of 6 B (no surplus array).
-    if (is_aware(in) && aware_kind(in) == kAwareTLRU) wc[i] = std::min(wc[i], kNumW - 2);
     if (in.policy == TLRU_POLICY_TAIL_BELADY && g_opt_w < 0) {
       // entries hold X >= 1 (tombstones are compacted before the state counts as full), so
       // W > C never overflows; the live conversations of a trace bound it too (<= ~91 on the
@@ -560,6 +562,10 @@ static tlru_status make_plan(const tlru_trace* traces, uint32_t nt, const tlru_i
       while (k < kNumW - 1 && static_cast<uint32_t>(kWClasses[k]) < need) ++k;
       wc[i] = k;
     }
+    // lanes with a surplus array (End-/Length-Aware, Belady) are launched for classes up to
+    // kNumW - 2 only (1024 entries x 8 B x 32 lanes exceed shared memory): cap them whatever
+    // tlru_set_sim_options asked for -- larger states are re-run by the fix-up
+    if (is_aware(in) && aware_kind(in) != kAwareForced) wc[i] = std::min(wc[i], kNumW - 2);
     const uint64_t E = traces[in.trace].num_events;
     const uint64_t off = offsets ? offsets[i] : packed;
     packed += E;
@@ -812,44 +818,127 @@ static tlru_status launch_et(const std::vector<EtSeg>& segs, const EtSeg* d_segs
 
 using namespace tlru;
 
-extern "C" tlru_status tlru_sim_workspace_size(const tlru_trace* traces, uint32_t nt, const tlru_instance* inst,
-                                               uint32_t ni, size_t* bytes) {
-  clear_error();
-  if (!bytes) TLRU_FAIL(TLRU_EINVAL, "bytes is NULL");
+// Engine of one instance: the stack engine needs the stack property (LRU, T-LRU,
+// Threshold-LRU) and a universe that keeps its 32-bit window sums exact.
+constexpr uint64_t kStackUniverseMax = 0xFFFF0000ull;
+static uint32_t engine_of(const tlru_instance& in, const tlru_trace* traces) {
+  if (g_opt_engine == TLRU_ENGINE_REPLAY || in.policy > TLRU_POLICY_THRESHOLD) return TLRU_ENGINE_REPLAY;
+  if (traces[in.trace].universe_blocks > kStackUniverseMax) return TLRU_ENGINE_REPLAY;
+  return TLRU_ENGINE_STACK;
+}
+
+// Workspace bytes of one engine for these instances (offsets do not change sizes).
+static tlru_status engine_ws_bytes(uint32_t engine, const tlru_trace* traces, uint32_t nt, const tlru_instance* inst,
+                                   uint32_t ni, size_t* bytes) {
   Plan P;
   TLRU_TRY(make_plan(traces, nt, inst, ni, nullptr, &P));
-  Carver cv(nullptr);
-  SimWs w;
-  carve_sim(cv, P, ni, &w);
+  if (engine == TLRU_ENGINE_REPLAY) {
+    Carver cv(nullptr);
+    SimWs w;
+    carve_sim(cv, P, ni, &w);
+    *bytes = cv.used;
+    return TLRU_OK;
+  }
   size_t sb = 0;
   TLRU_TRY(stack_workspace(traces, nt, inst, ni, &sb));
   Carver cv2(nullptr);
   cv2.take<SegDev>(ni + 1);
   cv2.take<uint32_t>(uint64_t(ni + 1) * P.bins);
   cv2.take<unsigned long long>(ni + 1);
-  *bytes = std::max(cv.used, cv2.used + 256 + sb);
+  *bytes = cv2.used + 256 + sb;
   return TLRU_OK;
 }
 
-extern "C" tlru_status tlru_simulate_batch(const tlru_trace* traces, uint32_t nt, const tlru_instance* inst,
-                                           uint32_t ni, uint16_t* uncached, const uint64_t* offsets,
-                                           tlru_result* results, void* ws, size_t ws_bytes, cudaStream_t st) {
+// The batch split by engine: ids[e] = instances of engine e (ascending).
+struct EngineSplit {
+  std::vector<uint32_t> ids[2];
+  bool mixed() const { return !ids[0].empty() && !ids[1].empty(); }
+};
+
+static tlru_status split_batch(const tlru_trace* traces, uint32_t nt, const tlru_instance* inst, uint32_t ni,
+                               EngineSplit* S) {
+  if (ni > 0 && !inst) TLRU_FAIL(TLRU_EINVAL, "inst is NULL");
+  if (nt > 0 && !traces) TLRU_FAIL(TLRU_EINVAL, "traces is NULL");
+  for (uint32_t i = 0; i < ni; ++i) {
+    if (inst[i].trace >= nt) TLRU_FAIL(TLRU_EINVAL, "instance %u: trace index %u out of range", i, inst[i].trace);
+    S->ids[engine_of(inst[i], traces)].push_back(i);
+  }
+  return TLRU_OK;
+}
+
+// Mixed batch: [results of the sub-batches (tlru_result[ni]), instance maps (u32[ni])] then the
+// larger engine's workspace.
+static void carve_mixed(Carver& cv, uint32_t ni, tlru_result** res_tmp, uint32_t** map) {
+  *res_tmp = cv.take<tlru_result>(ni + 1);
+  *map = cv.take<uint32_t>(ni + 1);
+}
+
+static tlru_status sub_batch(const tlru_instance* inst, const uint64_t* offs, const std::vector<uint32_t>& ids,
+                             std::vector<tlru_instance>* si, std::vector<uint64_t>* so) {
+  si->resize(ids.size());
+  so->resize(ids.size());
+  for (size_t k = 0; k < ids.size(); ++k) {
+    (*si)[k] = inst[ids[k]];
+    (*so)[k] = offs[ids[k]];
+  }
+  return TLRU_OK;
+}
+
+extern "C" tlru_status tlru_sim_workspace_size(const tlru_trace* traces, uint32_t nt, const tlru_instance* inst,
+                                               uint32_t ni, size_t* bytes) {
   clear_error();
-  g_stats = tlru_sim_stats{};
-  g_counters = nullptr;
-  g_ev_recorded = false;
-  g_out.launches = 0;
+  if (!bytes) TLRU_FAIL(TLRU_EINVAL, "bytes is NULL");
+  EngineSplit S;
+  TLRU_TRY(split_batch(traces, nt, inst, ni, &S));
+  if (!S.mixed()) {  // one engine: either may be selected at run time, size for both
+    Plan P;
+    TLRU_TRY(make_plan(traces, nt, inst, ni, nullptr, &P));
+    size_t a = 0, b = 0;
+    TLRU_TRY(engine_ws_bytes(TLRU_ENGINE_REPLAY, traces, nt, inst, ni, &a));
+    TLRU_TRY(engine_ws_bytes(TLRU_ENGINE_STACK, traces, nt, inst, ni, &b));
+    *bytes = std::max(a, b);
+    return TLRU_OK;
+  }
+  std::vector<uint64_t> zero(ni, 0);
+  size_t need = 0;
+  for (int e = 0; e < 2; ++e) {
+    std::vector<tlru_instance> si;
+    std::vector<uint64_t> so;
+    sub_batch(inst, zero.data(), S.ids[e], &si, &so);
+    size_t b = 0;
+    TLRU_TRY(engine_ws_bytes(static_cast<uint32_t>(e), traces, nt, si.data(), static_cast<uint32_t>(si.size()), &b));
+    need = std::max(need, b);
+  }
+  Carver cv(nullptr);
+  tlru_result* r;
+  uint32_t* m;
+  carve_mixed(cv, ni, &r, &m);
+  *bytes = ((cv.used + 255) & ~size_t(255)) + need;
+  return TLRU_OK;
+}
+
+__global__ void scatter_results_kernel(const tlru_result* __restrict__ src, const uint32_t* __restrict__ map,
+                                       uint32_t n, tlru_result* __restrict__ dst) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) dst[map[i]] = src[i];
+}
+
+// One engine over ni instances with explicit (host) offsets.  results / the histogram export take
+// row i, or row hist_map[i] of hist_out (device map, nullable).  `timing`: record g_ev / the s2_out
+// interval (a mixed batch records around both engines instead).
+static tlru_status run_engine(uint32_t engine, const tlru_trace* traces, uint32_t nt, const tlru_instance* inst,
+                              uint32_t ni, uint16_t* uncached, const uint64_t* offsets, tlru_result* results,
+                              uint32_t* hist_out, uint32_t hist_bins, const uint32_t* hist_map, void* ws,
+                              size_t ws_bytes, cudaStream_t st, bool timing) {
   if (ni == 0) return TLRU_OK;
-  if (!results) TLRU_FAIL(TLRU_EINVAL, "results is NULL");
   Plan P;
   TLRU_TRY(make_plan(traces, nt, inst, ni, offsets, &P));
   if (!uncached) {
     for (uint32_t i = 0; i < ni; ++i)
       if (traces[inst[i].trace].num_events > 0) TLRU_FAIL(TLRU_EINVAL, "uncached is NULL");
   }
-  // End-/Length-Aware instances have no stack property: such a batch runs on the replay engine
-  g_stats.engine = P.any_aware ? TLRU_ENGINE_REPLAY : g_opt_engine;
-  if (g_stats.engine == TLRU_ENGINE_STACK) {
+  if (hist_out && hist_bins < P.bins)
+    TLRU_FAIL(TLRU_ERANGE, "hist_bins = %u must exceed every trace's max_history (%u)", hist_bins, P.bins - 1);
+  if (engine == TLRU_ENGINE_STACK) {
     Carver cv(ws);
     SegDev* segs = cv.take<SegDev>(ni + 1);
     uint32_t* hist = cv.take<uint32_t>(uint64_t(ni + 1) * P.bins);
@@ -861,16 +950,18 @@ extern "C" tlru_status tlru_simulate_batch(const tlru_trace* traces, uint32_t nt
     TLRU_CUDA(cudaMemsetAsync(hist, 0, uint64_t(ni) * P.bins * sizeof(uint32_t), st));
     TLRU_CUDA(cudaMemsetAsync(clamped, 0, ni * sizeof(unsigned long long), st));
     unsigned nk = 0;
-    TLRU_TRY(record(0, st));
+    if (timing) TLRU_TRY(record(0, st));
     for (int k = 1; k < 5; ++k)
       if (!g_ev[k]) TLRU_CUDA(cudaEventCreate(&g_ev[k]));
-    g_out = OutTiming{g_ev[3], g_ev[4], 0u};
+    if (timing || g_out.first == nullptr) g_out = OutTiming{g_ev[3], g_ev[4], g_out.launches};
     TLRU_TRY(stack_simulate(traces, nt, inst, ni, boffs.data(), uncached, results, cv, segs, P.bins, hist, clamped,
-                            ws_bytes, st, &nk, g_ev[1], &g_out));  // records g_ev[1] between the engine and K3
-    TLRU_TRY(record(2, st));
-    g_ev_recorded = true;
-    g_stats.kernels = nk;
-    g_stats.segment_events = 0;
+                            ws_bytes, st, &nk, timing ? g_ev[1] : nullptr, &g_out));  // g_ev[1]: engine | K3
+    TLRU_TRY(launch_hist_export(hist, ni, P.bins, hist_map, hist_out, hist_bins, st));
+    if (timing) {
+      TLRU_TRY(record(2, st));
+      g_ev_recorded = true;
+    }
+    g_stats.kernels += nk + (hist_out ? 1u : 0u);
     return TLRU_OK;
   }
   Carver cv(ws);
@@ -920,7 +1011,7 @@ extern "C" tlru_status tlru_simulate_batch(const tlru_trace* traces, uint32_t nt
   TLRU_CUDA(cudaMemsetAsync(w.hist, 0, uint64_t(ni) * P.bins * sizeof(uint32_t), st));
   TLRU_CUDA(cudaMemsetAsync(w.clamped, 0, ni * sizeof(unsigned long long), st));
   // K2: largest state class first (longest per-event latency)
-  TLRU_TRY(record(0, st));
+  if (timing) TLRU_TRY(record(0, st));
   for (int k = kNumW - 1; k >= 0; --k) {
     const ItemDev* d = w.items + item_off[k];
     const ItemDev* da = w.items + aware_off[k];
@@ -980,15 +1071,18 @@ extern "C" tlru_status tlru_simulate_batch(const tlru_trace* traces, uint32_t nt
     TLRU_CHECK_LAUNCH();
     ++g_stats.kernels;
   }
-  TLRU_TRY(record(1, st));
+  if (timing) TLRU_TRY(record(1, st));
   // K3: histogram of b per instance -> percentiles, TEL, SLO; then the counters
   TLRU_TRY(launch_hist(uncached, w.segs, ni, P.bins, w.hist, w.clamped, st));
   TLRU_TRY(launch_finalize(w.segs, ni, P.bins, w.hist, w.clamped, 1.0, nullptr, results, st));
   sim_results_kernel<<<grid_for(ni, 128), 128, 0, st>>>(ni, w.acc, results);
   TLRU_CHECK_LAUNCH();
-  TLRU_TRY(record(2, st));
-  g_ev_recorded = true;
-  g_stats.kernels += 3;
+  TLRU_TRY(launch_hist_export(w.hist, ni, P.bins, hist_map, hist_out, hist_bins, st));
+  if (timing) {
+    TLRU_TRY(record(2, st));
+    g_ev_recorded = true;
+  }
+  g_stats.kernels += 3 + (hist_out ? 1u : 0u);
   g_stats.chains = 0;
   for (int k = 0; k < kNumW; ++k)
     g_stats.chains += (P.items[k].size() + P.items_aware[k].size() + P.items_nos[k].size()) * 32 +
@@ -1001,6 +1095,72 @@ extern "C" tlru_status tlru_simulate_batch(const tlru_trace* traces, uint32_t nt
     }
   g_counters = w.counters;
   return TLRU_OK;
+}
+
+
+extern "C" tlru_status tlru_simulate_batch_ex(const tlru_trace* traces, uint32_t nt, const tlru_instance* inst,
+                                              uint32_t ni, uint16_t* uncached, const uint64_t* offsets,
+                                              tlru_result* results, uint32_t* hist, uint32_t hist_bins, void* ws,
+                                              size_t ws_bytes, cudaStream_t st) {
+  clear_error();
+  g_stats = tlru_sim_stats{};
+  g_counters = nullptr;
+  g_ev_recorded = false;
+  g_out = OutTiming{};
+  if (ni == 0) return TLRU_OK;
+  if (!results) TLRU_FAIL(TLRU_EINVAL, "results is NULL");
+  if (hist && hist_bins == 0) TLRU_FAIL(TLRU_ERANGE, "hist_bins must be > 0");
+  EngineSplit S;
+  TLRU_TRY(split_batch(traces, nt, inst, ni, &S));
+  std::vector<uint64_t> offs(ni);  // explicit offsets (packed prefix sums of E_i when NULL)
+  for (uint64_t i = 0, packed = 0; i < ni; ++i) {
+    offs[i] = offsets ? offsets[i] : packed;
+    packed += traces[inst[i].trace].num_events;
+  }
+  if (!S.mixed()) {
+    g_stats.engine = S.ids[TLRU_ENGINE_STACK].empty() ? TLRU_ENGINE_REPLAY : TLRU_ENGINE_STACK;
+    return run_engine(g_stats.engine, traces, nt, inst, ni, uncached, offs.data(), results, hist, hist_bins, nullptr,
+                      ws, ws_bytes, st, true);
+  }
+  // both engines, each on its own instances (stack first: its s2_out interval is the dominant kernel)
+  g_stats.engine = TLRU_ENGINE_MIXED;
+  Carver cv(ws);
+  tlru_result* res_tmp;
+  uint32_t* map;
+  carve_mixed(cv, ni, &res_tmp, &map);
+  TLRU_TRY(check_ws(cv, ws, ws_bytes));
+  const size_t head = (cv.used + 255) & ~size_t(255);
+  if (ws_bytes < head) TLRU_FAIL(TLRU_ERANGE, "workspace too small for a mixed batch");
+  std::vector<uint32_t> allmap;
+  for (int e = 1; e >= 0; --e) allmap.insert(allmap.end(), S.ids[e].begin(), S.ids[e].end());
+  TLRU_CUDA(cudaMemcpyAsync(map, allmap.data(), ni * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
+  TLRU_TRY(record(0, st));
+  uint32_t done = 0;
+  uint32_t kernels = 0;
+  for (int e = 1; e >= 0; --e) {
+    std::vector<tlru_instance> si;
+    std::vector<uint64_t> so;
+    sub_batch(inst, offs.data(), S.ids[e], &si, &so);
+    const uint32_t n = static_cast<uint32_t>(si.size());
+    g_stats.kernels = 0;
+    TLRU_TRY(run_engine(static_cast<uint32_t>(e), traces, nt, si.data(), n, uncached, so.data(), res_tmp + done, hist,
+                        hist_bins, map + done, static_cast<char*>(ws) + head, ws_bytes - head, st, false));
+    kernels += g_stats.kernels;
+    done += n;
+  }
+  scatter_results_kernel<<<grid_for(ni, 128), 128, 0, st>>>(res_tmp, map, ni, results);
+  TLRU_CHECK_LAUNCH();
+  TLRU_TRY(record(1, st));
+  TLRU_TRY(record(2, st));
+  g_ev_recorded = true;
+  g_stats.kernels = kernels + 1;
+  return TLRU_OK;
+}
+
+extern "C" tlru_status tlru_simulate_batch(const tlru_trace* traces, uint32_t nt, const tlru_instance* inst,
+                                           uint32_t ni, uint16_t* uncached, const uint64_t* offsets,
+                                           tlru_result* results, void* ws, size_t ws_bytes, cudaStream_t st) {
+  return tlru_simulate_batch_ex(traces, nt, inst, ni, uncached, offsets, results, nullptr, 0, ws, ws_bytes, st);
 }
 
 extern "C" tlru_status tlru_set_sim_options(uint32_t segment_events, uint32_t state_entries) {

@@ -13,11 +13,12 @@ import numpy as np
 import torch
 
 from . import _abi
-from ._abi import (ENGINE_REPLAY, ENGINE_STACK, POLICY_END_AWARE, POLICY_ET_LRU, POLICY_LENGTH_AWARE, POLICY_TLRU_FORCED, POLICY_LRU, POLICY_TAIL_BELADY, POLICY_THRESHOLD, POLICY_TLRU, RESULT_DTYPE, TAIL_DTYPE, TLRU_NONE, GenParams, Instance, SimStats,
+from ._abi import (ENGINE_MIXED, ENGINE_REPLAY, ENGINE_STACK, POLICY_END_AWARE, POLICY_ET_LRU, POLICY_LENGTH_AWARE, POLICY_TLRU_FORCED, POLICY_LRU, POLICY_TAIL_BELADY, POLICY_THRESHOLD, POLICY_TLRU, RESULT_DTYPE, TAIL_DTYPE, TLRU_NONE, GenParams, Instance, SimStats,
                    Trace, TlruError, check, lib)
 
-__all__ = ["DeviceTrace", "generate_traces", "trace_from_turns", "simulate_batch", "tail_metrics", "last_sim_stats", "set_sim_options", "set_sim_engine", "set_etlru_model",
-           "ENGINE_REPLAY", "ENGINE_STACK",
+__all__ = ["DeviceTrace", "generate_traces", "trace_from_turns", "simulate_batch", "tail_metrics", "last_sim_stats",
+           "set_sim_options", "set_sim_engine", "set_etlru_model", "pool_histograms", "tail_from_histograms",
+           "ENGINE_REPLAY", "ENGINE_STACK", "ENGINE_MIXED",
            "POLICY_LRU", "POLICY_TLRU", "POLICY_THRESHOLD", "POLICY_END_AWARE", "POLICY_LENGTH_AWARE", "POLICY_TAIL_BELADY", "POLICY_ET_LRU", "POLICY_TLRU_FORCED", "TLRU_NONE", "TlruError", "RESULT_DTYPE", "TAIL_DTYPE", "version"]
 
 
@@ -51,6 +52,8 @@ class DeviceTrace:
     num_events: int = 0
     max_history: int = 0
     num_conversations: int = 0
+    universe_blocks: int = 0
+    flags: int = 0
 
     def struct(self) -> Trace:
         t = Trace()
@@ -58,6 +61,8 @@ class DeviceTrace:
         t.num_events = self.num_events
         t.max_history = self.max_history
         t.num_conversations = self.num_conversations
+        t.universe_blocks = self.universe_blocks
+        t.flags = self.flags
         t.sim = self.sim.data_ptr()
         t.next = self.next.data_ptr()
         for name in ("conv", "prompt", "response", "time_ticks", "is_last"):
@@ -115,15 +120,25 @@ def generate_traces(params: list[dict], device="cuda", exports: bool = True, str
         ws = _workspace(sz.value, device)
         ts = tr.struct()
         check(lib.tlru_generate_traces(ctypes.byref(g), 1, ctypes.byref(ts), _ptr(ws), sz.value, st))
-        tr.num_events, tr.max_history, tr.num_conversations = ts.num_events, ts.max_history, ts.num_conversations
+        _read_back(tr, ts)
         out.append(tr)
     return out
 
 
+def _read_back(tr: DeviceTrace, ts: Trace) -> None:
+    tr.num_events, tr.max_history, tr.num_conversations = ts.num_events, ts.max_history, ts.num_conversations
+    tr.universe_blocks, tr.flags = ts.universe_blocks, ts.flags
+
+
 def trace_from_turns(conv: torch.Tensor, q: torch.Tensor, a: torch.Tensor, exports: bool = True,
-                     stream=None) -> DeviceTrace:
-    """tlru_trace_from_turns: conv (int32 holding uint32 ids), q, a (16-bit) device tensors in event order."""
+                     stream=None, ticks: torch.Tensor | None = None) -> DeviceTrace:
+    """tlru_trace_from_turns: conv (int32 holding uint32 ids), q, a (16-bit) device tensors in event order;
+    ticks (int64 holding uint64 arrival times, non-decreasing) optional -- without them the trace's
+    time_ticks are event indices and ET-LRU rejects it (TLRU_TRACE_SYNTHETIC_TICKS)."""
     assert conv.is_cuda and q.is_cuda and a.is_cuda
+    if ticks is not None:
+        assert ticks.is_cuda and ticks.dtype in (torch.int64, torch.uint64) and ticks.numel() == conv.numel()
+        ticks = ticks.contiguous()
     E = conv.numel()
     conv = conv.contiguous()
     assert q.dtype in (torch.uint16, torch.int16) and a.dtype in (torch.uint16, torch.int16)
@@ -134,9 +149,9 @@ def trace_from_turns(conv: torch.Tensor, q: torch.Tensor, a: torch.Tensor, expor
     check(lib.tlru_upload_workspace_size(E, ctypes.byref(sz)))
     ws = _workspace(sz.value, conv.device)
     ts = tr.struct()
-    check(lib.tlru_trace_from_turns(_ptr(conv), _ptr(q), _ptr(a), E, ctypes.byref(ts), _ptr(ws), sz.value,
-                                    _stream(stream)))
-    tr.num_events, tr.max_history, tr.num_conversations = ts.num_events, ts.max_history, ts.num_conversations
+    check(lib.tlru_trace_from_turns(_ptr(conv), _ptr(q), _ptr(a), _ptr(ticks), E, ctypes.byref(ts), _ptr(ws),
+                                    sz.value, _stream(stream)))
+    _read_back(tr, ts)
     return tr
 
 
@@ -161,11 +176,21 @@ class SimBatch:
     results: torch.Tensor
     ws: torch.Tensor
     tstructs: "ctypes.Array" = field(default=None)
+    hist: torch.Tensor | None = None   # [ni][hist_bins] int32 (uint32 counts) when requested
+    hist_bins: int = 0
 
-    def run(self, stream=None) -> None:
+    def run(self, stream=None, check_state: bool = False) -> None:
+        """Enqueue tlru_simulate_batch(_ex) on `stream` (asynchronous).  check_state=True
+        synchronizes and raises if a replay chain overflowed even its global-memory state
+        (failed_chains > 0: its b rows would be invalid; tlru.h)."""
         off = self.offsets.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64))
-        check(lib.tlru_simulate_batch(self.tstructs, len(self.traces), self.inst, self.ni, _ptr(self.uncached), off,
-                                      _ptr(self.results), _ptr(self.ws), self.ws.numel(), _stream(stream)))
+        check(lib.tlru_simulate_batch_ex(self.tstructs, len(self.traces), self.inst, self.ni, _ptr(self.uncached),
+                                         off, _ptr(self.results), _ptr(self.hist), self.hist_bins, _ptr(self.ws),
+                                         self.ws.numel(), _stream(stream)))
+        if check_state:
+            st = last_sim_stats()
+            if st["failed_chains"]:
+                raise TlruError(5, f"{st['failed_chains']} chains overflowed their state (TLRU_ESTATE)")
 
     def results_numpy(self) -> np.ndarray:
         return self.results.cpu().numpy().view(RESULT_DTYPE).copy()
@@ -176,8 +201,9 @@ class SimBatch:
         return self.uncached[o:o + E].view(torch.int16).cpu().numpy().view(np.uint16)
 
 
-def prepare_batch(traces: list[DeviceTrace], rows, align: int = 8) -> SimBatch:
-    """Allocate b (each instance's row starts at a multiple of `align` requests), results and workspace."""
+def prepare_batch(traces: list[DeviceTrace], rows, align: int = 8, hist_bins: int = 0) -> SimBatch:
+    """Allocate b (each instance's row starts at a multiple of `align` requests), results and workspace;
+    with hist_bins > 0 also the per-instance histograms of b (tlru_simulate_batch_ex)."""
     rows = list(rows)
     ni = len(rows)
     inst = instances_array(rows)
@@ -195,14 +221,48 @@ def prepare_batch(traces: list[DeviceTrace], rows, align: int = 8) -> SimBatch:
                     uncached=torch.empty(max(tot, 8), dtype=torch.uint16, device=device),
                     offsets=offsets,
                     results=torch.empty(max(ni, 1) * RESULT_DTYPE.itemsize, dtype=torch.uint8, device=device),
-                    ws=_workspace(sz.value, device), tstructs=tstructs)
+                    ws=_workspace(sz.value, device), tstructs=tstructs,
+                    hist=torch.empty(max(ni, 1) * hist_bins, dtype=torch.int32, device=device) if hist_bins else None,
+                    hist_bins=int(hist_bins))
 
 
-def simulate_batch(traces: list[DeviceTrace], rows, stream=None) -> SimBatch:
-    """tlru_simulate_batch: rows = [(trace, policy, capacity, xi, q_hat, slo), ...]."""
-    batch = prepare_batch(traces, rows)
-    batch.run(stream)
+def simulate_batch(traces: list[DeviceTrace], rows, stream=None, hist_bins: int = 0) -> SimBatch:
+    """tlru_simulate_batch: rows = [(trace, policy, capacity, xi, q_hat, slo[, threshold]), ...].
+    Synchronizes and raises if a chain overflowed its state (failed_chains, tlru.h)."""
+    batch = prepare_batch(traces, rows, hist_bins=hist_bins)
+    batch.run(stream, check_state=True)
     return batch
+
+
+def pool_histograms(hist: torch.Tensor, bins: int, pool, npool: int, pooled: torch.Tensor | None = None,
+                    stream=None) -> torch.Tensor:
+    """tlru_pool_histograms: pooled[pool[i]] += hist[i] (hist: [ni * bins] int32 of uint32 counts; pooled:
+    [npool * bins] int64 of uint64 counts, allocated zeroed when None).  pool[i] = TLRU_NONE skips i."""
+    pool = np.ascontiguousarray(np.asarray(pool, np.uint32))
+    ni = pool.size
+    if pooled is None:
+        pooled = torch.zeros(max(npool, 1) * bins, dtype=torch.int64, device=hist.device)
+    sz = ctypes.c_size_t()
+    check(lib.tlru_pool_workspace_size(ni, ctypes.byref(sz)))
+    ws = _workspace(sz.value, hist.device)
+    check(lib.tlru_pool_histograms(_ptr(hist), ni, bins, pool.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32)), npool,
+                                   _ptr(pooled), _ptr(ws), sz.value, _stream(stream)))
+    return pooled
+
+
+def tail_from_histograms(hist: torch.Tensor, bins: int, xi, xi_ms, slo, alpha: float, stream=None) -> torch.Tensor:
+    """tlru_tail_from_histograms over [ns * bins] int64 (uint64) counts; returns a device uint8 tensor of
+    ns TAIL_DTYPE records (asynchronous; `.cpu().numpy().view(TAIL_DTYPE)` to read)."""
+    dev = hist.device
+    ns = hist.numel() // bins
+    xi_t = torch.as_tensor(np.asarray(xi, np.uint32).view(np.int32), device=dev)
+    slo_t = torch.as_tensor(np.asarray(slo, np.uint32).view(np.int32), device=dev)
+    xim = torch.as_tensor(np.asarray(xi_ms, np.float64), device=dev)
+    out = torch.empty(max(ns, 1) * TAIL_DTYPE.itemsize, dtype=torch.uint8, device=dev)
+    check(lib.tlru_tail_from_histograms(_ptr(hist), ns, bins, _ptr(xi_t), _ptr(xim), _ptr(slo_t), float(alpha),
+                                        _ptr(out), _stream(stream)))
+    out.keepalive = (xi_t, slo_t, xim)  # the kernel reads them asynchronously
+    return out
 
 
 def set_sim_options(segment_events: int = 0, state_entries: int = 0) -> None:

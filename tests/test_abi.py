@@ -64,6 +64,21 @@ def test_host_validation_codes(abi):
     assert abi.lib.tlru_set_sim_options(0, 0) == 0
 
 
+def test_pool_and_tail_host_validation(abi):
+    """Host-side checks of the pooled-metrics calls (no device work is reached)."""
+    fake = ctypes.c_void_p(256)  # never dereferenced: validation fails first
+    pool = (ctypes.c_uint32 * 3)(0, 0xFFFFFFFF, 2)
+    sz = ctypes.c_size_t()
+    assert abi.lib.tlru_pool_workspace_size(3, ctypes.byref(sz)) == 0 and sz.value >= 12
+    assert abi.lib.tlru_pool_histograms(fake, 3, 10, pool, 2, fake, fake, sz.value, None) == 1  # pool[2] >= npool
+    assert b"pool[2]" in abi.lib.tlru_last_error()
+    assert abi.lib.tlru_pool_histograms(None, 3, 10, pool, 3, fake, fake, sz.value, None) == 1  # hist NULL
+    assert abi.lib.tlru_pool_histograms(fake, 3, 0, pool, 3, fake, fake, sz.value, None) == 1  # bins == 0
+    assert abi.lib.tlru_tail_from_histograms(fake, 2, 70000, None, None, None, 12.5, fake, None) == 1
+    assert abi.lib.tlru_tail_from_histograms(fake, 2, 10, None, None, None, -1.0, fake, None) == 1
+    assert abi.lib.tlru_tail_from_histograms(None, 0, 10, None, None, None, 1.0, None, None) == 0  # ns == 0
+
+
 def test_sim_workspace_rejects_unknown_policy(abi):
     tr = (abi.Trace * 1)()
     tr[0].num_events = 0

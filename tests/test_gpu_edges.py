@@ -9,7 +9,17 @@ import torch
 
 import oracle as O
 from paper_2510_15152_b200.inputs import random_trace
-from test_gpu_aware import upload
+from test_gpu_aware import upload as _upload
+
+
+def upload(T, conv, q, a):
+    """Upload with arrival time = event index (explicit ticks: ET-LRU rejects synthetic ones)."""
+    if len(conv) == 0:
+        return _upload(T, conv, q, a)
+    c = torch.from_numpy(np.asarray(conv, np.uint32).view(np.int32).copy()).cuda()
+    qq = torch.from_numpy(np.asarray(q, np.uint16).view(np.int16).copy()).cuda()
+    aa = torch.from_numpy(np.asarray(a, np.uint16).view(np.int16).copy()).cuda()
+    return T.trace_from_turns(c, qq, aa, ticks=torch.arange(len(conv), dtype=torch.int64, device="cuda"))
 
 pytestmark = pytest.mark.gpu
 TAB = [0.0, 0.0, math.log(0.4), math.log(0.2), -math.inf]
@@ -32,7 +42,7 @@ def T():
 
 def oracle_b(pol, conv, q, a, C, xi, qh, thr=0):
     if pol == 6:
-        ticks = np.arange(len(conv), dtype=np.uint64)  # the upload numbers events: time = index
+        ticks = np.arange(len(conv), dtype=np.uint64)  # uploaded with time = event index
         return O.replay_etlru(conv, q, a, ticks, C, xi, MU, TAB)
     return O.replay(conv, q, a, pol, C, xi, qh, threshold=thr)
 

@@ -32,9 +32,28 @@ def T():
     T.set_sim_engine(T.ENGINE_STACK)
 
 
-def with_ticks(T, tr, ticks):
-    tr.time_ticks[: tr.num_events].copy_(torch.from_numpy(np.asarray(ticks, np.uint64).view(np.int64)))
+def upload_ticks(T, conv, q, a, ticks):
+    """Upload with the trace's real arrival times (tlru_trace_from_turns' ticks input)."""
+    c = torch.from_numpy(np.asarray(conv, np.uint32).view(np.int32).copy()).cuda()
+    qq = torch.from_numpy(np.asarray(q, np.uint16).view(np.int16).copy()).cuda()
+    aa = torch.from_numpy(np.asarray(a, np.uint16).view(np.int16).copy()).cuda()
+    tk = torch.from_numpy(np.asarray(ticks, np.uint64).view(np.int64).copy()).cuda()
+    tr = T.trace_from_turns(c, qq, aa, ticks=tk)
+    assert tr.flags == 0
     return tr
+
+
+def test_etlru_rejects_synthetic_ticks(T):
+    """An upload without ticks numbers the events (TLRU_TRACE_SYNTHETIC_TICKS): ET-LRU's beliefs
+    decay with time, so the batch is TLRU_EINVAL rather than silently per-event decay."""
+    tr = upload(T, [0, 1, 0], [1, 1, 1], [0, 0, 0])
+    assert tr.flags == 1
+    assert np.array_equal(tr.time_ticks[:3].cpu().numpy(), [0, 1, 2])
+    T.set_etlru_model(1e-6, prompt_law_ln_surv(WILDCHAT))
+    with pytest.raises(T.TlruError, match="EINVAL.*ticks"):
+        T.simulate_batch([tr], [(0, ET, 4, 2, 2, 16)])
+    with pytest.raises(T.TlruError, match="EINVAL.*non-decreasing"):
+        upload_ticks(T, [0, 1, 0], [1, 1, 1], [0, 0, 0], [5, 3, 9])
 
 
 def check_et(bt, rows, otr, mu, table):
@@ -66,7 +85,7 @@ def test_random_traces_mixed_batch(T, tab):
     for s in range(2):
         conv, q, a = random_trace(4000 + 10 * tab + s, 5000, 70, q_max=5, a_max=6, locality=0.6)
         ticks = np.cumsum(rng.integers(0, 4, size=conv.size)).astype(np.uint64)
-        traces.append(with_ticks(T, upload(T, conv, q, a), ticks))
+        traces.append(upload_ticks(T, conv, q, a, ticks))
         otr.append((conv, q, a, ticks))
         for C in (0, 1, 3, 20, 90, 400):
             rows += [(s, ET, C, xi, 0, 8) for xi in (0, 2, 5, 12)]
@@ -105,7 +124,7 @@ def test_state_overflow_rerun(T):
     T.set_etlru_model(0.2, tab)
     conv, q, a = random_trace(4100, 6000, 200, q_max=3, a_max=3, locality=0.2)
     ticks = np.arange(conv.size, dtype=np.uint64) * 3
-    tr = with_ticks(T, upload(T, conv, q, a), ticks)
+    tr = upload_ticks(T, conv, q, a, ticks)
     rows = [(0, ET, C, xi, 0, 8) for C in (300, 900) for xi in (0, 6)]
     T.set_sim_options(0, 32)
     try:
@@ -155,7 +174,7 @@ def test_short_segments_verified(T):
     T.set_etlru_model(0.02, tab)
     conv, q, a = random_trace(4200, 20000, 30, q_max=4, a_max=4, locality=0.1)
     ticks = np.cumsum(np.random.default_rng(4).integers(0, 5, size=conv.size)).astype(np.uint64)
-    tr = with_ticks(T, upload(T, conv, q, a), ticks)
+    tr = upload_ticks(T, conv, q, a, ticks)
     rows = [(0, ET, C, xi, 0, 8) for C in (8, 40, 150, 600) for xi in (0, 3, 9)]
     T.set_sim_options(256, 0)
     try:
@@ -176,7 +195,7 @@ def test_long_prompt_law_table(T):
     T.set_etlru_model(0.03, tab)
     conv, q, a = random_trace(4300, 4000, 40, q_max=30, a_max=30, locality=0.6)
     ticks = np.cumsum(np.random.default_rng(7).integers(0, 3, size=conv.size)).astype(np.uint64)
-    tr = with_ticks(T, upload(T, conv, q, a), ticks)
+    tr = upload_ticks(T, conv, q, a, ticks)
     rows = [(0, ET, C, xi, 0, 8) for C in (50, 300, 1500) for xi in (200, 450, 690)]
     bt = T.simulate_batch([tr], rows)
     check_et(bt, rows, [(conv, q, a, ticks)], 0.03, tab)

@@ -311,11 +311,13 @@ def test_config5_bench_launch_sampled(T):
                 assert all(a >= b for a, b in zip(sums, sums[1:]))
 
 
-def test_config5_stratified(T):
-    """SURVEY 8(d) full-sweep parity: a stratified sample with >= 1 instance per (C, policy)
-    and per (xi, policy) of the config-5 grid, checked element by element against the oracle
-    (seed 0, all 1000 of its instances in the bench's one-trace launch; 50 oracle replays on
-    host threads -- the oracle's ctypes calls release the GIL)."""
+def test_config5_full_grid_one_seed(T):
+    """SURVEY 8(d) full-sweep parity, one seed: EVERY (C, xi, policy) cell of the config-5 grid --
+    all 1000 instances of seed 0 in the bench's one-trace launch (default engine) -- against the
+    oracle element by element (1000 oracle replays on host threads; the ctypes calls release the
+    GIL, and each worker compares its own row so host memory stays bounded).  Then the replay
+    engine (Alg. 1 request by request) on the same 1000 instances: identical b BYTES, histograms
+    and results."""
     import os
     from concurrent.futures import ThreadPoolExecutor
     T.set_sim_engine(T.ENGINE_STACK)
@@ -324,28 +326,44 @@ def test_config5_stratified(T):
     o = O.generate(p)
     assert g.num_events == o.E
     rows = [(0,) + tuple(r[1:]) for r in config5_rows(1)]
-    bt = T.simulate_batch([g], rows)
+    assert len({r[1:4] for r in rows}) == 1000
+    bins = g.max_history + 1
+    bt = T.simulate_batch([g], rows, hist_bins=bins)
+    torch.cuda.synchronize()
     res = bt.results_numpy()
-    key = {r: i for i, r in enumerate(rows)}
-    picks = [key[(0, pol, C, XI_CONFIG5[(k + 7 * pol) % len(XI_CONFIG5)], Q_HAT, SLO_BLOCKS)]
-             for pol in (0, 1) for k, C in enumerate(CAPS_CONFIG5)]
-    assert {(rows[i][1], rows[i][3]) for i in picks} == {(pol, xi) for pol in (0, 1) for xi in XI_CONFIG5}
 
     def one(i):
         _, pol, C, xi, qh, slo = rows[i]
-        return i, O.replay(o.conv, o.q, o.a, pol, C, xi, qh)
+        r = O.replay(o.conv, o.q, o.a, pol, C, xi, qh)
+        if not np.array_equal(bt.b(i).astype(np.uint64), r.b):
+            return i, "b"
+        tl = O.tail(r.b, xi, ALPHA_MS * xi, slo, ALPHA_MS)
+        got = res[i]
+        if (got["sum_uncached"], got["tel_blocks"], got["slo_violations"]) != (tl.sum_b, tl.tel_blocks,
+                                                                                tl.slo_violations):
+            return i, "tel/slo"
+        if (got["p50"], got["p90"], got["p95"], got["p99"]) != (tl.p50, tl.p90, tl.p95, tl.p99):
+            return i, "percentiles"
+        if (got["evicted_trim"], got["evicted_lru"], got["max_occupancy"]) != (r.evicted_trim, r.evicted_lru,
+                                                                                r.max_occupancy):
+            return i, "evictions"
+        return i, None
 
-    with ThreadPoolExecutor(max_workers=max(1, min(len(picks), os.cpu_count() or 1))) as ex:
-        for i, r in ex.map(one, picks):
-            _, pol, C, xi, qh, slo = rows[i]
-            assert np.array_equal(bt.b(i).astype(np.uint64), r.b), rows[i]
-            tl = O.tail(r.b, xi, ALPHA_MS * xi, slo, ALPHA_MS)
-            got = res[i]
-            assert (got["sum_uncached"], got["tel_blocks"], got["slo_violations"]) == \
-                (tl.sum_b, tl.tel_blocks, tl.slo_violations), rows[i]
-            assert (got["p50"], got["p90"], got["p95"], got["p99"]) == (tl.p50, tl.p90, tl.p95, tl.p99), rows[i]
-            assert (got["evicted_trim"], got["evicted_lru"], got["max_occupancy"]) == \
-                (r.evicted_trim, r.evicted_lru, r.max_occupancy), rows[i]
+    with ThreadPoolExecutor(max_workers=max(1, os.cpu_count() or 1)) as ex:
+        bad = [(rows[i], what) for i, what in ex.map(one, range(len(rows))) if what]
+    assert not bad, bad[:5]
+    # the replay engine on the same launch: byte-identical b rows, histograms and results
+    bt.uncached.zero_()
+    bt.run(check_state=True)
+    T.set_sim_engine(T.ENGINE_REPLAY)
+    rb = T.prepare_batch([g], rows, hist_bins=bins)
+    rb.uncached.zero_()
+    rb.run(check_state=True)
+    assert T.last_sim_stats()["engine"] == T.ENGINE_REPLAY
+    T.set_sim_engine(T.ENGINE_STACK)
+    assert torch.equal(rb.uncached, bt.uncached)
+    assert torch.equal(rb.hist, bt.hist)
+    assert rb.results_numpy().tobytes() == bt.results_numpy().tobytes()
 
 
 # ----------------------------------------------------------------------------- tail metrics
@@ -372,11 +390,14 @@ def test_tail_metrics_against_oracle(T):
         assert o["n_clamped"] == 0
 
 
-def test_tail_metrics_clamps_and_counts(T):
+def test_tail_metrics_never_truncates(T):
+    """b above max_b is TLRU_ERANGE, not a clamped percentile (never silent truncation)."""
     b = np.array([1, 5, 9, 70, 80], np.uint16)
     dev = torch.from_numpy(b.view(np.int16).copy()).cuda()
-    out = T.tail_metrics(dev, [0, 5], [0], [0.0], [0], 1.0, 50)
-    assert out[0]["n_clamped"] == 2 and out[0]["max_b"] == 50
+    with pytest.raises(T.TlruError, match="ERANGE.*2 values"):
+        T.tail_metrics(dev, [0, 5], [0], [0.0], [0], 1.0, 50)
+    out = T.tail_metrics(dev, [0, 5], [0], [0.0], [0], 1.0, 80)
+    assert out[0]["n_clamped"] == 0 and out[0]["max_b"] == 80 and out[0]["p99"] == 80
 
 
 # ----------------------------------------------------------------------------- errors through the ABI

@@ -81,3 +81,28 @@ def test_gather_identical_for_any_world_size(world):
         assert p.exitcode == 0
     expected = fake_results(config5_rows(4)).tobytes()
     assert got == expected
+
+
+def test_plan_strong_partitions_and_balances():
+    """Strong-scaling shards (sweep.plan_strong): a deterministic partition, contiguous in the stack
+    engine's (trace, D, C) order, within the modelled optimum for contiguous cuts, and cutting inside
+    traces so 10 traces spread over 8 ranks (whole-trace sharding would cap efficiency at 10/16)."""
+    from paper_2510_15152_b200.sweep import plan_strong, row_d_key, shard_cost
+    rows = config5_rows(10)
+    total = shard_cost(rows, range(len(rows)))
+    for world in (1, 2, 3, 4, 8, 16):
+        sh = plan_strong(rows, world)
+        assert len(sh) == world and sh == plan_strong(rows, world)
+        assert sorted(i for s in sh for i in s) == list(range(len(rows)))
+        order = sorted(range(len(rows)), key=lambda i: (rows[i][0], row_d_key(rows[i]), rows[i][2], i))
+        pos = {i: k for k, i in enumerate(order)}
+        for s in sh:  # contiguous in the engine's order
+            if s:
+                ks = sorted(pos[i] for i in s)
+                assert ks[-1] - ks[0] + 1 == len(ks)
+        costs = [shard_cost(rows, s) for s in sh]
+        assert max(costs) <= total / world * 1.25 + 0.61  # one extra trace pass per shard at most
+    sh8 = plan_strong(rows, 8)
+    assert all(len({rows[i][0] for i in s}) <= 2 for s in sh8)
+    assert max(shard_cost(rows, s) for s in sh8) < total / 8 / 0.8  # modelled efficiency > 80%
+    assert plan_strong(rows[:3], 5)[3:] == [[], []]  # more ranks than instances: idle ranks

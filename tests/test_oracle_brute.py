@@ -24,14 +24,15 @@ def test_thm2_tlru_attains_optimal_expected_tel():
     (Alg. 1, Q_hat = Q) minimizes expected TEL in the belief MDP (App. B).
     Also checks the test has power: LRU and the weak-budget reading miss the optimum."""
     n = lru_opt = weak_opt = 0
-    for inst in _instances(120, 11):
+    for inst in _instances(240, 11):  # >= 200 instances (BASELINE config 2, SURVEY c.5)
         vo = belief_mdp_value(**inst)
         vt = belief_mdp_value(**inst, policy="tlru")
         assert vt == vo, inst
         lru_opt += belief_mdp_value(**inst, policy="lru") == vo
         weak_opt += belief_mdp_value(**inst, policy="tlru", budget="weak") == vo
         n += 1
-    assert lru_opt < n - 20 and weak_opt < n - 20
+    assert n >= 200
+    assert lru_opt < n - 40 and weak_opt < n - 40
 
 
 def test_thm2_corollary_lru_optimal_at_xi0():
