@@ -317,10 +317,11 @@ class Sweep:
                                                 T._ptr(self.pxim), T._ptr(self.pslo), self.alpha,
                                                 T._ptr(self.pooled_tails), T._stream(stream)))
 
-    def step(self, stream, gen_stream=None, sim_streams=None) -> None:
+    def step(self, stream, gen_stream=None, sim_streams=None, combine: bool = True) -> None:
         """One pass: pipelined when gen_stream / sim_streams are given (trace j+1 generated on the
         generation stream while traces are simulated on alternating simulation streams), else
-        sequential on `stream`."""
+        sequential on `stream`.  combine=False skips row a10 (tools/scale_probe.py times one rank's
+        share alone on one GPU)."""
         with torch.cuda.stream(stream):
             self.pooled.zero_()
         if gen_stream is None:
@@ -328,7 +329,8 @@ class Sweep:
                 self.gen(j, stream)
             for j in range(len(self.batches)):
                 self.simulate(j, stream)
-            self.combine(stream)
+            if combine:
+                self.combine(stream)
             return
         ev0 = torch.cuda.Event()
         ev0.record(stream)
@@ -345,7 +347,8 @@ class Sweep:
         stream.wait_stream(gen_stream)
         for sB in sim_streams:
             stream.wait_stream(sB)
-        self.combine(stream)
+        if combine:
+            self.combine(stream)
 
     # -- host views (tests / reports; synchronize)
     def table_numpy(self) -> np.ndarray:
