@@ -196,6 +196,7 @@ END_AWARE = 3
 LENGTH_AWARE = 4
 TAIL_BELADY = 5  # Thm 1 hindsight policy, Reading #26
 TLRU_FORCED = 7  # T-LRU under forced caching (App. C), Reading #28
+BELADY_FORCED = 8  # Tail-Optimized Belady under forced caching (App. C), Reading #29
 ET_LRU = 6  # Def. 1 / Alg. 2, Reading #27 -- see replay_etlru
 
 

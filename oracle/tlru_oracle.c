@@ -392,8 +392,14 @@ static void list_push_tail(conv_state* s, list_ends* l, int which, int64_t i) {
    eviction step scans it for the maximum next arrival (never-returning = +infinity; ties
    among those by lower conversation id, SPEC S:248 -- unobservable: they never return
    and are all free).  Counters as oracle_replay (Phase 1 -> evicted_trim). */
+/* forced != 0: Tail-Optimized Belady under forced caching (App. C: "Theorem 1
+   continues to hold" with constraint (3) as an equality), Reading #29: the post-decision state
+   holds theta's whole history, so theta takes no part in either phase; only if the other
+   conversations cannot make room (theta alone exceeds C) does theta lose its tail blocks --
+   above-budget blocks first, they are the tail -- counted with the Phase-2 evictions (as forced
+   T-LRU, Reading #28). */
 static int replay_tail_belady(const uint32_t* dense, int64_t n, const uint32_t* q, const uint32_t* a,
-                              const uint64_t* nxt, uint64_t E, uint64_t C, uint64_t xi,
+                              const uint64_t* nxt, uint64_t E, uint64_t C, uint64_t xi, int forced,
                               uint64_t* b_out, uint64_t* counters_out) {
     uint64_t* X = (uint64_t*)calloc((size_t)(n ? n : 1), 8);   /* cached blocks x_i */
     uint64_t* L = (uint64_t*)calloc((size_t)(n ? n : 1), 8);   /* history length L_i */
@@ -433,6 +439,7 @@ static int replay_tail_belady(const uint32_t* dense, int64_t n, const uint32_t* 
                     int64_t best = -1;
                     for (int64_t k = 0; k < nres; ++k) {
                         int64_t i = res[k];
+                        if (forced && i == c) continue;   /* theta is kept whole */
                         uint64_t avail = phase == 1 ? sur[i] : X[i];
                         if (avail == 0) continue;
                         if (best < 0 || nx[i] > nx[best] || (nx[i] == nx[best] && i < best)) best = i;
@@ -445,6 +452,14 @@ static int replay_tail_belady(const uint32_t* dense, int64_t n, const uint32_t* 
                     used -= k;
                     over -= k;
                 }
+            }
+            if (forced && over > 0) {   /* theta alone exceeds C: its tail blocks go */
+                uint64_t k = over;
+                X[c] -= k;
+                sur[c] -= sur[c] < k ? sur[c] : k;
+                used -= k;
+                over = 0;
+                ev_far += k;
             }
             /* drop conversations left with no cached block from the resident array */
             int64_t w = 0;
@@ -474,6 +489,7 @@ static int replay_tail_belady(const uint32_t* dense, int64_t n, const uint32_t* 
    evicted_lru, max_occupancy}; released blocks are not evictions.  5 = Tail-Optimized
    Belady (Thm 1, replay_tail_belady above; evicted_lru counts its Phase-2
    furthest-in-future evictions).  7 = T-LRU under forced caching (App. C, Reading #28).
+   8 = Tail-Optimized Belady under forced caching (App. C, Reading #29).
    Returns 0, or -1 on allocation failure. */
 int oracle_replay(const uint32_t* conv, const uint32_t* q, const uint32_t* a, uint64_t E,
                   int policy, uint64_t C, uint64_t xi, uint64_t q_hat, uint64_t threshold,
@@ -494,8 +510,8 @@ int oracle_replay(const uint32_t* conv, const uint32_t* q, const uint32_t* a, ui
         seen[dense[t]] = (int64_t)t;
     }
     free(seen);
-    if (policy == 5) {  /* Tail-Optimized Belady (Thm 1) */
-        int rc = replay_tail_belady(dense, n, q, a, nxt, E, C, xi, b_out, counters_out);
+    if (policy == 5 || policy == 8) {  /* Tail-Optimized Belady (Thm 1); 8: under forced caching */
+        int rc = replay_tail_belady(dense, n, q, a, nxt, E, C, xi, policy == 8, b_out, counters_out);
         free(s);
         free(dense);
         free(nxt);

@@ -120,3 +120,58 @@ def test_special_cases_and_invariants(seed):
             if xi == 0:
                 # xi = 0: only never-returning conversations hold free blocks
                 pass
+
+
+# ----------------------------------------------------------------------------- forced caching (App. C)
+def test_forced_belady_hand_vector():
+    """Fig. 1 under forced caching (Reading #29): B must keep its 100 blocks, so A pays 200."""
+    v = json.load(open(os.path.join(GOLDEN, "tail_belady.json")))["fig1_forced"]
+    r = O.replay(v["conv"], v["q"], v["a"], O.BELADY_FORCED, v["C"], v["xi"])
+    assert [int(x) for x in r.b] == v["b"]
+    assert [r.evicted_trim, r.evicted_lru] == v["evicted"] and r.max_occupancy == v["max_occupancy"]
+    assert tel(r.b, v["xi"]) == v["tel"] == hindsight_opt(np.array(v["conv"]), np.array(v["q"]),
+                                                           np.array(v["a"]), v["C"], v["xi"], forced=True)
+
+
+def test_forced_belady_attains_the_forced_hindsight_optimum():
+    """App. C: Theorem 1 continues to hold under forced caching -- the forced
+    Tail-Optimized Belady's TEL equals the exact forced hindsight optimum (Eq. 5 with constraint
+    (3) as an equality; a DP over every feasible schedule, no eviction rule in it) on tiny traces,
+    for every xi.  Power: it differs from the optional-caching Belady on a quarter of them, and it
+    never exceeds forced T-LRU."""
+    rnd = random.Random(9)
+    n = differs = 0
+    for seed in range(690):
+        if seed < 400:
+            conv, q, a = tiny_trace(seed, max_conv=3, max_turns=2, qs=(1, 2), as_=(0, 1))
+        else:
+            conv, q, a = tiny_trace(1000 + seed, max_conv=3, max_turns=3, qs=(1, 2, 3), as_=(0, 1, 2))
+            if len(conv) > 7:
+                continue
+        C, xi = rnd.randint(0, 6), rnd.randint(0, 4)
+        r = O.replay(conv, q, a, O.BELADY_FORCED, C, xi)
+        got = tel(r.b, xi)
+        assert got == hindsight_opt(conv, q, a, C, xi, forced=True), (seed, C, xi)
+        assert got <= tel(O.replay(conv, q, a, O.TLRU_FORCED, C, xi, 1).b, xi)
+        differs += got != tel(O.replay(conv, q, a, O.TAIL_BELADY, C, xi).b, xi)
+        n += 1
+    assert n >= 600 and differs >= 40
+
+
+def test_forced_belady_invariants():
+    """Occupancy <= C after every request, b >= q, first turns b = q, eviction identity
+    (inserted - cached at the end), and theta keeps min(L, C) blocks after its own request."""
+    for seed in range(30):
+        conv, q, a = random_trace(seed, 400, 20, q_max=6, a_max=4)
+        for C in (0, 3, 17, 60, 10 ** 4):
+            for xi in (0, 4, 12):
+                r = O.replay(conv, q, a, O.BELADY_FORCED, C, xi)
+                b = r.b.astype(np.int64)
+                assert r.max_occupancy <= C and np.all(b >= q)
+                seen = set()
+                for t, c in enumerate(conv.tolist()):
+                    if c not in seen:
+                        assert b[t] == q[t]
+                        seen.add(c)
+                total_in = int(a.astype(np.int64).sum() + b.sum())
+                assert r.evicted_trim + r.evicted_lru == total_in - min(C, total_in)
