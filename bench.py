@@ -238,6 +238,11 @@ def workload_global(name: str):
         rows = [(t, 7, C, xi, Q_HAT, SLO_BLOCKS) for t in range(n) for C in CAPS_CONFIG5 for xi in (4, 8, 16, 24)]
         return rows, n, ("T-LRU under forced caching (App. C): 10 seeds x 10^6-conversation traces x 25 capacities "
                          "x xi in {4, 8, 16, 24} = 1000 instances (replay engine)")
+    if name == "forced_belady":
+        rows = [(t, 8, C, xi, Q_HAT, SLO_BLOCKS) for t in range(n) for C in CAPS_CONFIG5 for xi in (4, 8, 16, 24)]
+        return rows, n, ("Tail-Optimized Belady under forced caching (App. C, P:657-662): 10 seeds x "
+                         "10^6-conversation traces x 25 capacities x xi in {4, 8, 16, 24} = 1000 instances "
+                         "(replay engine)")
     if name == "config5x3":
         return config5_rows(n, threshold_lru=True), n, (
             "config5 sweep with the paper's three policies: 10 seeds x 10^6-conversation traces x 25 capacities x "
@@ -559,7 +564,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-replay", action="store_true", help="skip timing the replay engine")
     ap.add_argument("--replay-instances", type=int, default=0, help="limit the replay-engine sample (0 = all of seed 0)")
-    ap.add_argument("--config", choices=("config5", "config5x3", "spectrum", "etlru", "forced", "config4"),
+    ap.add_argument("--config", choices=("config5", "config5x3", "spectrum", "etlru", "forced", "forced_belady",
+                                         "config4"),
                     default="config5")
     ap.add_argument("--scaling", choices=("strong", "weak"), default="strong",
                     help="strong: the one sweep sharded over the ranks (default); weak: every rank its own seeds")

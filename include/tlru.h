@@ -42,7 +42,7 @@ typedef enum {
   TLRU_EINVAL = 1,       /* bad argument or configuration (block_tokens == 0, rate <= 0, q == 0, ...) */
   TLRU_ERANGE = 2,       /* buffer / workspace too small, or a value exceeds its field width (J > 65535) */
   TLRU_ECUDA = 3,        /* CUDA runtime error; tlru_last_error() carries cudaGetErrorString */
-  TLRU_EUNSUPPORTED = 4, /* policy family not built (policy > TLRU_POLICY_TLRU_FORCED) */
+  TLRU_EUNSUPPORTED = 4, /* policy family not built (policy > TLRU_POLICY_BELADY_FORCED) */
   TLRU_ESTATE = 5        /* internal per-chain state pool exhausted with no fallback left */
 } tlru_status;
 
@@ -206,6 +206,12 @@ tlru_status tlru_trace_from_turns(const uint32_t* conv, const uint16_t* q, const
  *   post-decision state must hold theta's whole history -- Phases 1 and 2 skip
  *   theta; only if theta alone exceeds C does it lose tail blocks (counted in
  *   evicted_lru).  With xi <= q_hat it equals LRU.  Replay engine only.
+ * Tail-Optimized Belady under forced caching (App. C: "Theorem 1
+ *   continues to hold" with constraint (3) as an equality; Reading #29): the
+ *   Tail-Optimized Belady rule with theta excluded from both phases; only if
+ *   theta alone exceeds C does it lose tail blocks, above-budget ones first
+ *   (counted in evicted_lru).  Its TEL is the forced hindsight optimum.  Replay
+ *   engine only.
  * ------------------------------------------------------------------------ */
 enum {
   TLRU_POLICY_LRU = 0,
@@ -215,7 +221,8 @@ enum {
   TLRU_POLICY_LENGTH_AWARE = 4,
   TLRU_POLICY_TAIL_BELADY = 5,
   TLRU_POLICY_ET_LRU = 6,
-  TLRU_POLICY_TLRU_FORCED = 7 /* > 7 -> TLRU_EUNSUPPORTED */
+  TLRU_POLICY_TLRU_FORCED = 7,
+  TLRU_POLICY_BELADY_FORCED = 8 /* > 8 -> TLRU_EUNSUPPORTED */
 };
 
 typedef struct {

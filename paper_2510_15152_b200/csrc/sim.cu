@@ -250,7 +250,8 @@ __global__ void __launch_bounds__(32) sim_kernel(const ItemDev* __restrict__ ite
           if (active) {
             const uint32_t La = sim_La(ev);
             const uint32_t s0 = nxk == TLRU_NONE ? 0u : min(La, lp.xi > qn ? lp.xi - qn : 0u);
-            const uint32_t b = chain_request_belady(c, st, base + k, sim_J(ev), La, nxk, s0);
+            const uint32_t b = chain_request_belady(c, st, base + k, sim_J(ev), La, nxk, s0,
+                                                    lp.policy == TLRU_POLICY_BELADY_FORCED);
             bst[lane * BST_STRIDE + k] = static_cast<uint16_t>(b);
             if (c.overflow) active = false;
           }
@@ -354,7 +355,7 @@ __global__ void aware_fix_kernel(const LaneDev* __restrict__ lanes, const uint32
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nal; i += gridDim.x * blockDim.x) {
     const LaneDev lp = lanes[alane[i]];
     const TraceDev tr = traces[atrace[i]];
-    const bool bel = lp.policy == TLRU_POLICY_TAIL_BELADY;
+    const bool bel = lp.policy == TLRU_POLICY_TAIL_BELADY || lp.policy == TLRU_POLICY_BELADY_FORCED;
     const uint32_t nseg = static_cast<uint32_t>((tr.E + aw.seg_len - 1) / aw.seg_len);
     GlobalState st{tau_pool + size_t(i) * Wp, X_pool + size_t(i) * Wp, S_pool + size_t(i) * Wp};
     bool failed = false, carry = false;  // carry: the pool holds the exact state at the end of segment k - 1
@@ -404,7 +405,8 @@ __global__ void aware_fix_kernel(const LaneDev* __restrict__ lanes, const uint32
         if (bel) {
           const uint32_t La = sim_La(ev);
           const uint32_t s0 = nx == TLRU_NONE ? 0u : min(La, lp.xi > qn ? lp.xi - qn : 0u);
-          bout[lp.boff + e] = static_cast<uint16_t>(chain_request_belady(c, st, e, sim_J(ev), La, nx, s0));
+          bout[lp.boff + e] = static_cast<uint16_t>(
+              chain_request_belady(c, st, e, sim_J(ev), La, nx, s0, lp.policy == TLRU_POLICY_BELADY_FORCED));
           continue;
         }
         const uint32_t Dcur = lp.policy == TLRU_POLICY_LENGTH_AWARE ? (lp.xi > qn ? lp.xi - qn : 0u) : lp.D;
@@ -476,7 +478,7 @@ static int w_class(uint32_t C, uint32_t nconv) {
 
 static bool is_aware(const tlru_instance& in) { return in.policy >= TLRU_POLICY_END_AWARE; }
 static uint32_t aware_kind(const tlru_instance& in) {
-  if (in.policy == TLRU_POLICY_TAIL_BELADY) return kAwareBelady;
+  if (in.policy == TLRU_POLICY_TAIL_BELADY || in.policy == TLRU_POLICY_BELADY_FORCED) return kAwareBelady;
   if (in.policy == TLRU_POLICY_TLRU_FORCED) return kAwareForced;
   return is_aware(in) ? kAwareTLRU : 0u;
 }
@@ -530,9 +532,10 @@ static tlru_status make_plan(const tlru_trace* traces, uint32_t nt, const tlru_i
   for (uint32_t i = 0; i < ni; ++i) {
     const tlru_instance& in = inst[i];
     if (in.trace >= nt) TLRU_FAIL(TLRU_EINVAL, "instance %u: trace index %u out of range", i, in.trace);
-    if (in.policy > TLRU_POLICY_TLRU_FORCED)
-      TLRU_FAIL(TLRU_EUNSUPPORTED, "instance %u: policy %u is not built (0..7: LRU, T-LRU, Threshold-LRU, "
-                "End-Aware, Length-Aware, Tail-Optimized Belady, ET-LRU, forced-caching T-LRU)", i, in.policy);
+    if (in.policy > TLRU_POLICY_BELADY_FORCED)
+      TLRU_FAIL(TLRU_EUNSUPPORTED, "instance %u: policy %u is not built (0..8: LRU, T-LRU, Threshold-LRU, "
+                "End-Aware, Length-Aware, Tail-Optimized Belady, ET-LRU, forced-caching T-LRU, forced-caching "
+                "Tail-Optimized Belady)", i, in.policy);
     if (in.policy == TLRU_POLICY_ET_LRU) {
       if (g_et_mu < 0.0) TLRU_FAIL(TLRU_EINVAL, "instance %u: ET-LRU needs tlru_set_etlru_model first", i);
       if (traces[in.trace].num_events > 0 && !traces[in.trace].time_ticks)
@@ -553,7 +556,7 @@ static tlru_status make_plan(const tlru_trace* traces, uint32_t nt, const tlru_i
     // conversations (128 or 256 entries) or splitting End- from Length-Aware lanes was slower on
     // the spectrum workload (wider capacity ranges per warp, more frequent compaction).
     // Forced-caching chains keep LRU-like state: up to 1024 entries of 6 B (no surplus array).
-    if (in.policy == TLRU_POLICY_TAIL_BELADY && g_opt_w < 0) {
+    if ((in.policy == TLRU_POLICY_TAIL_BELADY || in.policy == TLRU_POLICY_BELADY_FORCED) && g_opt_w < 0) {
       // entries hold X >= 1 (tombstones are compacted before the state counts as full), so
       // W > C never overflows; the live conversations of a trace bound it too (<= ~91 on the
       // preset): 128 entries, larger states are re-run by the fix-up from global memory

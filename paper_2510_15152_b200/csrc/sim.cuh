@@ -357,7 +357,8 @@ __device__ __forceinline__ uint32_t chain_request_aware(ChainRegs& c, const St& 
 // compaction.  A new key goes to its sorted position, shifting the shorter side (head - 1 or
 // tail + 1 must be free; else tombstones are compacted; else the chain overflows).
 template <class St>
-__device__ __forceinline__ bool belady_insert(ChainRegs& c, const St& st, uint32_t key, uint32_t x, uint32_t s) {
+__device__ __forceinline__ bool belady_insert(ChainRegs& c, const St& st, uint32_t key, uint32_t x, uint32_t s,
+                                              uint32_t& pos) {
   uint32_t lo = c.head, n = c.tail - c.head;
   while (n > 0) {  // lower_bound of key in T[head, tail)
     const uint32_t half = n >> 1;
@@ -406,14 +407,19 @@ __device__ __forceinline__ bool belady_insert(ChainRegs& c, const St& st, uint32
   st.T(lo) = key;
   st.Xr(lo) = static_cast<uint16_t>(x);
   st.Sr(lo) = static_cast<uint16_t>(s);
+  pos = lo;
   return true;
 }
 
 // Request at event e: J, La from the sim view, nx = theta's next arrival (TLRU_NONE: never),
 // s0 = min(La, max(xi - q_next, 0)) = La - (La + q_next - xi)^+ (unused when nx is NONE).
+// forced (App. C; Reading #29): the post-decision state holds theta's whole history,
+// so theta's blocks take part in neither phase; Phase 2 then skips theta's entry (entries before
+// it that it empties stay as tombstones), and only if theta alone exceeds C does it lose its tail
+// blocks -- its above-budget ones first (they are the tail) -- counted in ev_lru.
 template <class St>
 __device__ __forceinline__ uint32_t chain_request_belady(ChainRegs& c, const St& st, uint32_t e, uint32_t J,
-                                                         uint32_t La, uint32_t nx, uint32_t s0) {
+                                                         uint32_t La, uint32_t nx, uint32_t s0, bool forced = false) {
   uint32_t x_old = 0;
   if (c.head < c.tail && st.T(c.head) == e) {  // theta's entry: the smallest key
     x_old = st.Xr(c.head);
@@ -422,14 +428,20 @@ __device__ __forceinline__ uint32_t chain_request_belady(ChainRegs& c, const St&
   }
   const uint32_t b = J - x_old;  // job - x
   c.used += La - x_old;          // X_theta <- L_theta (Reading #7)
+  uint32_t tpos = 0xFFFFFFFFu;   // theta's entry (forced: excluded from both phases)
+  uint32_t tdead = 0;            // forced: theta's never-returning blocks, held apart from dead
   if (nx == TLRU_NONE) {
-    c.dead += La;                // budget 0: every block free
+    if (forced) tdead = La;
+    else c.dead += La;           // budget 0: every block free
   } else {
-    if (!belady_insert(c, st, nx, La, s0)) {
+    if (!belady_insert(c, st, nx, La, s0, tpos)) {
       c.overflow = true;
       return b;
     }
-    c.fsum += s0;
+    if (!forced) {
+      c.fsum += s0;
+      tpos = 0xFFFFFFFFu;
+    }
   }
   if (c.used > c.C) {
     uint32_t over = c.used - c.C;
@@ -440,6 +452,7 @@ __device__ __forceinline__ uint32_t chain_request_belady(ChainRegs& c, const St&
     c.ev_trim += kd;
     for (uint32_t j = c.tail; over > 0 && c.fsum > 0 && j > c.head;) {
       --j;
+      if (j == tpos) continue;
       const uint32_t s = st.Sr(j);
       if (s == 0) continue;
       const uint32_t take = min(s, over);
@@ -449,17 +462,43 @@ __device__ __forceinline__ uint32_t chain_request_belady(ChainRegs& c, const St&
       over -= take;
       c.ev_trim += take;
     }
-    // Phase 2: furthest-in-future, partial; every S is 0 here
-    while (over > 0) {
-      const uint32_t x = st.Xr(c.tail - 1);
-      const uint32_t take = min(x, over);
-      st.Xr(c.tail - 1) = static_cast<uint16_t>(x - take);
-      over -= take;
-      c.ev_lru += take;
-      if (x == take) --c.tail;
+    // Phase 2: furthest-in-future, partial; every S is 0 here (theta's aside)
+    if (tpos == 0xFFFFFFFFu) {
+      while (over > 0 && c.tail > c.head) {
+        const uint32_t x = st.Xr(c.tail - 1);
+        const uint32_t take = min(x, over);
+        st.Xr(c.tail - 1) = static_cast<uint16_t>(x - take);
+        over -= take;
+        c.ev_lru += take;
+        if (x == take) --c.tail;
+      }
+    } else {
+      for (uint32_t j = c.tail; over > 0 && j > c.head;) {
+        --j;
+        if (j == tpos) continue;
+        const uint32_t x = st.Xr(j);
+        const uint32_t take = min(x, over);
+        st.Xr(j) = static_cast<uint16_t>(x - take);
+        over -= take;
+        c.ev_lru += take;
+      }
+    }
+    if (over > 0) {  // forced: theta alone exceeds C -- its tail blocks go, above-budget first
+      if (tpos == 0xFFFFFFFFu) {
+        tdead -= over;
+      } else {
+        const uint32_t s = st.Sr(tpos);
+        st.Sr(tpos) = static_cast<uint16_t>(s - min(s, over));
+        st.Xr(tpos) = static_cast<uint16_t>(st.Xr(tpos) - over);
+      }
+      c.ev_lru += over;
     }
     while (c.tail > c.head && st.Xr(c.tail - 1) == 0) --c.tail;
     c.used = c.C;
+  }
+  if (forced) {  // theta rejoins the state
+    if (tpos != 0xFFFFFFFFu) c.fsum += st.Sr(tpos);
+    c.dead += tdead;
   }
   c.max_occ = max(c.max_occ, c.used);
   return b;
