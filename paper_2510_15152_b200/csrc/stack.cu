@@ -604,8 +604,16 @@ __global__ void __launch_bounds__(S_THREADS, 4) s2_win_kernel(const uint64_t* __
   for (uint32_t d = 0; d < ch.nd; ++d) A[uint64_t(d) * Astride + e] = static_cast<AT>(min(anf_s[d][t], amax));
 }
 
-struct GroupDev {  // <= group-size instances of one chunk sharing D[d]: [inst0 + k0, inst0 + k0 + n)
-  uint32_t d, k0, n, pad;
+// An s2_out group of one chunk row d.  kind 0 (writer): instance rows [inst0 + k0, inst0 + k0 + n)
+// (sorted by C), whose b rows it writes.  kind 1 (histograms): the row's distinct capacities
+// ("cells" -- instances with equal (D, C) have equal b on every event) [k0, k0 + n) of the chunk's
+// cell table, whose histograms of b it builds: once per cell instead of once per instance.
+struct GroupDev {
+  uint32_t d, k0, n, kind;
+};
+
+struct CellDev {  // instances [k0, k0 + m) of the StackInstDev table (batch-global) share (d, C)
+  uint32_t C, k0, m, d;
 };
 
 // s2_out: one CTA = (instance group, event range).  Per 4 events per thread: b for every
@@ -621,11 +629,12 @@ struct GroupDev {  // <= group-size instances of one chunk sharing D[d]: [inst0 
 __global__ void __launch_bounds__(256) s2_cnt_kernel(const ChunkDev* __restrict__ chunk,
                                                      const StackInstDev* __restrict__ insts,
                                                      const GroupDev* __restrict__ groups, uint32_t tcap,
-                                                     uint8_t* __restrict__ cnt_g) {
+                                                     uint8_t* __restrict__ cnt_g, const CellDev* __restrict__ cells) {
   __shared__ uint32_t C_s[GI_MAX];
   const GroupDev g = groups[blockIdx.x];
   const uint32_t t = threadIdx.x;
-  if (t < GI_MAX) C_s[t] = t < g.n ? insts[chunk->inst0 + g.k0 + t].C : 0xFFFFFFFFu;
+  if (t < GI_MAX)
+    C_s[t] = t < g.n ? (g.kind ? cells[g.k0 + t].C : insts[chunk->inst0 + g.k0 + t].C) : 0xFFFFFFFFu;
   __syncthreads();
   if (C_s[g.n - 1] >= tcap) return;
   uint8_t* row = cnt_g + uint64_t(blockIdx.x) * ((tcap + 15u) & ~15u);
@@ -647,7 +656,8 @@ __global__ void __launch_bounds__(256, 4) s2_out_kernel(const ChunkDev* __restri
                                                      const uint32_t* __restrict__ LbJ, uint32_t E, uint32_t range_len,
                                                      uint32_t bins, uint32_t rows, uint32_t tcap, bool aligned16,
                                                      uint16_t* __restrict__ bout, uint32_t* __restrict__ hist,
-                                                     const uint4* __restrict__ cnt_g, uint32_t range0) {
+                                                     const uint4* __restrict__ cnt_g, uint32_t range0,
+                                                     const CellDev* __restrict__ cells, uint32_t* __restrict__ gcell) {
   // [rows >= group size][hb2] difference rows, two 16-bit counters per word (bins 2v, 2v+1).  The
   // counters wrap into each other, but a word's final value is lo + 65536 * hi (mod 2^32) and
   // decodes exactly while |lo|, |hi| <= 32767, which range_len <= OUT_RANGE_MAX guarantees.
@@ -662,19 +672,29 @@ __global__ void __launch_bounds__(256, 4) s2_out_kernel(const ChunkDev* __restri
   const GroupDev g = groups[blockIdx.x];
   const uint32_t rid = range0 + blockIdx.y;
   const uint32_t t = threadIdx.x, n = g.n;
+  const bool hist_group = g.kind != 0;  // else a writer group: b rows only
   const uint32_t D = chunk->D[g.d], nsat = totals->nsat[g.d], inst0 = chunk->inst0;
   if (t < GI_MAX) {
     if (t < n) {
-      const StackInstDev in = insts[inst0 + g.k0 + t];
-      C_s[t] = in.C;
-      C2_s[t] = in.C * 0x10001u;  // used only when C <= 65535
-      inst_s[t] = in.inst;
-      off_s[t] = in.boff;
+      if (hist_group) {  // a cell: its capacity, its first instance's row (warm-up b), its gcell row
+        const CellDev cl = cells[g.k0 + t];
+        C_s[t] = cl.C;
+        C2_s[t] = cl.C * 0x10001u;
+        inst_s[t] = g.k0 + t;
+        off_s[t] = insts[cl.k0].boff;
+      } else {
+        const StackInstDev in = insts[inst0 + g.k0 + t];
+        C_s[t] = in.C;
+        C2_s[t] = in.C * 0x10001u;  // used only when C <= 65535
+        inst_s[t] = in.inst;
+        off_s[t] = in.boff;
+      }
     } else {
       C_s[t] = 0xFFFFFFFFu;  // sentinel: the branch-free searches below never count it
     }
   }
-  for (uint32_t k = t; k < n * hb2; k += blockDim.x) hw[k] = 0;  // row n (never read) is not kept
+  if (hist_group)
+    for (uint32_t k = t; k < n * hb2; k += blockDim.x) hw[k] = 0;  // row n (never read) is not kept
   __syncthreads();
   const bool packed_all = C_s[n - 1] <= 65535u;  // capacities are sorted
   const bool use_cnt = C_s[n - 1] < tcap;
@@ -690,7 +710,7 @@ __global__ void __launch_bounds__(256, 4) s2_out_kernel(const ChunkDev* __restri
     while (j < n && C_s[j] == C_s[t]) ++j;
     run_s[t] = j;
   }
-  if (use_cnt) {  // the group's table, built once by s2_cnt_kernel
+  if (hist_group && use_cnt) {  // the group's table, built once by s2_cnt_kernel
     const uint4* src = cnt_g + uint64_t(blockIdx.x) * ((tcap + 15u) >> 4);
     for (uint32_t k = t; k < (tcap + 15u) >> 4; k += blockDim.x) reinterpret_cast<uint4*>(cnt)[k] = src[k];
   }
@@ -741,6 +761,7 @@ __global__ void __launch_bounds__(256, 4) s2_out_kernel(const ChunkDev* __restri
     if (e >= e_end) continue;
     const uint32_t nv = min(EV, e_end - e);
     const bool warm = (e / S_THREADS) < nsat;  // the 8 events share a 256-event block
+    if (warm && !hist_group) continue;  // b written by s2_warm
     if (warm) {  // b written by s2_warm: histogram only, one range update per run of equal C
       for (uint32_t i = 0; i < n;) {
         const uint16_t* row = bout + off_s[i] + e;
@@ -769,6 +790,7 @@ __global__ void __launch_bounds__(256, 4) s2_out_kernel(const ChunkDev* __restri
       if constexpr (sizeof(AT) == 2) return half(A2, u);
       else return static_cast<uint32_t>(Ad[e + u]);
     };
+    if (hist_group) {
     // ---- histograms: per event, prefix (b = J), middle (individual), suffix (b = J - N).
     // k1 = #{C_i <= a}, k2 = #{C_i < a + N} = #{C_i <= a + N - 1}: table lookups (all 8 events
     // before the first atomic), else branch-free searches
@@ -798,15 +820,17 @@ __global__ void __launch_bounds__(256, 4) s2_out_kernel(const ChunkDev* __restri
       }
       if (hi < n) hadd(hi, b1, 1);
     }
-    // ---- b for every instance of the group: b = J - min(N, (C - A)^+)
+    continue;
+    }
+    // ---- b for every instance of the group: b = J - min(N, (C - A)^+), once per run of equal C
     if (packed_all && aligned16 && nv == EV) {
-#pragma unroll 2
-      for (uint32_t i = 0; i < n; ++i) {
-        const uint32_t C2 = C2_s[i];
+      for (uint32_t i = 0; i < n;) {
+        const uint32_t C2 = C2_s[i], j = run_s[i];
         uint32_t w[4];
 #pragma unroll
         for (int k = 0; k < 4; ++k) w[k] = __vsub2(J2[k], __vminu2(N2[k], __vsub2(__vmaxu2(C2, A2[k]), A2[k])));
-        *reinterpret_cast<uint4*>(bout + off_s[i] + e) = make_uint4(w[0], w[1], w[2], w[3]);
+        const uint4 wv = make_uint4(w[0], w[1], w[2], w[3]);
+        for (; i < j; ++i) *reinterpret_cast<uint4*>(bout + off_s[i] + e) = wv;
       }
     } else {
       for (uint32_t i = 0; i < n; ++i) {
@@ -820,8 +844,9 @@ __global__ void __launch_bounds__(256, 4) s2_out_kernel(const ChunkDev* __restri
       }
     }
   }
+  if (!hist_group) return;
   __syncthreads();
-  for (uint32_t v2 = t; v2 < hb2; v2 += blockDim.x) {  // prefix over the instance axis -> histograms
+  for (uint32_t v2 = t; v2 < hb2; v2 += blockDim.x) {  // prefix over the cell axis -> cell histograms
     int run0 = 0, run1 = 0;
     const uint32_t v = 2 * v2;
     for (uint32_t i = 0; i < n; ++i) {
@@ -829,11 +854,21 @@ __global__ void __launch_bounds__(256, 4) s2_out_kernel(const ChunkDev* __restri
       const int lo = static_cast<int16_t>(w & 0xFFFFu);
       run0 += lo;
       run1 += static_cast<int>(w - static_cast<uint32_t>(lo)) >> 16;
-      uint32_t* h = hist + uint64_t(inst_s[i]) * bins + v;
+      uint32_t* h = gcell + uint64_t(inst_s[i]) * bins + v;
       if (run0) atomicAdd(h, static_cast<uint32_t>(run0));
       if (run1) atomicAdd(h + 1, static_cast<uint32_t>(run1));  // run1 != 0 implies v + 1 < bins
     }
   }
+}
+
+// Per (instance of the chunk, bin): the instance's histogram row = its cell's (s2_out's histogram
+// groups build one per distinct (D, C)).
+__global__ void s2_instcopy_kernel(const StackInstDev* __restrict__ insts, const uint32_t* __restrict__ inst_cell,
+                                   uint32_t ninst, uint32_t bins, const uint32_t* __restrict__ gcell,
+                                   uint32_t* __restrict__ hist) {
+  const uint32_t v = blockIdx.x * blockDim.x + threadIdx.x, k = blockIdx.y;
+  if (v >= bins || k >= ninst) return;
+  hist[uint64_t(insts[k].inst) * bins + v] = gcell[uint64_t(inst_cell[k]) * bins + v];
 }
 
 // ----------------------------------------------------------------------------- s3
@@ -874,8 +909,12 @@ struct StackPlan {
   std::vector<Chunk> chunks;
   std::vector<StackInstDev> insts;
   std::vector<uint32_t> inst_chunk;
-  std::vector<GroupDev> groups;        // s2_out instance groups, chunk-major
+  std::vector<GroupDev> groups;        // s2_out groups (writers, then histogram groups), chunk-major
   std::vector<uint32_t> group0;        // first group of each chunk (+ end)
+  std::vector<CellDev> cells;          // distinct (row, C) of each chunk, chunk-major, (row, C) order
+  std::vector<uint32_t> cell0;         // first cell of each chunk (+ end)
+  std::vector<uint32_t> inst_cell;     // per StackInstDev: its chunk-local cell
+  uint32_t max_cells = 1;              // cells of the largest chunk (gcell rows)
   uint64_t Emax = 0;
   uint32_t maxbins = 1;
   uint32_t gi = 0;                     // instances per s2_out group (0 = unfused path)
@@ -962,10 +1001,24 @@ static void make_stack_plan(const tlru_trace* traces, uint32_t nt, const tlru_in
   const uint32_t hb2 = (P->maxbins + 1) / 2;  // maxbins == the batch's histogram bins
   const uint32_t gfit = (OUT_SMEM - 16u - ((P->tcap + 15u) & ~15u)) / (4u * hb2);
   P->gi = gfit >= 8u ? std::min(GI_CAP, gfit) : 0u;
+  P->inst_cell.assign(P->insts.size(), 0u);
   for (const StackPlan::Chunk& ch : P->chunks) {
     P->group0.push_back(static_cast<uint32_t>(P->groups.size()));
+    const uint32_t cbase = static_cast<uint32_t>(P->cells.size());
+    P->cell0.push_back(cbase);
+    for (uint32_t d = 0; d < ch.dev.nd; ++d) {  // cells: runs of equal C within the row
+      for (uint32_t k = ch.dev.dbeg[d]; k < ch.dev.dbeg[d + 1];) {
+        const uint32_t C = P->insts[ch.dev.inst0 + k].C;
+        uint32_t k2 = k + 1;
+        while (k2 < ch.dev.dbeg[d + 1] && P->insts[ch.dev.inst0 + k2].C == C) ++k2;
+        for (uint32_t x = k; x < k2; ++x) P->inst_cell[ch.dev.inst0 + x] = static_cast<uint32_t>(P->cells.size()) - cbase;
+        P->cells.push_back(CellDev{C, ch.dev.inst0 + k, k2 - k, d});
+        k = k2;
+      }
+    }
+    P->max_cells = std::max<uint32_t>(P->max_cells, static_cast<uint32_t>(P->cells.size()) - cbase);
     if (!P->gi) continue;
-    for (uint32_t d = 0; d < ch.dev.nd; ++d) {  // near-equal groups of <= gi instances
+    for (uint32_t d = 0; d < ch.dev.nd; ++d) {  // writers: near-equal groups of <= gi instances
       const uint32_t m = ch.dev.dbeg[d + 1] - ch.dev.dbeg[d], ngd = (m + P->gi - 1) / P->gi;
       for (uint32_t q = 0, k = ch.dev.dbeg[d]; q < ngd; ++q) {
         const uint32_t sz = m / ngd + (q < m % ngd ? 1u : 0u);
@@ -973,8 +1026,23 @@ static void make_stack_plan(const tlru_trace* traces, uint32_t nt, const tlru_in
         k += sz;
       }
     }
+    for (uint32_t d = 0; d < ch.dev.nd; ++d) {  // histograms: near-equal groups of <= gi cells per row
+      uint32_t c0 = 0, c1 = 0;
+      for (uint32_t c = cbase; c < P->cells.size(); ++c)
+        if (P->cells[c].d == d) {
+          if (c1 == 0) c0 = c - cbase;
+          c1 = c - cbase + 1;
+        }
+      const uint32_t m = c1 - c0, ngd = (m + P->gi - 1) / P->gi;
+      for (uint32_t q = 0, k = c0; q < ngd; ++q) {
+        const uint32_t sz = m / ngd + (q < m % ngd ? 1u : 0u);
+        P->groups.push_back(GroupDev{d, k, sz, 1u});
+        k += sz;
+      }
+    }
   }
   P->group0.push_back(static_cast<uint32_t>(P->groups.size()));
+  P->cell0.push_back(static_cast<uint32_t>(P->cells.size()));
 }
 
 struct StackWs {
@@ -991,6 +1059,9 @@ struct StackWs {
   uint32_t* LbJ;       // [event] L_before | J << 16
   uint8_t* cnt;        // [group][tcap rounded to 16] s2_out count tables
   uint32_t Astride;
+  CellDev* cells;      // the plan's cells
+  uint32_t* inst_cell; // per StackInstDev: chunk-local cell
+  uint32_t* gcell;     // [cell][bins] the cells' histograms, reused per chunk
 };
 
 static void carve_stack(Carver& cv, const StackPlan& P, uint32_t ni, StackWs* w) {
@@ -1009,6 +1080,9 @@ static void carve_stack(Carver& cv, const StackPlan& P, uint32_t ni, StackWs* w)
   w->A = cv.take<uint32_t>((abytes + 3) / 4);
   w->LbJ = cv.take<uint32_t>(P.gi ? P.Emax + 8 : 1);
   w->cnt = cv.take<uint8_t>(P.gi ? P.groups.size() * ((P.tcap + 15u) & ~size_t(15)) : 16);
+  w->cells = cv.take<CellDev>(P.cells.size() + 1);
+  w->inst_cell = cv.take<uint32_t>(P.inst_cell.size() + 1);
+  w->gcell = cv.take<uint32_t>(P.gi ? uint64_t(P.max_cells) * P.maxbins : 1);
 }
 
 tlru_status stack_workspace(const tlru_trace* traces, uint32_t nt, const tlru_instance* inst, uint32_t ni,
@@ -1058,20 +1132,29 @@ static tlru_status launch_s2(const tlru_trace& tr, const ChunkDev* ch, const Chu
     TLRU_CHECK_LAUNCH();
     TLRU_CUDA(cudaFuncSetAttribute(s2_out_kernel<AT, HT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(out_smem)));
+    const CellDev* cells = w.cells + P.cell0[c];
+    const uint32_t ncell = P.cell0[c + 1] - P.cell0[c];
     if (ng) {
-      s2_cnt_kernel<<<ng, 256, 0, st>>>(ch, w.insts, w.groups + g0, P.tcap, cnt_g);
+      s2_cnt_kernel<<<ng, 256, 0, st>>>(ch, w.insts, w.groups + g0, P.tcap, cnt_g, cells);
       TLRU_CHECK_LAUNCH();
+      TLRU_CUDA(cudaMemsetAsync(w.gcell, 0, size_t(ncell) * bins * sizeof(uint32_t), st));
     }
     for (uint32_t r0 = 0; ng && r0 < nranges; r0 += 65535u) {  // grid.y <= 65535
       if (ot && ot->first && ot->launches == 0) TLRU_CUDA(cudaEventRecord(ot->first, st));
       s2_out_kernel<AT, HT><<<dim3(ng, std::min(65535u, nranges - r0)), 256, out_smem, st>>>(
           ch, w.insts, w.groups + g0, tot, Aptr, w.Astride, w.LbJ, E, rl, bins, P.gi, P.tcap, aligned16, bout, hist,
-          reinterpret_cast<const uint4*>(cnt_g), r0);
+          reinterpret_cast<const uint4*>(cnt_g), r0, cells, w.gcell);
       TLRU_CHECK_LAUNCH();
       if (ot && ot->last) {
         TLRU_CUDA(cudaEventRecord(ot->last, st));
         ++ot->launches;
       }
+    }
+    if (ng) {  // instance histograms = their cells'
+      const uint32_t k0 = P.chunks[c].dev.inst0, nik = P.chunks[c].dev.ninst;
+      s2_instcopy_kernel<<<dim3((bins + 127) / 128, nik), 128, 0, st>>>(w.insts + k0, w.inst_cell + k0, nik, bins,
+                                                                         w.gcell, hist);
+      TLRU_CHECK_LAUNCH();
     }
     return TLRU_OK;
   };
@@ -1101,6 +1184,12 @@ tlru_status stack_simulate(const tlru_trace* traces, uint32_t nt, const tlru_ins
                               cudaMemcpyHostToDevice, st));
     if (!P.groups.empty())
       TLRU_CUDA(cudaMemcpyAsync(w.groups, P.groups.data(), P.groups.size() * sizeof(GroupDev),
+                                cudaMemcpyHostToDevice, st));
+    if (!P.cells.empty())
+      TLRU_CUDA(cudaMemcpyAsync(w.cells, P.cells.data(), P.cells.size() * sizeof(CellDev), cudaMemcpyHostToDevice,
+                                st));
+    if (!P.inst_cell.empty())
+      TLRU_CUDA(cudaMemcpyAsync(w.inst_cell, P.inst_cell.data(), P.inst_cell.size() * sizeof(uint32_t),
                                 cudaMemcpyHostToDevice, st));
   }
   TLRU_CUDA(cudaMemsetAsync(w.totals, 0, (nc + 1) * sizeof(ChunkTotals), st));
