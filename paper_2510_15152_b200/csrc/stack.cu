@@ -35,6 +35,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdlib>
 #include <type_traits>
 #include <vector>
 
@@ -661,7 +662,7 @@ __global__ void __launch_bounds__(256, 4) s2_out_kernel(const ChunkDev* __restri
   // [rows >= group size][hb2] difference rows, two 16-bit counters per word (bins 2v, 2v+1).  The
   // counters wrap into each other, but a word's final value is lo + 65536 * hi (mod 2^32) and
   // decodes exactly while |lo|, |hi| <= 32767, which range_len <= OUT_RANGE_MAX guarantees.
-  extern __shared__ uint32_t hw[];
+  extern __shared__ __align__(128) uint32_t hw[];
   const uint32_t hb2 = (bins + 1) >> 1;
   __shared__ uint32_t C2_s[GI_MAX], C_s[GI_MAX], inst_s[GI_MAX], run_s[GI_MAX];
   __shared__ uint64_t off_s[GI_MAX];
@@ -754,6 +755,77 @@ __global__ void __launch_bounds__(256, 4) s2_out_kernel(const ChunkDev* __restri
     }
   };
   load(e_begin + EV * t, l0n, l1n, an);
+  if (!hist_group && packed_all && aligned16) {
+    // ---- writer group, TMA path: per tile of stride = 2048 events, b of each run (distinct C)
+    // is computed once into a shared-memory stage (one 16-byte vector per thread) and written to
+    // every row of the run by cp.async.bulk (4 KB contiguous per row); runs go WB at a time
+    // through a WS-slot ring (wait_group.read before a slot is reused).  No histogram work here,
+    // so the barriers do not wait on uneven per-thread work.
+    constexpr uint32_t WB = 6, WS = 2;  // runs per batch, stage slots: 2 x 6 x 4 KB = 48 KB
+    uint4* stg = reinterpret_cast<uint4*>(hw);
+    __shared__ uint32_t rstart_s[GI_MAX], ri_s[GI_MAX], nr_s;
+    if (t == 0) {  // runs of equal C: their first instance; each instance's run index
+      uint32_t nr = 0;
+      for (uint32_t i = 0; i < n;) {
+        rstart_s[nr] = i;
+        for (uint32_t k = i; k < run_s[i]; ++k) ri_s[k] = nr;
+        ++nr;
+        i = run_s[i];
+      }
+      nr_s = nr;
+    }
+    __syncthreads();
+    const uint32_t nr = nr_s;
+    const uint32_t e_lo = max(e_begin, nsat * S_THREADS);  // warm-up blocks: s2_warm wrote b
+    uint32_t it = 0;
+    for (uint32_t base = e_begin; base < e_end; base += stride) {
+      const uint32_t e = base + EV * t;
+      const uint4 l0 = l0n, l1 = l1n, ap = an;
+      if (base + stride < e_end) load(e + stride, l0n, l1n, an);
+      const uint32_t tlo = max(base, e_lo), thi = min(base + stride, e_end);
+      if (tlo >= thi) continue;  // uniform: the whole tile is warm
+      const uint32_t lw[EV] = {l0.x, l0.y, l0.z, l0.w, l1.x, l1.y, l1.z, l1.w};
+      const uint32_t A2[4] = {ap.x, ap.y, ap.z, ap.w};
+      uint32_t J2[4], N2[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        J2[k] = __byte_perm(lw[2 * k], lw[2 * k + 1], 0x7632);
+        const uint32_t L2 = __byte_perm(lw[2 * k], lw[2 * k + 1], 0x5410);
+        N2[k] = __vsub2(__vmaxu2(L2, D2), D2);
+        if (HT) N2[k] &= __vcmpgeu2(L2, T2);
+      }
+      const uint32_t v0 = (tlo - base) / EV, nv16 = (thi - tlo) / EV;  // full 8-event vectors
+      for (uint32_t rb = 0; rb < nr; rb += WB, ++it) {
+        const uint32_t sl = it % WS;
+        if (it >= WS && t < GI_MAX) asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(WS - 1) : "memory");
+        __syncthreads();  // slot sl is free again
+        for (uint32_t q = 0; q < WB && rb + q < nr; ++q) {
+          const uint32_t C2 = C2_s[rstart_s[rb + q]];
+          uint32_t w[4];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) w[k] = __vsub2(J2[k], __vminu2(N2[k], __vsub2(__vmaxu2(C2, A2[k]), A2[k])));
+          stg[(sl * WB + q) * 256 + t] = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncthreads();
+        if (t < n && ri_s[t] >= rb && ri_s[t] < rb + WB) {
+          const uint4* src = stg + (sl * WB + (ri_s[t] - rb)) * 256;
+          uint16_t* dst = bout + off_s[t] + tlo;
+          if (nv16) {
+            const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(src + v0));
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(sa),
+                         "r"(nv16 * 16u)
+                         : "memory");
+          }
+          const uint16_t* s16 = reinterpret_cast<const uint16_t*>(src);
+          for (uint32_t u = tlo + nv16 * EV; u < thi; ++u) bout[off_s[t] + u] = s16[u - base];  // trace end
+        }
+        if (t < GI_MAX) asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
+    }
+    if (t < GI_MAX) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    return;
+  }
   for (uint32_t base = e_begin; base < e_end; base += stride) {
     const uint32_t e = base + EV * t;
     const uint4 l0 = l0n, l1 = l1n, ap = an;
@@ -1002,6 +1074,7 @@ static void make_stack_plan(const tlru_trace* traces, uint32_t nt, const tlru_in
   const uint32_t gfit = (OUT_SMEM - 16u - ((P->tcap + 15u) & ~15u)) / (4u * hb2);
   P->gi = gfit >= 8u ? std::min(GI_CAP, gfit) : 0u;
   P->inst_cell.assign(P->insts.size(), 0u);
+  const uint32_t wcap = P->gi;  // measured: 12 / 16 / 24 / 32 rows per writer -> 0.91 / 0.88 / 0.89 / 0.95 ms
   for (const StackPlan::Chunk& ch : P->chunks) {
     P->group0.push_back(static_cast<uint32_t>(P->groups.size()));
     const uint32_t cbase = static_cast<uint32_t>(P->cells.size());
@@ -1018,8 +1091,8 @@ static void make_stack_plan(const tlru_trace* traces, uint32_t nt, const tlru_in
     }
     P->max_cells = std::max<uint32_t>(P->max_cells, static_cast<uint32_t>(P->cells.size()) - cbase);
     if (!P->gi) continue;
-    for (uint32_t d = 0; d < ch.dev.nd; ++d) {  // writers: near-equal groups of <= gi instances
-      const uint32_t m = ch.dev.dbeg[d + 1] - ch.dev.dbeg[d], ngd = (m + P->gi - 1) / P->gi;
+    for (uint32_t d = 0; d < ch.dev.nd; ++d) {  // writers: near-equal groups of <= wcap instances
+      const uint32_t m = ch.dev.dbeg[d + 1] - ch.dev.dbeg[d], ngd = (m + wcap - 1) / wcap;
       for (uint32_t q = 0, k = ch.dev.dbeg[d]; q < ngd; ++q) {
         const uint32_t sz = m / ngd + (q < m % ngd ? 1u : 0u);
         P->groups.push_back(GroupDev{d, k, sz, 0u});
@@ -1123,8 +1196,10 @@ static tlru_status launch_s2(const tlru_trace& tr, const ChunkDev* ch, const Chu
   uint32_t rl = (E + nr - 1) / nr;
   rl = std::min(OUT_RANGE_MAX, (rl + 1023u) & ~1023u);
   const uint32_t nranges = (E + rl - 1) / rl;
-  const size_t out_smem = ((size_t(P.gi) * ((bins + 1) / 2) + 3) & ~size_t(3)) * sizeof(uint32_t) +
-                          ((P.tcap + 15) & ~15u);
+  // histogram groups: rows + count table; writer groups (TMA path): 3 stage slots x 4 runs x 4 KB
+  const size_t out_smem = std::max<size_t>(((size_t(P.gi) * ((bins + 1) / 2) + 3) & ~size_t(3)) * sizeof(uint32_t) +
+                                               ((P.tcap + 15) & ~15u),
+                                           size_t(48) * 1024);
   uint8_t* cnt_g = w.cnt + size_t(g0) * ((P.tcap + 15u) & ~15u);
   auto out = [&](auto* Aptr) -> tlru_status {
     using AT = std::remove_const_t<std::remove_pointer_t<decltype(Aptr)>>;
