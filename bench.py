@@ -287,7 +287,7 @@ def run_ours(args, rank, world, local_rank):
     # memory-bound simulation kernels' CTAs retire
     prio = int(os.environ.get("BENCH_GEN_PRIO", "-1"))
     sA = torch.cuda.Stream(device=dev, priority=prio)
-    nsim = int(os.environ.get("BENCH_SIM_STREAMS", "2"))
+    nsim = int(os.environ.get("BENCH_SIM_STREAMS", "4"))  # measured: 2 / 3 / 4 streams 18.5 / 18.39 / 18.34 ms
     sBs = [torch.cuda.Stream(device=dev) for _ in range(nsim)]
 
     def step():
