@@ -206,6 +206,11 @@ tlru_status tlru_trace_from_turns(const uint32_t* conv, const uint16_t* q, const
  *   post-decision state must hold theta's whole history -- Phases 1 and 2 skip
  *   theta; only if theta alone exceeds C does it lose tail blocks (counted in
  *   evicted_lru).  With xi <= q_hat it equals LRU.  Replay engine only.
+ *   Feasibility: constraint (3) as an equality cannot hold on a request whose
+ *   history exceeds the cache (L_after > C); the library does not fail such a
+ *   run -- theta keeps its C most recent blocks -- and does not flag it: the
+ *   number of such requests of an instance is #{e : L_after_e > C}, a function
+ *   of the trace alone (e.g. from the exported q / response arrays).
  * Tail-Optimized Belady under forced caching (App. C: "Theorem 1
  *   continues to hold" with constraint (3) as an equality; Reading #29): the
  *   Tail-Optimized Belady rule with theta excluded from both phases; only if
