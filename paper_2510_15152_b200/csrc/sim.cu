@@ -556,7 +556,12 @@ static tlru_status make_plan(const tlru_trace* traces, uint32_t nt, const tlru_i
     // conversations (128 or 256 entries) or splitting End- from Length-Aware lanes was slower on
     // the spectrum workload (wider capacity ranges per warp, more frequent compaction).
     // Forced-caching chains keep LRU-like state: up to 1024 entries of 6 B (no surplus array).
-    if ((in.policy == TLRU_POLICY_TAIL_BELADY || in.policy == TLRU_POLICY_BELADY_FORCED) && g_opt_w < 0) {
+    if ((in.policy == TLRU_POLICY_TAIL_BELADY || in.policy == TLRU_POLICY_BELADY_FORCED ||
+         in.policy == TLRU_POLICY_END_AWARE || in.policy == TLRU_POLICY_LENGTH_AWARE) &&
+        g_opt_w < 0) {
+      // End-/Length-Aware release a conversation's blocks at its last turn, so they too hold at
+      // most the open conversations (measured on the preset: 128 entries, no re-run, spectrum
+      // workload 2.5x faster than the capacity classes' 512 entries = one warp per SM)
       // entries hold X >= 1 (tombstones are compacted before the state counts as full), so
       // W > C never overflows; the live conversations of a trace bound it too (<= ~91 on the
       // preset): 128 entries, larger states are re-run by the fix-up from global memory
@@ -569,6 +574,9 @@ static tlru_status make_plan(const tlru_trace* traces, uint32_t nt, const tlru_i
     // kNumW - 2 only (1024 entries x 8 B x 32 lanes exceed shared memory): cap them whatever
     // tlru_set_sim_options asked for -- larger states are re-run by the fix-up
     if (is_aware(in) && aware_kind(in) != kAwareForced) wc[i] = std::min(wc[i], kNumW - 2);
+    // forced-caching T-LRU lanes (6 B entries): 1024 entries x 32 lanes is one warp per SM; 512
+    // (two warps) held every state of the preset up to C = 4096 (no re-run) and was 2.2x faster
+    if (aware_kind(in) == kAwareForced && g_opt_w < 0) wc[i] = std::min(wc[i], kNumW - 2);
     const uint64_t E = traces[in.trace].num_events;
     const uint64_t off = offsets ? offsets[i] : packed;
     packed += E;
