@@ -272,6 +272,8 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.set_device(dev)
     stream = torch.cuda.current_stream()
     rows_all, n_traces, wl_desc = workload_global(args.config)
+    if args.segment_events:
+        T.set_sim_options(args.segment_events, 0)
     n_total = len(rows_all)
     strong = args.scaling == "strong"
     if any(r[1] == T.POLICY_ET_LRU for r in rows_all):  # ET-LRU model: belief decay per µs tick, prompt law
@@ -567,6 +569,8 @@ def main():
     ap.add_argument("--config", choices=("config5", "config5x3", "spectrum", "etlru", "forced", "forced_belady",
                                          "config4"),
                     default="config5")
+    ap.add_argument("--segment-events", type=int, default=0,
+                    help="replay-engine segment length (tlru_set_sim_options; 0 = automatic)")
     ap.add_argument("--scaling", choices=("strong", "weak"), default="strong",
                     help="strong: the one sweep sharded over the ranks (default); weak: every rank its own seeds")
     args = ap.parse_args()
