@@ -69,7 +69,7 @@ def lib():
         L.oracle_replay.restype = ctypes.c_int
         L.oracle_replay_etlru.argtypes = [u32p, u32p, u32p, u64p, ctypes.c_uint64, ctypes.c_uint64,
                                           ctypes.c_uint64, ctypes.c_double, ctypes.POINTER(ctypes.c_double),
-                                          ctypes.c_uint64, u64p, u64p]
+                                          ctypes.c_uint64, ctypes.c_int, u64p, u64p]
         L.oracle_replay_etlru.restype = ctypes.c_int
         L.oracle_tail.argtypes = [u64p, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_double, ctypes.c_uint64,
                                   ctypes.c_double, u64p, ctypes.POINTER(ctypes.c_double)]
@@ -197,6 +197,7 @@ LENGTH_AWARE = 4
 TAIL_BELADY = 5  # Thm 1 hindsight policy, Reading #26
 TLRU_FORCED = 7  # T-LRU under forced caching (App. C), Reading #28
 BELADY_FORCED = 8  # Tail-Optimized Belady under forced caching (App. C), Reading #29
+ETLRU_FORCED = 9  # ET-LRU under forced caching (App. C), Reading #30 (replay_etlru(forced=True))
 ET_LRU = 6  # Def. 1 / Alg. 2, Reading #27 -- see replay_etlru
 
 
@@ -225,11 +226,13 @@ def replay(conv, q, a, policy: int, C: int, xi: int = 0, q_hat: int = 0, thresho
     return Replay(b, int(cnt[0]), int(cnt[1]), int(cnt[2]))
 
 
-def replay_etlru(conv, q, a, ticks, C: int, xi: int, mu_tick: float, ln_surv) -> Replay:
+def replay_etlru(conv, q, a, ticks, C: int, xi: int, mu_tick: float, ln_surv, forced: bool = False) -> Replay:
     """Expected-Tail-Optimized LRU (Def. 1 / Alg. 2; Reading #27):
     greedy block-by-block eviction by the ranking criterion mu * time_i + ln P(Q >= X_i - L_i + xi).
     ticks[E]: event times (u64 microseconds); ln_surv[k] = ln P(Q >= k), k = 0..K.
-    evicted_trim = blocks evicted with P = 0, evicted_lru = the others."""
+    evicted_trim = blocks evicted with P = 0, evicted_lru = the others.
+    forced: under forced caching (App. C; Reading #30) theta keeps its whole history
+    while its turn is served (only if it alone exceeds C does it lose the excess, evicted_lru)."""
     conv = np.ascontiguousarray(conv, dtype=np.uint32)
     q = np.ascontiguousarray(q, dtype=np.uint32)
     a = np.ascontiguousarray(a, dtype=np.uint32)
@@ -240,8 +243,8 @@ def replay_etlru(conv, q, a, ticks, C: int, xi: int, mu_tick: float, ln_surv) ->
     cnt = np.zeros(3, np.uint64)
     rc = lib().oracle_replay_etlru(_p(conv, ctypes.c_uint32), _p(q, ctypes.c_uint32), _p(a, ctypes.c_uint32),
                                    _p(ticks, ctypes.c_uint64), E, int(C), int(xi), float(mu_tick),
-                                   _p(ls, ctypes.c_double), ls.shape[0] - 1, _p(b, ctypes.c_uint64),
-                                   _p(cnt, ctypes.c_uint64))
+                                   _p(ls, ctypes.c_double), ls.shape[0] - 1, 1 if forced else 0,
+                                   _p(b, ctypes.c_uint64), _p(cnt, ctypes.c_uint64))
     if rc != 0:
         raise MemoryError("oracle_replay_etlru")
     return Replay(b, int(cnt[0]), int(cnt[1]), int(cnt[2]))

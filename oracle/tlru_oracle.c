@@ -625,9 +625,14 @@ int oracle_replay(const uint32_t* conv, const uint32_t* q, const uint32_t* a, ui
    k = 0..K (k <= 0 -> ln 1 = 0, k > K -> -inf: the block is TEL-safe); ties -> older last
    turn first (then the same conversation's tail block).  evicted_trim counts blocks evicted
    with P = 0 (-inf), evicted_lru the others.  time_i = the tick of conversation i's last turn. */
+/* forced != 0: ET-LRU under forced caching (App. C: decision space X_F with
+   Y_theta = L -- theta's whole history stays; Reading #30): theta is not a candidate of the
+   greedy while serving its own turn; if no other block is left and the cache still exceeds C
+   (theta alone holds more than C), theta loses the excess from its tail, counted with the
+   P > 0 evictions (evicted_lru, as forced T-LRU, Reading #28). */
 int oracle_replay_etlru(const uint32_t* conv, const uint32_t* q, const uint32_t* a, const uint64_t* ticks,
                         uint64_t E, uint64_t C, uint64_t xi, double mu_tick, const double* ln_surv,
-                        uint64_t K, uint64_t* b_out, uint64_t* counters_out) {
+                        uint64_t K, int forced, uint64_t* b_out, uint64_t* counters_out) {
     uint32_t* dense = (uint32_t*)malloc((E ? E : 1) * 4);
     if (!dense) return -1;
     int64_t n = densify(conv, E, dense);
@@ -659,6 +664,7 @@ int oracle_replay_etlru(const uint32_t* conv, const uint32_t* q, const uint32_t*
             for (int64_t k = 0; k < nres; ++k) {
                 int64_t i = res[k];
                 if (X[i] == 0) continue;
+                if (forced && i == c) continue;          /* Y_theta = L (App. C) */
                 /* P(L_i + Q_i - xi >= X_i) = P(Q_i >= X_i - L_i + xi) */
                 int64_t kk = (int64_t)X[i] - (int64_t)L[i] + (int64_t)xi;
                 double lg = kk <= 0 ? 0.0 : ((uint64_t)kk > K ? NEG_INF : ln_surv[kk]);
@@ -666,6 +672,13 @@ int oracle_replay_etlru(const uint32_t* conv, const uint32_t* q, const uint32_t*
                 if (best < 0 || v < best_v || (v == best_v && tau[i] < tau[best])) {
                     best = i; best_v = v; best_lg = lg;
                 }
+            }
+            if (best < 0) {                             /* forced: theta alone exceeds C */
+                uint64_t k = used - C;
+                X[c] -= k;
+                used = C;
+                ev_other += k;
+                break;
             }
             X[best] -= 1;
             used -= 1;
