@@ -238,6 +238,11 @@ def workload_global(name: str):
         rows = [(t, 7, C, xi, Q_HAT, SLO_BLOCKS) for t in range(n) for C in CAPS_CONFIG5 for xi in (4, 8, 16, 24)]
         return rows, n, ("T-LRU under forced caching (App. C): 10 seeds x 10^6-conversation traces x 25 capacities "
                          "x xi in {4, 8, 16, 24} = 1000 instances (replay engine)")
+    if name == "etlru_forced":
+        rows = [(t, 9, C, xi, Q_HAT, SLO_BLOCKS) for t in range(n) for C in CAPS_CONFIG5 for xi in (4, 8, 16, 24)]
+        return rows, n, ("ET-LRU under forced caching (App. C, P:664-672): 10 seeds x 10^6-conversation traces x "
+                         "25 capacities x xi in {4, 8, 16, 24} = 1000 instances, belief mu = 1/90 s, the preset's "
+                         "prompt law")
     if name == "forced_belady":
         rows = [(t, 8, C, xi, Q_HAT, SLO_BLOCKS) for t in range(n) for C in CAPS_CONFIG5 for xi in (4, 8, 16, 24)]
         return rows, n, ("Tail-Optimized Belady under forced caching (App. C, P:657-662): 10 seeds x "
@@ -276,7 +281,7 @@ def run_ours(args, rank, world, local_rank):
         T.set_sim_options(args.segment_events, 0)
     n_total = len(rows_all)
     strong = args.scaling == "strong"
-    if any(r[1] == T.POLICY_ET_LRU for r in rows_all):  # ET-LRU model: belief decay per µs tick, prompt law
+    if any(r[1] in (T.POLICY_ET_LRU, T.POLICY_ETLRU_FORCED) for r in rows_all):  # ET-LRU model: belief decay per µs tick, prompt law
         from paper_2510_15152_b200.inputs import WILDCHAT, prompt_law_ln_surv
         T.set_etlru_model(WILDCHAT["death_rate"] * 1e-6, prompt_law_ln_surv(WILDCHAT))
 
@@ -388,7 +393,7 @@ def run_ours(args, rank, world, local_rank):
     # ---- e2e: the same step through the public API from pinned host buffers (H2D of each trace's
     # turns on stream A, upload + simulation + pooling on the simulation streams, the collectives),
     # the result table and the pooled metrics read back to the host
-    need_ticks = any(r[1] == T.POLICY_ET_LRU for r in rows_all)  # ET-LRU beliefs read the event times
+    need_ticks = any(r[1] in (T.POLICY_ET_LRU, T.POLICY_ETLRU_FORCED) for r in rows_all)  # ET-LRU beliefs read the event times
     host_turns, host_ticks = [], []
     for tr in traces:
         E = tr.num_events
@@ -567,7 +572,7 @@ def main():
     ap.add_argument("--no-replay", action="store_true", help="skip timing the replay engine")
     ap.add_argument("--replay-instances", type=int, default=0, help="limit the replay-engine sample (0 = all of seed 0)")
     ap.add_argument("--config", choices=("config5", "config5x3", "spectrum", "etlru", "forced", "forced_belady",
-                                         "config4"),
+                                         "etlru_forced", "config4"),
                     default="config5")
     ap.add_argument("--segment-events", type=int, default=0,
                     help="replay-engine segment length (tlru_set_sim_options; 0 = automatic)")

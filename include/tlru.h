@@ -42,7 +42,7 @@ typedef enum {
   TLRU_EINVAL = 1,       /* bad argument or configuration (block_tokens == 0, rate <= 0, q == 0, ...) */
   TLRU_ERANGE = 2,       /* buffer / workspace too small, or a value exceeds its field width (J > 65535) */
   TLRU_ECUDA = 3,        /* CUDA runtime error; tlru_last_error() carries cudaGetErrorString */
-  TLRU_EUNSUPPORTED = 4, /* policy family not built (policy > TLRU_POLICY_BELADY_FORCED) */
+  TLRU_EUNSUPPORTED = 4, /* policy family not built (policy > TLRU_POLICY_ETLRU_FORCED) */
   TLRU_ESTATE = 5        /* internal per-chain state pool exhausted with no fallback left */
 } tlru_status;
 
@@ -217,6 +217,11 @@ tlru_status tlru_trace_from_turns(const uint32_t* conv, const uint16_t* q, const
  *   theta alone exceeds C does it lose tail blocks, above-budget ones first
  *   (counted in evicted_lru).  Its TEL is the forced hindsight optimum.  Replay
  *   engine only.
+ * ET-LRU under forced caching (App. C: Y_theta = L; Reading #30):
+ *   ET-LRU whose greedy never picks theta while its turn is served; if no other
+ *   block is left and the cache still exceeds C, theta loses the excess from its
+ *   tail (evicted_lru).  With a fixed prompt length it is forced T-LRU.
+ *   Needs the ET-LRU model and real ticks, like ET-LRU.  One warp per instance.
  * ------------------------------------------------------------------------ */
 enum {
   TLRU_POLICY_LRU = 0,
@@ -227,7 +232,8 @@ enum {
   TLRU_POLICY_TAIL_BELADY = 5,
   TLRU_POLICY_ET_LRU = 6,
   TLRU_POLICY_TLRU_FORCED = 7,
-  TLRU_POLICY_BELADY_FORCED = 8 /* > 8 -> TLRU_EUNSUPPORTED */
+  TLRU_POLICY_BELADY_FORCED = 8,
+  TLRU_POLICY_ETLRU_FORCED = 9 /* > 9 -> TLRU_EUNSUPPORTED */
 };
 
 typedef struct {

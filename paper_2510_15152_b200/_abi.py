@@ -23,6 +23,7 @@ POLICY_TAIL_BELADY = 5
 POLICY_ET_LRU = 6
 POLICY_TLRU_FORCED = 7
 POLICY_BELADY_FORCED = 8
+POLICY_ETLRU_FORCED = 9
 ENGINE_REPLAY = 0
 ENGINE_STACK = 1
 ENGINE_MIXED = 2

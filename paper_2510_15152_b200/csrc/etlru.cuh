@@ -32,6 +32,7 @@ namespace tlru {
 struct EtItem {  // one ET-LRU instance
   uint32_t inst, trace, C, xi;
   uint64_t boff;
+  uint32_t forced, pad;  // forced caching (App. C; Reading #30)
 };
 
 struct EtSeg {  // one warp of the segment kernel
@@ -94,6 +95,7 @@ struct EtState {
   int64_t xi;
   unsigned long long ev_free, ev_other;
   bool overflow;
+  bool forced;  // theta is not a candidate while its turn is served (Y_theta = L, App. C)
 
   __device__ __forceinline__ void carve(unsigned char* pool, uint32_t c) {
     cap = c;
@@ -149,6 +151,7 @@ __device__ __forceinline__ uint32_t et_request(EtState& S, const EtCtx& m, uint3
   }
   ++S.n;
   S.used += La - x_old;
+  uint32_t th = S.forced ? S.n - 1 : 0xFFFFFFFFu;  // forced: theta's slot, excluded below
   __syncwarp();
   // ---- lines 8-12: evict the overflow, minimum ranking criterion first
   while (S.used > S.C) {
@@ -157,6 +160,7 @@ __device__ __forceinline__ uint32_t et_request(EtState& S, const EtCtx& m, uint3
     uint32_t t1 = 0xFFFFFFFFu, t2 = 0xFFFFFFFFu, s1 = 0;
 #pragma unroll 4
     for (uint32_t s = lane; s < S.n; s += 32) {
+      if (s == th) continue;
       const uint64_t ks = S.key[s];
       const uint32_t ts = S.tau[s];
       if (ks < k1 || (ks == k1 && ts < t1)) {
@@ -173,6 +177,18 @@ __device__ __forceinline__ uint32_t et_request(EtState& S, const EtCtx& m, uint3
     uint64_t kmin, krun;
     uint32_t tmin, trun;
     et_warp_min(k1, t1, kmin, tmin);
+    if (kmin == ~0ull) {  // forced: only theta is left and it alone exceeds C -- it loses the excess
+      __syncwarp();
+      if (lane == 0) {
+        const uint32_t xn = S.X[th] - over;
+        S.X[th] = static_cast<uint16_t>(xn);
+        S.key[th] = et_ord(__dadd_rn(S.base[th], m.lg(int64_t(xn) - int64_t(S.L[th]) + S.xi)));
+      }
+      S.ev_other += over;
+      S.used = S.C;
+      __syncwarp();
+      break;
+    }
     const int wl = __ffs(__ballot_sync(0xFFFFFFFFu, k1 == kmin && t1 == tmin)) - 1;
     const uint32_t j = __shfl_sync(0xFFFFFFFFu, s1, wl);
     if (lane == wl) {  // the runner-up: the winner lane's second or any other lane's best
@@ -201,6 +217,7 @@ __device__ __forceinline__ uint32_t et_request(EtState& S, const EtCtx& m, uint3
     S.used -= cnt;
     const uint32_t xn = xj - cnt;
     __syncwarp();
+    if (xn == 0 && j != S.n - 1 && th == S.n - 1) th = j;  // theta moves into j's slot
     if (lane == 0) {
       if (xn == 0) {
         if (j != S.n - 1) S.move_slot(j, S.n - 1);
@@ -292,12 +309,13 @@ __device__ __forceinline__ void et_ctx_init(EtCtx& c, const EtModel& m, double* 
   c.mu = m.mu_tick;
 }
 
-__device__ __forceinline__ void et_state_init(EtState& S, uint32_t C, uint32_t xi) {
+__device__ __forceinline__ void et_state_init(EtState& S, uint32_t C, uint32_t xi, bool forced) {
   S.n = S.used = S.max_occ = 0;
   S.C = C;
   S.xi = xi;
   S.ev_free = S.ev_other = 0;
   S.overflow = false;
+  S.forced = forced;
 }
 
 // One warp per (instance, segment); W slots in shared memory after the table copy.
@@ -313,7 +331,7 @@ __global__ void __launch_bounds__(32) etlru_seg_kernel(const EtSeg* __restrict__
   et_ctx_init(m, mdl, reinterpret_cast<double*>(smem));
   EtState S;
   S.carve(smem + kEtTab * sizeof(double), W);
-  et_state_init(S, it.C, it.xi);
+  et_state_init(S, it.C, it.xi, it.forced != 0);
   const uint32_t s = sj.seg * sg.seg_len;
   const uint32_t s_end = static_cast<uint32_t>(min(uint64_t(s) + sg.seg_len, tr.E));
   const uint32_t s0 = s > sg.burn ? s - sg.burn : 0u;
@@ -353,7 +371,7 @@ __global__ void __launch_bounds__(32) etlru_fix_kernel(const EtItem* __restrict_
   et_ctx_init(m, mdl, tab_s);
   EtState S;
   S.carve(gpool + size_t(i) * Wg * 24, Wg);
-  et_state_init(S, it.C, it.xi);
+  et_state_init(S, it.C, it.xi, it.forced != 0);
   const uint32_t nseg = static_cast<uint32_t>((tr.E + sg.seg_len - 1) / sg.seg_len);
   const size_t sw = et_snap_words(sg.wsnap);
   bool carry = false;  // S holds the exact state at the end of segment k - 1
@@ -366,7 +384,7 @@ __global__ void __launch_bounds__(32) etlru_fix_kernel(const EtItem* __restrict_
       continue;
     }
     if (!carry) {
-      et_state_init(S, it.C, it.xi);
+      et_state_init(S, it.C, it.xi, it.forced != 0);
       if (k > 0) {
         if (Fp[0] == 0xFFFFFFFFu) {  // the previous end state was too large to save
           if (lane == 0) atomicAdd(nfail, 1u);

@@ -532,11 +532,11 @@ static tlru_status make_plan(const tlru_trace* traces, uint32_t nt, const tlru_i
   for (uint32_t i = 0; i < ni; ++i) {
     const tlru_instance& in = inst[i];
     if (in.trace >= nt) TLRU_FAIL(TLRU_EINVAL, "instance %u: trace index %u out of range", i, in.trace);
-    if (in.policy > TLRU_POLICY_BELADY_FORCED)
-      TLRU_FAIL(TLRU_EUNSUPPORTED, "instance %u: policy %u is not built (0..8: LRU, T-LRU, Threshold-LRU, "
+    if (in.policy > TLRU_POLICY_ETLRU_FORCED)
+      TLRU_FAIL(TLRU_EUNSUPPORTED, "instance %u: policy %u is not built (0..9: LRU, T-LRU, Threshold-LRU, "
                 "End-Aware, Length-Aware, Tail-Optimized Belady, ET-LRU, forced-caching T-LRU, forced-caching "
-                "Tail-Optimized Belady)", i, in.policy);
-    if (in.policy == TLRU_POLICY_ET_LRU) {
+                "Tail-Optimized Belady, forced-caching ET-LRU)", i, in.policy);
+    if (in.policy == TLRU_POLICY_ET_LRU || in.policy == TLRU_POLICY_ETLRU_FORCED) {
       if (g_et_mu < 0.0) TLRU_FAIL(TLRU_EINVAL, "instance %u: ET-LRU needs tlru_set_etlru_model first", i);
       if (traces[in.trace].num_events > 0 && !traces[in.trace].time_ticks)
         TLRU_FAIL(TLRU_EINVAL, "instance %u: ET-LRU needs the trace's time_ticks (beliefs, P:255)", i);
@@ -587,14 +587,15 @@ static tlru_status make_plan(const tlru_trace* traces, uint32_t nt, const tlru_i
     std::vector<uint32_t> keep;
     for (uint32_t i : order) {
       const tlru_instance& in = inst[i];
-      if (in.policy != TLRU_POLICY_ET_LRU) {
+      if (in.policy != TLRU_POLICY_ET_LRU && in.policy != TLRU_POLICY_ETLRU_FORCED) {
         keep.push_back(i);
         continue;
       }
       P->any_aware = true;
       const uint32_t C = std::min<uint32_t>(in.capacity, 0x7FFF0000u);
       const int k = g_opt_w >= 0 ? g_opt_w : w_class(C, traces[in.trace].num_conversations);
-      P->et_items.push_back(EtItem{i, in.trace, C, in.xi, P->segs[i].begin});
+      P->et_items.push_back(EtItem{i, in.trace, C, in.xi, P->segs[i].begin,
+                                   in.policy == TLRU_POLICY_ETLRU_FORCED ? 1u : 0u, 0u});
       et_cls.push_back(k);
       ++P->n_et;
     }

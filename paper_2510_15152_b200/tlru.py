@@ -13,13 +13,13 @@ import numpy as np
 import torch
 
 from . import _abi
-from ._abi import (ENGINE_MIXED, ENGINE_REPLAY, ENGINE_STACK, POLICY_END_AWARE, POLICY_ET_LRU, POLICY_LENGTH_AWARE, POLICY_TLRU_FORCED, POLICY_BELADY_FORCED, POLICY_LRU, POLICY_TAIL_BELADY, POLICY_THRESHOLD, POLICY_TLRU, RESULT_DTYPE, TAIL_DTYPE, TLRU_NONE, GenParams, Instance, SimStats,
+from ._abi import (ENGINE_MIXED, ENGINE_REPLAY, ENGINE_STACK, POLICY_END_AWARE, POLICY_ET_LRU, POLICY_LENGTH_AWARE, POLICY_TLRU_FORCED, POLICY_BELADY_FORCED, POLICY_ETLRU_FORCED, POLICY_LRU, POLICY_TAIL_BELADY, POLICY_THRESHOLD, POLICY_TLRU, RESULT_DTYPE, TAIL_DTYPE, TLRU_NONE, GenParams, Instance, SimStats,
                    Trace, TlruError, check, lib)
 
 __all__ = ["DeviceTrace", "generate_traces", "trace_from_turns", "simulate_batch", "tail_metrics", "last_sim_stats",
            "set_sim_options", "set_sim_engine", "set_etlru_model", "pool_histograms", "tail_from_histograms",
            "ENGINE_REPLAY", "ENGINE_STACK", "ENGINE_MIXED",
-           "POLICY_LRU", "POLICY_TLRU", "POLICY_THRESHOLD", "POLICY_END_AWARE", "POLICY_LENGTH_AWARE", "POLICY_TAIL_BELADY", "POLICY_ET_LRU", "POLICY_TLRU_FORCED", "POLICY_BELADY_FORCED", "TLRU_NONE", "TlruError", "RESULT_DTYPE", "TAIL_DTYPE", "version"]
+           "POLICY_LRU", "POLICY_TLRU", "POLICY_THRESHOLD", "POLICY_END_AWARE", "POLICY_LENGTH_AWARE", "POLICY_TAIL_BELADY", "POLICY_ET_LRU", "POLICY_TLRU_FORCED", "POLICY_BELADY_FORCED", "POLICY_ETLRU_FORCED", "TLRU_NONE", "TlruError", "RESULT_DTYPE", "TAIL_DTYPE", "version"]
 
 
 def version() -> str:

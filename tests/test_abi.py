@@ -83,7 +83,7 @@ def test_sim_workspace_rejects_unknown_policy(abi):
     tr = (abi.Trace * 1)()
     tr[0].num_events = 0
     inst = (abi.Instance * 1)()
-    inst[0].policy = 9  # beyond BELADY_FORCED: not built
+    inst[0].policy = 10  # beyond ETLRU_FORCED: not built
     sz = ctypes.c_size_t()
     assert abi.lib.tlru_sim_workspace_size(tr, 1, inst, 1, ctypes.byref(sz)) == 4  # EUNSUPPORTED
     inst[0].policy = 1

@@ -409,8 +409,8 @@ def test_upload_errors(T):
     tr = upload(T, [0], [1], [0])
     with pytest.raises(T.TlruError, match="EINVAL"):
         T.set_sim_engine(7)
-    with pytest.raises(T.TlruError, match="EUNSUPPORTED"):  # > BELADY_FORCED: not built
-        T.simulate_batch([tr], [(0, 9, 10, 0, 0, 0)])
+    with pytest.raises(T.TlruError, match="EUNSUPPORTED"):  # > ETLRU_FORCED: not built
+        T.simulate_batch([tr], [(0, 10, 10, 0, 0, 0)])
 
 
 @ENGINES
