@@ -57,7 +57,7 @@ E_REF = 2.5e6
 COST_TRACE_GEN_MS = 0.50
 COST_TRACE_PASS_MS = 0.10
 COST_PER_D_MS = 0.022
-COST_PER_INSTANCE_MS = 0.00099
+COST_PER_INSTANCE_MS = 0.00088  # round 2: s2_out 0.88 ms per 1000 instances (TMA writer groups)
 # replay-engine policies (End-/Length-Aware, Belady, ET-LRU, forced): per-instance replay cost
 COST_REPLAY_INSTANCE_MS = 0.40
 

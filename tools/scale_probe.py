@@ -30,7 +30,7 @@ def main():
     rows, _, _ = bench.workload_global("config5")
     st = torch.cuda.current_stream()
     sA = torch.cuda.Stream(priority=-1)
-    sBs = [torch.cuda.Stream(), torch.cuda.Stream()]
+    sBs = [torch.cuda.Stream() for _ in range(4)]  # as bench.py
     out = {}
     for world in args.worlds:
         per_rank = []
