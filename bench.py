@@ -288,7 +288,7 @@ def run_ours(args, rank, world, local_rank):
     # ---- setup (untimed): this rank's traces at their exact size, one batch per trace, pools
     sw = Sweep(rows_all, world, rank, lambda seed: preset("wildchat", seed, args.conversations), dev,
                scaling=args.scaling, backend="nccl")
-    shards, traces, batches, ids_by_trace = sw.shards, sw.traces, sw.batches, sw.ids_by_trace
+    shards, traces, batches, ids_by_trace = sw.shards, sw.sim_traces, sw.batches, sw.ids_by_trace
     E_loc, RS, HB, npool = sw.requests_local, sw.RS, sw.HB, sw.npool
     # generation (compute-bound) on a higher-priority stream: its CTAs take SM slots as the
     # memory-bound simulation kernels' CTAs retire
@@ -304,8 +304,8 @@ def run_ours(args, rank, world, local_rank):
         """One stream, no overlap; returns the summed engine / K3 / s2_out device times of the step."""
         with torch.cuda.stream(stream):
             sw.pooled.zero_()
-        for j in range(len(batches)):
-            sw.gen(j, stream)
+        for j in range(len(sw.held)):
+            sw.produce(j, stream)  # generated here (owner) and / or broadcast (shared generation)
         k2 = k3 = out_ms = 0.0
         out_n = 0
         for j in range(len(batches)):
@@ -423,7 +423,7 @@ def run_ours(args, rank, world, local_rank):
         for sB in sBs:
             sB.wait_event(ev0)
         for j, ((hc, hq, ha), (dc, dq, da), tr, ts, w) in enumerate(
-                zip(host_turns, dev_turns, traces, sw.tstructs, up_ws)):
+                zip(host_turns, dev_turns, traces, sw.sim_tstructs, up_ws)):
             sB = sBs[j % len(sBs)]
             with torch.cuda.stream(sA):
                 dc.copy_(hc, non_blocking=True)
@@ -485,9 +485,15 @@ def run_ours(args, rank, world, local_rank):
         t = json.load(open(tpath))
         if "s2_out_dram_bytes_per_request" in t:
             traffic = float(t["s2_out_dram_bytes_per_request"]) * E_loc / out_n
-    shard_info = {"instances": [len(s_) for s_ in shards], "traces": [len({int(rows_all[i][0]) for i in s_})
-                                                                       for s_ in shards],
-                  "modelled_ms": [round(shard_cost(rows_all, s_), 3) for s_ in shards]} if strong else None
+    shard_info = None
+    if strong:
+        shard_info = {"instances": [len(s_) for s_ in shards],
+                      "traces": [len({int(rows_all[i][0]) for i in s_}) for s_ in shards],
+                      "modelled_ms": [round(shard_cost(rows_all, s_, owners=sw.owners, rank=r_), 3)
+                                      for r_, s_ in enumerate(shards)],
+                      "generation": ("shared: each trace generated by the first rank using it and NCCL-broadcast "
+                                     "(12 B/event) to the other ranks using it" if sw.owners else
+                                     "each rank generates its traces")}
     line = {
         "metric": "simulated requests/sec", "value": value, "unit": "requests/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
@@ -496,8 +502,9 @@ def run_ours(args, rank, world, local_rank):
             "workload": wl_desc, "instances": n_total if strong else n_total * world,
             "requests_per_step": req_all, "conversations": args.conversations,
             "parallelism": (f"dp{world}: the sweep's instances sharded over {world} GPU(s) at sub-trace granularity "
-                            "(sweep.plan_strong; each rank regenerates its traces), NCCL all_gather of the results "
-                            "+ all_reduce of the pooled histograms" if strong else
+                            "(sweep.plan_strong; each trace generated once by its owner rank and broadcast to the "
+                            "other ranks using it), NCCL all_gather of the results + all_reduce of the pooled "
+                            "histograms" if strong else
                             f"dp{world}: every rank runs the whole sweep on its own seeds; NCCL all_gather / "
                             "all_reduce as in strong mode"),
             "shards": shard_info,

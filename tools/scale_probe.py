@@ -35,7 +35,7 @@ def main():
     for world in args.worlds:
         per_rank = []
         for rank in range(world):
-            sw = Sweep(rows, world, rank, lambda s: preset("wildchat", s, args.conversations), "cuda:0")
+            sw = Sweep(rows, world, rank, lambda s: preset("wildchat", s, args.conversations), "cuda:0", comm=False)
             for _ in range(args.warmup):
                 sw.step(st, sA, sBs, combine=False)
             torch.cuda.synchronize()
@@ -48,7 +48,7 @@ def main():
             ms = t0.elapsed_time(t1) / args.steps
             per_rank.append({"rank": rank, "ms": ms, "instances": len(sw.shards[rank]),
                              "traces": len(sw.my_traces), "requests": sw.requests_local,
-                             "modelled_ms": shard_cost(rows, sw.shards[rank])})
+                             "modelled_ms": shard_cost(rows, sw.shards[rank], owners=sw.owners, rank=rank)})
             del sw
             torch.cuda.empty_cache()
         step = max(r["ms"] for r in per_rank)
