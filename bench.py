@@ -518,7 +518,7 @@ def run_ours(args, rank, world, local_rank):
             "pooled": {"pools": npool, "bins": HB, "what": "per (policy, C, xi) over seeds: u64 b-histograms "
                        "summed per GPU (tlru_pool_histograms), all_reduce over GPUs, tlru_tail_from_histograms"},
             "pipelining": "traces generated on a high-priority stream A while earlier traces are simulated on "
-                          "two alternating streams; engine_ms / k3_ms / roofline.launch_ms from the sequential "
+                          "BENCH_SIM_STREAMS (4) alternating streams; engine_ms / k3_ms / roofline.launch_ms from the sequential "
                           "(single-stream) step",
         },
         "e2e": {"value": req_all / (e2e_ms / 1000.0), "unit": "requests/s", "h2d_bytes_per_step": h2d_bytes,
