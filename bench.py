@@ -525,7 +525,8 @@ def run_ours(args, rank, world, local_rank):
                 "d2h_bytes_per_step": d2h_bytes, "ms_per_step": e2e_ms},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak if achieved else None, "traffic": traffic,
-                     "kernel": "s2_out_kernel (b output + per-group histograms), per launch",
+                     "kernel": "s2_out_kernel (writer groups: b by TMA bulk stores; histogram groups: per-cell "
+                               "histograms), per launch",
                      "launch_ms": out_ms / out_n, "launches_per_step": out_n,
                      "algorithmic_bytes_per_launch": b_bytes / out_n,
                      "algorithmic_bytes": f"{OUT_B_BYTES} B/request: the b row written (irreducible output)",
