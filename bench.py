@@ -286,7 +286,7 @@ def run_ours(args, rank, world, local_rank):
         T.set_etlru_model(WILDCHAT["death_rate"] * 1e-6, prompt_law_ln_surv(WILDCHAT))
 
     # ---- setup (untimed): this rank's traces at their exact size, one batch per trace, pools
-    sw = Sweep(rows_all, world, rank, lambda seed: preset("wildchat", seed, args.conversations), dev,
+    sw = Sweep(rows_all, world, rank, lambda seed: preset(args.preset, seed, args.conversations), dev,
                scaling=args.scaling, backend="nccl")
     shards, traces, batches, ids_by_trace = sw.shards, sw.sim_traces, sw.batches, sw.ids_by_trace
     E_loc, RS, HB, npool = sw.requests_local, sw.RS, sw.HB, sw.npool
@@ -499,7 +499,9 @@ def run_ours(args, rank, world, local_rank):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": args.scaling, "vs_baseline": None, "dtype": "u32", "data": "synthetic",
         "config": {
-            "workload": wl_desc, "instances": n_total if strong else n_total * world,
+            "workload": wl_desc + ("" if args.preset == "wildchat" else
+                                   f" -- traces from the {args.preset} preset (App. E, P:724) instead"),
+            "instances": n_total if strong else n_total * world,
             "requests_per_step": req_all, "conversations": args.conversations,
             "parallelism": (f"dp{world}: the sweep's instances sharded over {world} GPU(s) at sub-trace granularity "
                             "(sweep.plan_strong; each trace generated once by its owner rank and broadcast to the "
@@ -582,6 +584,8 @@ def main():
     ap.add_argument("--config", choices=("config5", "config5x3", "spectrum", "etlru", "forced", "forced_belady",
                                          "etlru_forced", "config4"),
                     default="config5")
+    ap.add_argument("--preset", choices=("wildchat", "sharegpt"), default="wildchat",
+                    help="synthetic trace model: WildChat-shaped (BASELINE) or App. E's ShareGPT-shaped")
     ap.add_argument("--segment-events", type=int, default=0,
                     help="replay-engine segment length (tlru_set_sim_options; 0 = automatic)")
     ap.add_argument("--scaling", choices=("strong", "weak"), default="strong",
