@@ -101,3 +101,26 @@ def test_generated_preset_with_segments(T):
         T.set_sim_options(0, 0)
     assert st["failed_chains"] == 0
     check(bt, rows, [(o.conv, o.q, o.a, o.ticks)], mu, tab)
+
+
+def test_full_size_sampled(T):
+    """BASELINE trace size (10^6 conversations) in the launch configuration of
+    `bench.py --config etlru_forced` (one trace, its 100 rows in one batch): sampled instances
+    against the oracle, b and eviction counters."""
+    from paper_2510_15152_b200.inputs import CAPS_CONFIG5
+    p = preset("wildchat", 6, 1_000_000)
+    mu = WILDCHAT["death_rate"] * 1e-6
+    tab = prompt_law_ln_surv(WILDCHAT)
+    T.set_etlru_model(mu, tab)
+    tr = T.generate_traces([p], exports=True)[0]
+    rows = [(0, ETF, C, xi, 2, SLO_BLOCKS) for C in CAPS_CONFIG5 for xi in (4, 8, 16, 24)]
+    bt = T.simulate_batch([tr], rows)
+    assert T.last_sim_stats()["failed_chains"] == 0
+    o = O.generate(p)
+    res = bt.results_numpy()
+    for C, xi in ((16, 4), (256, 16), (CAPS_CONFIG5[20], 24)):
+        i = rows.index((0, ETF, C, xi, 2, SLO_BLOCKS))
+        r = O.replay_etlru(o.conv, o.q, o.a, o.ticks, C, xi, mu, tab, forced=True)
+        assert np.array_equal(bt.b(i).astype(np.uint64), r.b), (C, xi)
+        assert (res[i]["evicted_trim"], res[i]["evicted_lru"], res[i]["max_occupancy"]) == (
+            r.evicted_trim, r.evicted_lru, r.max_occupancy)
