@@ -302,7 +302,7 @@ tlru_status tlru_simulate_batch_ex(const tlru_trace* traces /*host[nt]*/, uint32
 /* Tuning / test knobs for tlru_simulate_batch on this thread (host; 0 = automatic).
  * segment_events: events per segment (rounded up to a multiple of 32; the cache
  *   state at each segment start is rebuilt exactly, so results do not depend on it).
- * state_entries: per-chain on-chip state entries W (one of 32..1024); chains that
+ * state_entries: per-chain on-chip state entries W (32, 64, 96, 128, 256, 512 or 1024); chains that
  *   outgrow it are re-run from global memory, so results do not depend on it. */
 tlru_status tlru_set_sim_options(uint32_t segment_events, uint32_t state_entries);
 

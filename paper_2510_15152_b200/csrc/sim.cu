@@ -454,8 +454,8 @@ __global__ void sim_results_kernel(uint32_t ni, const AccDev* acc, tlru_result* 
 }
 
 // ----------------------------------------------------------------------------- planner
-static const int kWClasses[] = {32, 64, 128, 256, 512, 1024};
-constexpr int kNumW = 6;
+static const int kWClasses[] = {32, 64, 96, 128, 256, 512, 1024};
+constexpr int kNumW = 7;
 constexpr int kSpillSlots = 128;
 
 static thread_local uint32_t g_opt_seg = 0;  // tlru_set_sim_options
@@ -560,12 +560,12 @@ static tlru_status make_plan(const tlru_trace* traces, uint32_t nt, const tlru_i
          in.policy == TLRU_POLICY_END_AWARE || in.policy == TLRU_POLICY_LENGTH_AWARE) &&
         g_opt_w < 0) {
       // End-/Length-Aware release a conversation's blocks at its last turn, so they too hold at
-      // most the open conversations (measured on the preset: 128 entries, no re-run, spectrum
-      // workload 2.5x faster than the capacity classes' 512 entries = one warp per SM)
+      // most the open conversations (~100 on the preset; measured: 96 entries, no re-run, spectrum
+      // rows of a trace 239 -> 96.5 -> 84.7 ms at 512 / 128 / 96 entries -- 512 is one warp per SM)
       // entries hold X >= 1 (tombstones are compacted before the state counts as full), so
       // W > C never overflows; the live conversations of a trace bound it too (<= ~91 on the
-      // preset): 128 entries, larger states are re-run by the fix-up from global memory
-      const uint32_t need = std::min<uint32_t>(C + 1, 128u);
+      // preset): 96 entries, larger states are re-run by the fix-up from global memory
+      const uint32_t need = std::min<uint32_t>(C + 1, 96u);
       int k = 0;
       while (k < kNumW - 1 && static_cast<uint32_t>(kWClasses[k]) < need) ++k;
       wc[i] = k;
@@ -1037,16 +1037,19 @@ static tlru_status run_engine(uint32_t engine, const tlru_trace* traces, uint32_
       case 1: TLRU_TRY((launch_w<64, false>(P.items[k], d, w, P.seg_len, uncached, st)));
               TLRU_TRY((launch_w<64, true>(ia, da, w, P.seg_len, uncached, st)));
               TLRU_TRY((launch_w<64, true, true>(in_, dn, w, P.seg_len, uncached, st))); break;
-      case 2: TLRU_TRY((launch_w<128, false>(P.items[k], d, w, P.seg_len, uncached, st)));
+      case 2: TLRU_TRY((launch_w<96, false>(P.items[k], d, w, P.seg_len, uncached, st)));
+              TLRU_TRY((launch_w<96, true>(ia, da, w, P.seg_len, uncached, st)));
+              TLRU_TRY((launch_w<96, true, true>(in_, dn, w, P.seg_len, uncached, st))); break;
+      case 3: TLRU_TRY((launch_w<128, false>(P.items[k], d, w, P.seg_len, uncached, st)));
               TLRU_TRY((launch_w<128, true>(ia, da, w, P.seg_len, uncached, st)));
               TLRU_TRY((launch_w<128, true, true>(in_, dn, w, P.seg_len, uncached, st))); break;
-      case 3: TLRU_TRY((launch_w<256, false>(P.items[k], d, w, P.seg_len, uncached, st)));
+      case 4: TLRU_TRY((launch_w<256, false>(P.items[k], d, w, P.seg_len, uncached, st)));
               TLRU_TRY((launch_w<256, true>(ia, da, w, P.seg_len, uncached, st)));
               TLRU_TRY((launch_w<256, true, true>(in_, dn, w, P.seg_len, uncached, st))); break;
-      case 4: TLRU_TRY((launch_w<512, false>(P.items[k], d, w, P.seg_len, uncached, st)));
+      case 5: TLRU_TRY((launch_w<512, false>(P.items[k], d, w, P.seg_len, uncached, st)));
               TLRU_TRY((launch_w<512, true>(ia, da, w, P.seg_len, uncached, st)));
               TLRU_TRY((launch_w<512, true, true>(in_, dn, w, P.seg_len, uncached, st))); break;
-      case 5: TLRU_TRY((launch_w<1024, false>(P.items[k], d, w, P.seg_len, uncached, st)));
+      case 6: TLRU_TRY((launch_w<1024, false>(P.items[k], d, w, P.seg_len, uncached, st)));
               TLRU_TRY((launch_w<1024, true, true>(in_, dn, w, P.seg_len, uncached, st))); break;
     }
   }
@@ -1058,10 +1061,11 @@ static tlru_status run_engine(uint32_t engine, const tlru_trace* traces, uint32_
       switch (k) {
         case 0: TLRU_TRY((launch_et<32>(v, d, w, m, uncached, st))); break;
         case 1: TLRU_TRY((launch_et<64>(v, d, w, m, uncached, st))); break;
-        case 2: TLRU_TRY((launch_et<128>(v, d, w, m, uncached, st))); break;
-        case 3: TLRU_TRY((launch_et<256>(v, d, w, m, uncached, st))); break;
-        case 4: TLRU_TRY((launch_et<512>(v, d, w, m, uncached, st))); break;
-        case 5: TLRU_TRY((launch_et<1024>(v, d, w, m, uncached, st))); break;
+        case 2: TLRU_TRY((launch_et<96>(v, d, w, m, uncached, st))); break;
+        case 3: TLRU_TRY((launch_et<128>(v, d, w, m, uncached, st))); break;
+        case 4: TLRU_TRY((launch_et<256>(v, d, w, m, uncached, st))); break;
+        case 5: TLRU_TRY((launch_et<512>(v, d, w, m, uncached, st))); break;
+        case 6: TLRU_TRY((launch_et<1024>(v, d, w, m, uncached, st))); break;
       }
     }
     // fix-up: re-run every segment whose start state was not exact (or that outgrew its slots)
@@ -1182,7 +1186,7 @@ extern "C" tlru_status tlru_set_sim_options(uint32_t segment_events, uint32_t st
   if (state_entries) {
     for (int k = 0; k < kNumW; ++k)
       if (static_cast<uint32_t>(kWClasses[k]) == state_entries) w = k;
-    if (w < 0) TLRU_FAIL(TLRU_EINVAL, "state_entries must be 0 or one of 32, 64, 128, 256, 512, 1024");
+    if (w < 0) TLRU_FAIL(TLRU_EINVAL, "state_entries must be 0 or one of 32, 64, 96, 128, 256, 512, 1024");
   }
   g_opt_seg = segment_events;
   g_opt_w = w;

@@ -14,7 +14,7 @@ tr = T.generate_traces([preset("wildchat", 0, 1_000_000)], exports=False)[0]
 pols = [int(x) for x in (sys.argv[1].split(",") if len(sys.argv) > 1 else "3,4,5")]
 rows = [(0, pol, C, xi, Q_HAT, SLO_BLOCKS) for pol in pols for C in CAPS_CONFIG5 for xi in (4, 8, 16, 24)]
 ref = None
-for W in (0, 128, 256, 512):
+for W in (0, 96, 128):
     T.set_sim_options(0, W)
     bt = T.prepare_batch([tr], rows)
     bt.run()
