@@ -135,6 +135,13 @@ tlru_status tlru_gen_workspace_size(const tlru_gen_params* p /*host*/, uint64_t 
 tlru_status tlru_count_events(const tlru_gen_params* p /*host*/, uint64_t* out /*host*/, void* ws,
                               size_t ws_bytes, cudaStream_t stream);
 
+/* Event slots of the trace `p` describes: turns allowed by the birth / death / turn clocks
+ * before the context-window rule drops any, so E <= slots.  A trace whose
+ * arrays hold >= slots entries is generated with one counting pass; with fewer (but >= E)
+ * tlru_generate_traces counts a second time, exactly.  Synchronizes `stream`. */
+tlru_status tlru_count_event_slots(const tlru_gen_params* p /*host*/, uint64_t* out /*host*/, void* ws,
+                                   size_t ws_bytes, cudaStream_t stream);
+
 /* Generate n traces (one per params entry) into traces[i] (host structs holding
  * device arrays).  capacity < E -> TLRU_ERANGE.  Fills num_events, max_history
  * and num_conversations.  Synchronizes `stream` once per trace (to read E). */

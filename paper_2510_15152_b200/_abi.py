@@ -12,6 +12,9 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libtlru.so")
+# measurement builds of the same sources with other compile-time tunables (tools/build_variant.py)
+if os.environ.get("TLRU_LIB_VARIANT"):
+    LIB_PATH = os.path.join(HERE, "variants", f"libtlru_{os.environ['TLRU_LIB_VARIANT']}.so")
 
 TLRU_NONE = 0xFFFFFFFF
 POLICY_LRU = 0
@@ -94,7 +97,7 @@ class SimStats(ctypes.Structure):
 
 
 EXPORTS = (
-    "tlru_last_error", "tlru_version", "tlru_launch_count", "tlru_trace_max_events", "tlru_gen_workspace_size", "tlru_count_events",
+    "tlru_last_error", "tlru_version", "tlru_launch_count", "tlru_trace_max_events", "tlru_gen_workspace_size", "tlru_count_events", "tlru_count_event_slots",
     "tlru_generate_traces", "tlru_upload_workspace_size", "tlru_trace_from_turns", "tlru_sim_workspace_size",
     "tlru_simulate_batch", "tlru_simulate_batch_ex", "tlru_set_sim_options", "tlru_set_sim_engine",
     "tlru_set_etlru_model", "tlru_last_sim_stats", "tlru_tail_workspace_size", "tlru_tail_metrics",
@@ -116,6 +119,7 @@ def _load():
         "tlru_trace_max_events": ([P(GenParams), P(u64)], st),
         "tlru_gen_workspace_size": ([P(GenParams), u64, P(sz)], st),
         "tlru_count_events": ([P(GenParams), P(u64), vp, sz, vp], st),
+        "tlru_count_event_slots": ([P(GenParams), P(u64), vp, sz, vp], st),
         "tlru_generate_traces": ([P(GenParams), u32, P(Trace), vp, sz, vp], st),
         "tlru_upload_workspace_size": ([u64, P(sz)], st),
         "tlru_trace_from_turns": ([vp, vp, vp, vp, u64, P(Trace), vp, sz, vp], st),

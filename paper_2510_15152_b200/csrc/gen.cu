@@ -519,6 +519,19 @@ extern "C" tlru_status tlru_count_events(const tlru_gen_params* p, uint64_t* out
   return run_count(p, w, stream, out, &mt, true);
 }
 
+extern "C" tlru_status tlru_count_event_slots(const tlru_gen_params* p, uint64_t* out, void* ws, size_t ws_bytes,
+                                              cudaStream_t stream) {
+  clear_error();
+  TLRU_TRY(validate_gen(p));
+  if (!out) TLRU_FAIL(TLRU_EINVAL, "out is NULL");
+  Carver cv(ws);
+  GenWs w;
+  TLRU_TRY(carve_gen(cv, p->num_conversations, 0, &w));
+  TLRU_TRY(check_ws(cv, ws, ws_bytes));
+  uint64_t mt;
+  return run_count(p, w, stream, out, &mt, false);
+}
+
 extern "C" tlru_status tlru_generate_traces(const tlru_gen_params* params, uint32_t n, tlru_trace* traces, void* ws,
                                             size_t ws_bytes, cudaStream_t st) {
   clear_error();

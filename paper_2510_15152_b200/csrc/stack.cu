@@ -48,6 +48,10 @@ constexpr int SND = 24;         // D values per chunk
 constexpr int S_THREADS = 256;  // events per s2 block
 constexpr uint32_t IT = 512;    // instance-table tile staged in shared memory by s2
 constexpr uint32_t WCH_MAX = 64;
+#ifndef TLRU_WIN_G
+#define TLRU_WIN_G 1
+#endif
+constexpr int WIN_G = TLRU_WIN_G;  // threads per window chunk in s2_win (window_phase)
 constexpr uint32_t GI_MAX = 64;                     // instances per s2_out group (hard limit)
 // Measured on B200 (config-5 sweep): groups of 13..24 instances are fastest.  Each CTA writes
 // one 16-byte store per instance row per 8 events, and the write stream loses DRAM efficiency
@@ -55,7 +59,11 @@ constexpr uint32_t GI_MAX = 64;                     // instances per s2_out grou
 // CTA, 5.9-6.9 with 8, 4.9 with 35); smaller groups re-read the per-event inputs more often.
 constexpr uint32_t GI_CAP = 16;
 constexpr uint32_t OUT_SMEM = 54u * 1024u;          // s2_out dynamic smem budget: 4 CTAs per SM
-constexpr uint32_t OUT_RANGE_MAX = 31u * 1024u;     // events per s2_out CTA (16-bit counters)
+#ifndef TLRU_OUT_RANGE
+#define TLRU_OUT_RANGE (31u * 1024u)
+#endif
+constexpr uint32_t OUT_RANGE_MAX = TLRU_OUT_RANGE;  // events per s2_out CTA (<= 31744: 16-bit counters)
+static_assert(OUT_RANGE_MAX <= 31u * 1024u && OUT_RANGE_MAX % 1024u == 0, "s2_out range");
 constexpr uint32_t TAB_MAX = 8192;                  // s2_out count table covers capacities < TAB_MAX
 
 struct ChunkDev {
@@ -260,39 +268,54 @@ __global__ void __launch_bounds__(T_THREADS) s1_totals_kernel(const ChunkDev* __
 }
 
 // ----------------------------------------------------------------------------- s2 common
-// Phase B of both s2 kernels: each thread takes window chunks `it` of the block and
-// accumulates, branch-free, sum L and sum max(L, Deff) per D pair over the chunk.
+// Phase B of the s2 kernels: groups of G adjacent threads take window chunks `it` of the block
+// and accumulate, branch-free, sum L and sum max(L, Deff) per D pair over the chunk.  Lane l of a
+// group reads the chunk's elements top - l, top - l - G, ..., so a group's loads are G
+// consecutive 8-byte records (G = 1: one thread per chunk, each lane of a warp on its own line --
+// the L1/TEX-bound form); the group's partial sums are then added by G - 1 xor-shuffles and its
+// lanes share the chunk's shared-memory atomics.
 // HT: the chunk has Threshold-LRU rows; element L then counts only where L >= T (T = 0 on the
 // other rows), and those rows (D = 0) have no free blocks.
-template <int ND, bool WITH_F, bool HT>
+template <int ND, bool WITH_F, bool HT, int G = 1>
 __device__ __forceinline__ void window_phase(const uint64_t* __restrict__ scanrec, uint32_t e0, uint32_t wch,
                                              const uint32_t* p_s, const uint32_t* cbeg_s, uint32_t ntot,
                                              const uint32_t* Deff, const uint32_t* Tr,
                                              uint32_t (*anf_s)[S_THREADS], uint32_t (*af_s)[S_THREADS]) {
+  static_assert(G >= 1 && G <= 32 && (G & (G - 1)) == 0, "G: a power of two <= 32");
   constexpr int NP = (ND + 1) / 2;
+  constexpr uint32_t NG = S_THREADS / G;  // groups per CTA
   uint32_t Dpk[NP], Tpk[NP];
 #pragma unroll
   for (int q = 0; q < NP; ++q) {
     Dpk[q] = Deff[2 * q] | (Deff[min(2 * q + 1, ND - 1)] << 16);
     Tpk[q] = HT ? (Tr[2 * q] | (Tr[min(2 * q + 1, ND - 1)] << 16)) : 0u;  // T <= 65535 (validated)
   }
-  for (uint32_t it = threadIdx.x; it < ntot; it += S_THREADS) {
-    uint32_t lo = 0, hi = S_THREADS;  // owner event: last j with cbeg_s[j] <= it
-    while (hi - lo > 1) {
-      const uint32_t mid = (lo + hi) >> 1;
-      if (cbeg_s[mid] <= it) lo = mid; else hi = mid;
+  const uint32_t lane = threadIdx.x % G, grp = threadIdx.x / G;
+  // G > 1: every thread runs the same number of rounds (the shuffles need whole warps)
+  const uint32_t rounds = G > 1 ? (ntot + NG - 1) / NG : 0u;
+  for (uint32_t r = 0, it = grp; G > 1 ? r < rounds : it < ntot; ++r, it += NG) {
+    uint32_t j = 0, ej = 0, top = 0, n = 0;
+    if (it < ntot) {
+      uint32_t lo = 0, hi = S_THREADS;  // owner event: last j with cbeg_s[j] <= it
+      while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (cbeg_s[mid] <= it) lo = mid; else hi = mid;
+      }
+      j = lo;
+      ej = e0 + j;
+      const uint32_t pj = p_s[j];
+      top = ej - 1 - (it - cbeg_s[j]) * wch;  // chunk covers [bot, top]
+      const uint32_t bot = max(pj + 1, top >= wch - 1 ? top - (wch - 1) : 0u);
+      n = top + 1 - bot;
     }
-    const uint32_t j = lo, ej = e0 + j, pj = p_s[j];
-    const uint32_t top = ej - 1 - (it - cbeg_s[j]) * wch;  // chunk covers [bot, top]
-    const uint32_t bot = max(pj + 1, top >= wch - 1 ? top - (wch - 1) : 0u);
     // a dead element (its conversation returns before ej) counts as L = 0; with n elements:
     //   A_nf = sum max(L, D) - n D,   A_f = sum L + n D - sum max(L, D)   (max + min = L + D)
     uint32_t mx2[NP], sumL = 0;
 #pragma unroll
     for (int q = 0; q < NP; ++q) mx2[q] = 0;
-    for (uint32_t x = top + 1; x-- > bot;) {
-      const uint64_t r = __ldg(scanrec + x);
-      const uint32_t L = static_cast<uint32_t>(r) > ej ? static_cast<uint32_t>(r >> 32) : 0u;
+    for (uint32_t k = lane; k < n; k += G) {
+      const uint64_t r_ = __ldg(scanrec + (top - k));
+      const uint32_t L = static_cast<uint32_t>(r_) > ej ? static_cast<uint32_t>(r_ >> 32) : 0u;
       if (WITH_F) sumL += L;
       const uint32_t L2 = L * 0x10001u;  // L in both 16-bit halves
 #pragma unroll
@@ -301,13 +324,21 @@ __device__ __forceinline__ void window_phase(const uint64_t* __restrict__ scanre
         else mx2[q] = __vadd2(mx2[q], __vmaxu2(L2, Dpk[q]));
       }
     }
-    const uint32_t n = top + 1 - bot;
+    if (G > 1) {  // the chunk's sums (< 2^16 per half: wch * maxL < 2^16)
+#pragma unroll
+      for (int o = 1; o < G; o <<= 1) {
+#pragma unroll
+        for (int q = 0; q < NP; ++q) mx2[q] = __vadd2(mx2[q], __shfl_xor_sync(0xFFFFFFFFu, mx2[q], o));
+        if (WITH_F) sumL += __shfl_xor_sync(0xFFFFFFFFu, sumL, o);
+      }
+    }
+    if (n == 0) continue;
 #pragma unroll
     for (int q = 0; q < NP; ++q) {
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int d = 2 * q + h;
-        if (d < ND) {
+        if (d < ND && (G == 1 || d % G == static_cast<int>(lane))) {
           const uint32_t smax = h ? (mx2[q] >> 16) : (mx2[q] & 0xFFFFu);
           const uint32_t nD = n * Deff[d];
           atomicAdd(&anf_s[d][j], smax - nD);
@@ -596,7 +627,7 @@ __global__ void __launch_bounds__(S_THREADS, 4) s2_win_kernel(const uint64_t* __
   uint32_t Deff[ND];
 #pragma unroll
   for (int d = 0; d < ND; ++d) Deff[d] = min(ch.D[d], maxL);
-  window_phase<ND, false, HT>(scanrec, e0, wch, p_s, cbeg_s, ntot, Deff, ch.T, anf_s, nullptr);
+  window_phase<ND, false, HT, WIN_G>(scanrec, e0, wch, p_s, cbeg_s, ntot, Deff, ch.T, anf_s, nullptr);
   __syncthreads();
   const uint32_t e = e0 + t;
   if (e >= E) return;

@@ -98,11 +98,12 @@ def _alloc_trace(E: int, device, exports: bool) -> DeviceTrace:
 
 
 def generate_traces(params: list[dict], device="cuda", exports: bool = True, stream=None,
-                    capacity: str = "exact") -> list[DeviceTrace]:
+                    capacity: str = "slots") -> list[DeviceTrace]:
     """tlru_generate_traces for each params dict (fields of tlru_gen_params).
 
-    capacity: "exact" sizes the trace with tlru_count_events; "bound" with
-    tlru_trace_max_events (N * max_turns)."""
+    capacity: "slots" (default) sizes the trace with tlru_count_event_slots, so every later
+    regeneration into it takes one counting pass; "exact" with tlru_count_events (E entries:
+    regenerations count twice); "bound" with tlru_trace_max_events (N * max_turns)."""
     out = []
     st = _stream(stream)
     for p in params:
@@ -114,7 +115,8 @@ def generate_traces(params: list[dict], device="cuda", exports: bool = True, str
         else:
             check(lib.tlru_gen_workspace_size(ctypes.byref(g), 0, ctypes.byref(sz)))
             ws = _workspace(sz.value, device)
-            check(lib.tlru_count_events(ctypes.byref(g), ctypes.byref(E), _ptr(ws), sz.value, st))
+            count = lib.tlru_count_event_slots if capacity == "slots" else lib.tlru_count_events
+            check(count(ctypes.byref(g), ctypes.byref(E), _ptr(ws), sz.value, st))
         tr = _alloc_trace(E.value, device, exports)
         check(lib.tlru_gen_workspace_size(ctypes.byref(g), tr.sim.numel(), ctypes.byref(sz)))
         ws = _workspace(sz.value, device)

@@ -194,7 +194,7 @@ def test_generator_bit_exact(T, name, seed, n):
     assert g.max_history == int(d.L_after.max()) and g.num_conversations == np.unique(o.conv).size
 
 
-@pytest.mark.parametrize("capacity", ["exact", "bound"])
+@pytest.mark.parametrize("capacity", ["exact", "slots", "bound"])
 def test_generator_context_cap_bit_exact(T, capacity):
     """L_max small enough that the context window ends conversations: with exact
     capacity the exact count path runs, with the N * max_turns bound the capped
@@ -212,6 +212,26 @@ def test_generator_context_cap_bit_exact(T, capacity):
     d = O.derive(o.conv, o.q, o.a)
     assert np.array_equal(prev, d.prev) and np.array_equal(La, d.L_after) and La.max() <= 30
     assert np.array_equal(g.next[:E].cpu().numpy().view(np.uint32), d.next)
+    if capacity == "slots":  # the clock-only slot count bounds E; this cap drops some turns
+        assert g.sim.numel() > E
+
+
+def test_event_slots_bound_events(T):
+    """tlru_count_event_slots >= tlru_count_events (= the oracle's E); equal without the cap."""
+    import ctypes
+    from paper_2510_15152_b200 import _abi as A
+    for cap in (30, 65535):
+        p = preset("wildchat", 5, 3000)
+        p["max_history_blocks"] = cap
+        g = T._gen_struct(p)
+        sz = ctypes.c_size_t()
+        A.check(A.lib.tlru_gen_workspace_size(ctypes.byref(g), 0, ctypes.byref(sz)))
+        ws = torch.empty(sz.value, dtype=torch.uint8, device="cuda")
+        E, S = ctypes.c_uint64(), ctypes.c_uint64()
+        A.check(A.lib.tlru_count_events(ctypes.byref(g), ctypes.byref(E), T._ptr(ws), sz.value, None))
+        A.check(A.lib.tlru_count_event_slots(ctypes.byref(g), ctypes.byref(S), T._ptr(ws), sz.value, None))
+        assert E.value == O.generate(p).E
+        assert (S.value > E.value) if cap == 30 else (S.value >= E.value)
 
 
 # ----------------------------------------------------------------------------- config 3: 10^4 conversations
