@@ -262,6 +262,50 @@ def workload_global(name: str):
         "step) x 25 capacities (16..4096 blocks, geometric) x 20 xi (2..40 blocks) x {LRU, T-LRU} = 10^4 instances")
 
 
+NEXT_FAMILIES = (  # (name, policies, xi values, what) -- DESIGN.md 6, bench --config <name> for the full workloads
+    ("spectrum", (3, 4, 5), (4, 8, 16, 24), "End-Aware, Length-Aware T-LRU, Tail-Optimized Belady (P:389-395, Thm 1)"),
+    ("threshold_lru", (2,), None, "Threshold-LRU, 1024 tokens = 8 blocks (P:307, P:322), stack engine"),
+    ("forced", (7,), (4, 8, 16, 24), "T-LRU under forced caching (App. C)"),
+    ("forced_belady", (8,), (4, 8, 16, 24), "Tail-Optimized Belady under forced caching (App. C, P:657-662)"),
+    ("etlru", (6,), (4, 8, 16, 24), "ET-LRU (Def. 1 / Alg. 2), belief mu = 1/90 s, the preset's prompt law"),
+    ("etlru_forced", (9,), (4, 8, 16, 24), "ET-LRU under forced caching (App. C, P:664-672)"),
+)
+
+
+def measure_next_rows(T, trace, HB, stream):
+    """One batch per NEXT family on one resident config-5 trace: 25 capacities x its xi values x its
+    policies; one warm-up call, then one call timed with CUDA events on `stream`."""
+    import torch
+
+    from paper_2510_15152_b200.inputs import (CAPS_CONFIG5, Q_HAT, SLO_BLOCKS, THRESHOLD_BLOCKS, WILDCHAT,
+                                              XI_CONFIG5, prompt_law_ln_surv)
+    T.set_etlru_model(WILDCHAT["death_rate"] * 1e-6, prompt_law_ln_surv(WILDCHAT))
+    out = {}
+    for name, pols, xis, what in NEXT_FAMILIES:
+        rows = [(0, pol, C, xi, Q_HAT, SLO_BLOCKS) + ((THRESHOLD_BLOCKS,) if pol == 2 else ())
+                for pol in pols for C in CAPS_CONFIG5 for xi in (xis or XI_CONFIG5)]
+        bt = T.prepare_batch([trace], rows, hist_bins=HB)
+        bt.run()
+        torch.cuda.synchronize()
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        bt.run()
+        t1.record(stream)
+        torch.cuda.synchronize()
+        st = T.last_sim_stats()
+        assert st["failed_chains"] == 0
+        ms = t0.elapsed_time(t1)
+        req = trace.num_events * len(rows)
+        out[name] = {"value": req / (ms / 1000.0), "unit": "requests/s", "ms": ms, "instances": len(rows),
+                     "requests": req, "what": what,
+                     "engine": {0: "replay", 1: "stack", 2: "mixed"}.get(st["engine"], str(st["engine"])),
+                     "spilled_chains": st["spilled_chains"],
+                     "sample": "rank 0's first config-5 trace (10^6 conversations), resident in HBM; one call of "
+                               "tlru_simulate_batch incl. tail metrics (no generation)"}
+        del bt
+    return out
+
+
 def run_ours(args, rank, world, local_rank):
     import ctypes
 
@@ -389,6 +433,13 @@ def run_ours(args, rank, world, local_rank):
         rep = dict(r, k2=statistics.mean(r["out"]), requests=traces[0].num_events * len(sub), instances=len(sub),
                    stats=rst)
         del rbatch
+
+    # ---- the paper's other policies on rank 0's first trace, one call each,
+    # timed on the device (the trace is already resident; generation is not in these figures).  Before the e2e
+    # arm, whose upload without ticks rewrites the trace's time_ticks with event indices
+    next_rows = None
+    if args.config == "config5" and rank == 0 and not args.no_next and traces:
+        next_rows = measure_next_rows(T, traces[0], HB, stream)
 
     # ---- e2e: the same step through the public API from pinned host buffers (H2D of each trace's
     # turns on stream A, upload + simulation + pooling on the simulation streams, the collectives),
@@ -566,6 +617,11 @@ def run_ours(args, rank, world, local_rank):
                          "frac": rep_achieved / peak, "kernel": "sim_kernel<W> (K2 replay)"},
             "note": "Alg. 1 replayed request by request (one lane per instance) on the first trace's instances; "
                     "b bytes, histograms and results identical to the stack engine"}
+    if next_rows is not None:
+        for v in next_rows.values():
+            v["roofline_10B"] = {"achieved": ALGO_BYTES_PER_REQUEST * v["value"] / 1e9, "peak": peak, "unit": "GB/s",
+                                 "frac": ALGO_BYTES_PER_REQUEST * v["value"] / 1e9 / peak}
+        line["next_rows"] = next_rows
     if not args.no_cpu_baseline and world == 1:  # the CPU oracle baseline: rank 0 at N = 1 only
         line["cpu_baseline"] = cpu_oracle_baseline(args.conversations)
     print(json.dumps(line), flush=True)
@@ -580,6 +636,7 @@ def main():
     ap.add_argument("--conversations", type=int, default=1_000_000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-replay", action="store_true", help="skip timing the replay engine")
+    ap.add_argument("--no-next", action="store_true", help="skip the NEXT-row policy measurements")
     ap.add_argument("--replay-instances", type=int, default=0, help="limit the replay-engine sample (0 = all of seed 0)")
     ap.add_argument("--config", choices=("config5", "config5x3", "spectrum", "etlru", "forced", "forced_belady",
                                          "etlru_forced", "config4"),

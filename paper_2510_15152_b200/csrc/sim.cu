@@ -601,10 +601,11 @@ static tlru_status make_plan(const tlru_trace* traces, uint32_t nt, const tlru_i
     }
     order.swap(keep);
     ni_lanes = static_cast<uint32_t>(order.size());
-    if (P->n_et) {  // segments: enough warps to fill the GPU, each >= 2x the burn-in
-      const uint64_t pe = (148ull * 24ull + P->n_et - 1) / P->n_et;
-      uint64_t sl = Emax ? (Emax + pe - 1) / pe : 8192;
-      sl = std::min<uint64_t>(std::max<uint64_t>(sl, 2ull * P->et_burn), 1ull << 24);
+    if (P->n_et) {  // segments of 3x the burn-in: the warps are latency-bound and their costs differ by
+      // capacity, so many short warps balance better than one wave of long ones (measured on B200,
+      // 10^6-conversation traces: 100 instances 1.6e8 -> 4.0e8 requests/s, 1000 instances 4.1e8 -> 5.2e8
+      // against "148 x 24 warps"; profiles/r02_perf.md)
+      uint64_t sl = 3ull * P->et_burn;
       if (g_opt_seg) sl = std::max<uint32_t>(g_opt_seg, 64);  // tests: short segments exercise the fix-up
       P->et_seg_len = static_cast<uint32_t>((sl + 31) & ~31ull);
       for (uint32_t k = 0; k < P->n_et; ++k) {
@@ -668,14 +669,12 @@ static tlru_status make_plan(const tlru_trace* traces, uint32_t nt, const tlru_i
   seg = (seg + 31) & ~31ull;
   P->seg_len = static_cast<uint32_t>(seg);
   {  // aware segments: enough warps to fill the GPU, but >= 2x the burn-in
-    uint64_t ag = 0;
     for (const GroupDev& g : P->groups) {
-      ag += g.aware ? 1u : 0u;
       P->any_forced = P->any_forced || g.aware == kAwareForced;
     }
-    const uint64_t pa = ag ? (148ull * 8ull + ag - 1) / ag : 1;
-    uint64_t sa = Emax ? (Emax + pa - 1) / pa : 8192;
-    sa = std::min<uint64_t>(std::max<uint64_t>(sa, P->any_forced ? P->aburn_long : 2ull * P->aburn), 1ull << 20);
+    // 3x the burn-in (forced caching: its long burn-in): short latency-bound warps balance better than
+    // one wave of long ones (spectrum workload 1.30e10 -> 1.46e10 requests/s against "148 x 8 warps")
+    uint64_t sa = P->any_forced ? P->aburn_long : 3ull * P->aburn;
     if (g_opt_seg) sa = std::max<uint32_t>(g_opt_seg, 64);  // tests: short segments exercise the fix-up
     P->aseg = static_cast<uint32_t>((sa + 31) & ~31ull);
   }
