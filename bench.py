@@ -465,6 +465,8 @@ def run_ours(args, rank, world, local_rank):
     h2d_bytes += sum(h.numel() * 8 for h in host_ticks if h is not None)
     d2h_bytes = host_table.numel() + host_ptails.numel()
 
+    sU = torch.cuda.Stream(device=dev)  # uploads (each step ends with a host sync, so no cross-step hazard)
+
     def e2e_step():
         with torch.cuda.stream(stream):
             sw.pooled.zero_()
@@ -473,23 +475,31 @@ def run_ours(args, rank, world, local_rank):
         sA.wait_event(ev0)
         for sB in sBs:
             sB.wait_event(ev0)
-        for j, ((hc, hq, ha), (dc, dq, da), tr, ts, w) in enumerate(
-                zip(host_turns, dev_turns, traces, sw.sim_tstructs, up_ws)):
-            sB = sBs[j % len(sBs)]
+        # every trace's H2D copies queued first on stream A; each upload (which synchronizes its own
+        # stream to read its validation flags) runs on stream U, so the host waits only for that
+        # trace's copy + upload while the simulation streams keep the GPU busy with earlier traces
+        evh = []
+        for j, ((hc, hq, ha), (dc, dq, da)) in enumerate(zip(host_turns, dev_turns)):
             with torch.cuda.stream(sA):
                 dc.copy_(hc, non_blocking=True)
                 dq.copy_(hq, non_blocking=True)
                 da.copy_(ha, non_blocking=True)
                 if dev_ticks[j] is not None:
                     dev_ticks[j].copy_(host_ticks[j], non_blocking=True)
-            ev = torch.cuda.Event()
-            ev.record(sA)
-            sB.wait_event(ev)
+            evh.append(torch.cuda.Event())
+            evh[-1].record(sA)
+        for j, ((dc, dq, da), tr, ts, w) in enumerate(zip(dev_turns, traces, sw.sim_tstructs, up_ws)):
+            sB = sBs[j % len(sBs)]
+            sU.wait_event(evh[j])
             _abi.check(_abi.lib.tlru_trace_from_turns(T._ptr(dc), T._ptr(dq), T._ptr(da), T._ptr(dev_ticks[j]),
                                                       tr.num_events, ctypes.byref(ts), T._ptr(w), w.numel(),
-                                                      T._stream(sB)))
+                                                      T._stream(sU)))
+            ev = torch.cuda.Event()
+            ev.record(sU)
+            sB.wait_event(ev)
             sw.simulate(j, sB)
         stream.wait_stream(sA)
+        stream.wait_stream(sU)
         for sB in sBs:
             stream.wait_stream(sB)
         sw.combine(stream)
