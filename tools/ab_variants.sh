@@ -1,3 +1,4 @@
+# usage: bash tools/ab_variants.sh "" name1 name2 ... (variants built by tools/build_variant.py)
 # A/B of libtlru variants: s2_out / s2_win alone (ncu, one config-5 trace) and the bench step
 for v in "$@"; do
   TLRU_LIB_VARIANT=$v ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"s2_out|s2_win" --csv python tools/stack_probe.py > gpurun_out/n_$v.csv 2>&1
