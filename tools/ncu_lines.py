@@ -8,7 +8,7 @@ import sys
 rep, kern = sys.argv[1], sys.argv[2]
 thr = float(sys.argv[3]) if len(sys.argv) > 3 else 0.01
 txt = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass",
-                      "--kernel-name", f"regex:{kern}"], capture_output=True, text=True).stdout
+                      "--kernel-name", f"regex:{kern}", "--launch-count", "1"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(txt)))
 hh = [i for i, r in enumerate(rows) if r[:2] == ["Line No", "Source"]][0]
 h = rows[hh]

@@ -84,14 +84,22 @@ int main() {
     printf("%-48s %.3f ms  %6.0f GB/s %s\n", name, best, bytes / best / 1e6, e ? cudaGetErrorString(e) : "");
   };
   char nm[128];
-  for (uint32_t R : {31744u, 8192u}) {
+  auto cur = [&](auto kern, int WB, int WS, uint32_t R) {
     const uint32_t nr = static_cast<uint32_t>((row_len + R - 1) / R);
-    const int sm = 2 * 6 * 4096;
-    cudaFuncSetAttribute(cur_kernel<6, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-    snprintf(nm, sizeof nm, "cur WB=6 WS=2 R=%u", R);
-    run(nm, [&] { cur_kernel<6, 2><<<dim3(ng, nr), 256, sm>>>(buf, row_len, G, R); });
+    const int sm = WS * WB * 4096;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    snprintf(nm, sizeof nm, "cur WB=%d WS=%d R=%u", WB, WS, R);
+    run(nm, [&] { kern<<<dim3(ng, nr), 256, sm>>>(buf, row_len, G, R); });
+  };
+  for (uint32_t R : {31744u, 8192u, 4096u}) {
+    cur(cur_kernel<6, 2>, 6, 2, R);
+    cur(cur_kernel<1, 4>, 1, 4, R);
+    cur(cur_kernel<1, 8>, 1, 8, R);
+    cur(cur_kernel<2, 4>, 2, 4, R);
+    cur(cur_kernel<4, 3>, 4, 3, R);
+    cur(cur_kernel<16, 1>, 16, 1, R);
   }
-  for (uint32_t R : {2048u, 4096u, 8192u}) {
+  for (uint32_t R : {4096u}) {
     const uint32_t nr = static_cast<uint32_t>((row_len + R - 1) / R);
     for (uint32_t pad : {0u, 24576u}) {
       {
