@@ -243,6 +243,12 @@ __global__ void __launch_bounds__(32) sim_kernel(const ItemDev* __restrict__ ite
     }
     for (uint32_t k = 0; k < nk; ++k) {
       const uint64_t ev = shfl64(evc, k);
+      // Synchronised compaction: when one lane's array is full (it must drop its tombstones before
+      // this insert), every lane compacts now -- the warp runs the loop once for all of them instead
+      // of once per lane at 32 different events.  Compaction only re-packs the live entries (the
+      // state is unchanged), so the outputs are identical.  Belady lanes keep their own (centred) layout.
+      if (!bel && __any_sync(0xFFFFFFFFu, active && c.tail == c.W) && active && c.head < c.tail)
+        chain_compact<AWARE>(c, st);
       if (AWARE) {
         const uint32_t qn = __shfl_sync(0xFFFFFFFFu, qnc, k);
         if (bel) {
