@@ -96,6 +96,13 @@ struct EtState {
   unsigned long long ev_free, ev_other;
   bool overflow;
   bool forced;  // theta is not a candidate while its turn is served (Y_theta = L, App. C)
+  // Incremental candidates (inc, the large slot classes): every lane keeps the two smallest
+  // (key, tau) of ITS slots (slot s belongs to lane s % 32) -- bk1/bt1 at slot bs1, then bk2/bt2 --
+  // so an eviction round needs no scan: only the lanes whose slots changed recompute theirs,
+  // the whole warp reading one such lane's <= 32 slots at once (et_rescan).
+  bool inc;
+  uint64_t bk1, bk2;
+  uint32_t bt1, bt2, bs1;
 
   __device__ __forceinline__ void carve(unsigned char* pool, uint32_t c) {
     cap = c;
@@ -114,6 +121,79 @@ struct EtState {
   }
 };
 
+#ifndef TLRU_ET_INC_MIN
+#define TLRU_ET_INC_MIN 256u
+#endif
+constexpr uint32_t kEtIncMin = TLRU_ET_INC_MIN;  // slot classes from this size keep incremental candidates
+
+__device__ __forceinline__ bool et_less(uint64_t k, uint32_t t, uint64_t K, uint32_t T) {
+  return k < K || (k == K && t < T);
+}
+
+// Lane o's two smallest (key, tau) over its slots o, o + 32, ... (< S.n, != ex), read by the whole
+// warp (one slot per lane while S.n <= 1024) and reduced with the same redux steps as a round.
+__device__ __forceinline__ void et_rescan(EtState& S, uint32_t o, uint32_t ex) {
+  const uint32_t lane = threadIdx.x & 31;
+  uint64_t a1 = ~0ull, a2 = ~0ull;
+  uint32_t u1 = 0xFFFFFFFFu, u2 = 0xFFFFFFFFu, s1 = 0;
+  for (uint32_t s = o + 32u * lane; s < S.n; s += 1024u) {
+    if (s == ex) continue;
+    const uint64_t k = S.key[s];
+    const uint32_t t = S.tau[s];
+    if (et_less(k, t, a1, u1)) {
+      a2 = a1;
+      u2 = u1;
+      a1 = k;
+      u1 = t;
+      s1 = s;
+    } else if (et_less(k, t, a2, u2)) {
+      a2 = k;
+      u2 = t;
+    }
+  }
+  uint64_t m1, m2;
+  uint32_t n1, n2;
+  et_warp_min(a1, u1, m1, n1);
+  const int wl = __ffs(__ballot_sync(0xFFFFFFFFu, a1 == m1 && u1 == n1)) - 1;
+  const uint32_t ms = __shfl_sync(0xFFFFFFFFu, s1, wl);
+  if (static_cast<int>(lane) == wl) {
+    a1 = a2;
+    u1 = u2;
+  }
+  et_warp_min(a1, u1, m2, n2);
+  if (lane == o) {
+    S.bk1 = m1;
+    S.bt1 = n1;
+    S.bs1 = ms;
+    S.bk2 = m2;
+    S.bt2 = n2;
+  }
+}
+
+// Slot s (key k, tau t) joins its owner lane's candidates (a new slot; keys only grow otherwise).
+__device__ __forceinline__ void et_offer(EtState& S, uint32_t s, uint64_t k, uint32_t t) {
+  if ((threadIdx.x & 31) != (s & 31u)) return;
+  if (et_less(k, t, S.bk1, S.bt1)) {
+    S.bk2 = S.bk1;
+    S.bt2 = S.bt1;
+    S.bk1 = k;
+    S.bt1 = t;
+    S.bs1 = s;
+  } else if (et_less(k, t, S.bk2, S.bt2)) {
+    S.bk2 = k;
+    S.bt2 = t;
+  }
+}
+
+// Every lane's candidates from scratch (after a snapshot load).
+__device__ __forceinline__ void et_cand_init(EtState& S) {
+  S.bk1 = S.bk2 = ~0ull;
+  S.bt1 = S.bt2 = 0xFFFFFFFFu;
+  S.bs1 = 0;
+  if (!S.inc) return;
+  for (uint32_t s = threadIdx.x & 31; s < S.n; s += 32) et_offer(S, s, S.key[s], S.tau[s]);
+}
+
 // One request (event e, sim view ev, time tk).  Returns b = J - X_theta (valid in every lane).
 __device__ __forceinline__ uint32_t et_request(EtState& S, const EtCtx& m, uint32_t e, uint64_t ev, uint64_t tk) {
   const int lane = threadIdx.x & 31;
@@ -130,9 +210,14 @@ __device__ __forceinline__ uint32_t et_request(EtState& S, const EtCtx& m, uint3
       const uint32_t p = static_cast<uint32_t>(__shfl_sync(0xFFFFFFFFu, hit, __ffs(bal) - 1));
       x_old = S.X[p];
       __syncwarp();
-      if (lane == 0 && p != S.n - 1) S.move_slot(p, S.n - 1);
+      const uint32_t last = S.n - 1;
+      if (lane == 0 && p != last) S.move_slot(p, last);
       --S.n;
       __syncwarp();
+      if (S.inc) {  // slot p now holds the former last slot
+        et_rescan(S, p & 31u, 0xFFFFFFFFu);
+        if ((last & 31u) != (p & 31u)) et_rescan(S, last & 31u, 0xFFFFFFFFu);
+      }
     }
   }
   const uint32_t b = J - x_old;  // job - x
@@ -141,13 +226,17 @@ __device__ __forceinline__ uint32_t et_request(EtState& S, const EtCtx& m, uint3
     S.overflow = true;
     return b;
   }
-  if (lane == 0) {
+  {
     const double bs = __dmul_rn(static_cast<double>(tk), m.mu);
-    S.base[S.n] = bs;
-    S.key[S.n] = et_ord(__dadd_rn(bs, m.lg(S.xi)));  // X = L: k = xi
-    S.tau[S.n] = e;
-    S.X[S.n] = static_cast<uint16_t>(La);
-    S.L[S.n] = static_cast<uint16_t>(La);
+    const uint64_t kt = et_ord(__dadd_rn(bs, m.lg(S.xi)));  // X = L: k = xi
+    if (lane == 0) {
+      S.base[S.n] = bs;
+      S.key[S.n] = kt;
+      S.tau[S.n] = e;
+      S.X[S.n] = static_cast<uint16_t>(La);
+      S.L[S.n] = static_cast<uint16_t>(La);
+    }
+    if (S.inc && !S.forced) et_offer(S, S.n, kt, e);  // forced: theta joins after its turn
   }
   ++S.n;
   S.used += La - x_old;
@@ -158,8 +247,15 @@ __device__ __forceinline__ uint32_t et_request(EtState& S, const EtCtx& m, uint3
     const uint32_t over = S.used - S.C;
     uint64_t k1 = ~0ull, k2 = ~0ull;
     uint32_t t1 = 0xFFFFFFFFu, t2 = 0xFFFFFFFFu, s1 = 0;
+    if (S.inc) {
+      k1 = S.bk1;
+      t1 = S.bt1;
+      s1 = S.bs1;
+      k2 = S.bk2;
+      t2 = S.bt2;
+    }
 #pragma unroll 4
-    for (uint32_t s = lane; s < S.n; s += 32) {
+    for (uint32_t s = lane; !S.inc && s < S.n; s += 32) {
       if (s == th) continue;
       const uint64_t ks = S.key[s];
       const uint32_t ts = S.tau[s];
@@ -217,10 +313,11 @@ __device__ __forceinline__ uint32_t et_request(EtState& S, const EtCtx& m, uint3
     S.used -= cnt;
     const uint32_t xn = xj - cnt;
     __syncwarp();
-    if (xn == 0 && j != S.n - 1 && th == S.n - 1) th = j;  // theta moves into j's slot
+    const uint32_t last = S.n - 1;
+    if (xn == 0 && j != last && th == last) th = j;  // theta moves into j's slot
     if (lane == 0) {
       if (xn == 0) {
-        if (j != S.n - 1) S.move_slot(j, S.n - 1);
+        if (j != last) S.move_slot(j, last);
       } else {
         S.X[j] = static_cast<uint16_t>(xn);
         S.key[j] = et_ord(__dadd_rn(bj, m.lg(int64_t(xn) - Lj + S.xi)));
@@ -228,6 +325,14 @@ __device__ __forceinline__ uint32_t et_request(EtState& S, const EtCtx& m, uint3
     }
     if (xn == 0) --S.n;
     __syncwarp();
+    if (S.inc) {  // j's key grew or j now holds the former last slot
+      et_rescan(S, j & 31u, th);
+      if (xn == 0 && (last & 31u) != (j & 31u)) et_rescan(S, last & 31u, th);
+    }
+  }
+  if (S.inc && S.forced && th != 0xFFFFFFFFu) {  // theta is a candidate again after its turn
+    __syncwarp();
+    et_offer(S, th, S.key[th], S.tau[th]);
   }
   S.max_occ = max(S.max_occ, S.used);
   return b;
@@ -297,6 +402,7 @@ __device__ void et_snap_load(EtState& S, const EtCtx& m, const TraceDev& tr, con
   S.n = n;
   S.used = in[1];
   __syncwarp();
+  et_cand_init(S);
 }
 
 __device__ __forceinline__ void et_ctx_init(EtCtx& c, const EtModel& m, double* tab_s) {
@@ -316,6 +422,8 @@ __device__ __forceinline__ void et_state_init(EtState& S, uint32_t C, uint32_t x
   S.ev_free = S.ev_other = 0;
   S.overflow = false;
   S.forced = forced;
+  S.inc = S.cap >= kEtIncMin;
+  et_cand_init(S);
 }
 
 // One warp per (instance, segment); W slots in shared memory after the table copy.
