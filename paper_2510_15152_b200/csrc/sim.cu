@@ -460,6 +460,9 @@ __global__ void sim_results_kernel(uint32_t ni, const AccDev* acc, tlru_result* 
 }
 
 // ----------------------------------------------------------------------------- planner
+#ifndef TLRU_FORCED_BURN
+#define TLRU_FORCED_BURN 8192u  // forced-caching lanes' burn-in (fragments kept only by Phase 2 can be old)
+#endif
 static const int kWClasses[] = {32, 64, 96, 128, 256, 512, 1024};
 constexpr int kNumW = 7;
 constexpr int kSpillSlots = 128;
@@ -497,7 +500,7 @@ struct Plan {
   std::vector<ItemDev> items_nos[kNumW];    // End-Aware / forced-caching segments (no surplus array)
   bool any_aware = false;
   std::vector<uint32_t> alane, atrace;       // aware lane -> global lane index, trace
-  uint32_t aseg = 8192, aburn = 4096, aburn_long = 16384, anseg_max = 1, awsnap = 32;
+  uint32_t aseg = 8192, aburn = 4096, aburn_long = TLRU_FORCED_BURN, anseg_max = 1, awsnap = 32;
   bool any_forced = false;
   std::vector<EtItem> et_items;              // ET-LRU instances (etlru.cuh)
   std::vector<EtSeg> et_segs[kNumW];         // their (instance, segment) warps per state class
