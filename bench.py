@@ -467,17 +467,26 @@ def run_ours(args, rank, world, local_rank):
 
     sU = torch.cuda.Stream(device=dev)  # uploads (each step ends with a host sync, so no cross-step hazard)
 
+    simdone = [torch.cuda.Event() for _ in traces]  # trace j's simulation of the previous step
+    d2h_done = [None]  # the previous step's result read-back (host waits on it one step later)
+
     def e2e_step():
+        """One step from pinned host buffers.  Steps are pipelined one deep: step i+1's H2D copies
+        and uploads start while step i's last simulations, collectives and D2H still run, and the
+        host waits for step i's result read-back during step i+1 (the last one before the timer
+        stops).  Hazards: trace j's upload waits for trace j's previous simulation (its arrays are
+        rewritten); the simulations wait for this step's pool reset, which follows the previous
+        step's collectives and D2H on `stream`."""
         with torch.cuda.stream(stream):
             sw.pooled.zero_()
         ev0 = torch.cuda.Event()
         ev0.record(stream)
-        sA.wait_event(ev0)
         for sB in sBs:
             sB.wait_event(ev0)
-        # every trace's H2D copies queued first on stream A; each upload (which synchronizes its own
-        # stream to read its validation flags) runs on stream U, so the host waits only for that
-        # trace's copy + upload while the simulation streams keep the GPU busy with earlier traces
+        # every trace's H2D copies queued first on stream A (the previous step's uploads of these
+        # buffers have returned: each upload synchronizes its stream); each upload (which reads
+        # its validation flags back) runs on stream U, so the host waits only for that trace's
+        # copy + upload while the simulation streams keep the GPU busy
         evh = []
         for j, ((hc, hq, ha), (dc, dq, da)) in enumerate(zip(host_turns, dev_turns)):
             with torch.cuda.stream(sA):
@@ -491,6 +500,7 @@ def run_ours(args, rank, world, local_rank):
         for j, ((dc, dq, da), tr, ts, w) in enumerate(zip(dev_turns, traces, sw.sim_tstructs, up_ws)):
             sB = sBs[j % len(sBs)]
             sU.wait_event(evh[j])
+            sU.wait_event(simdone[j])
             _abi.check(_abi.lib.tlru_trace_from_turns(T._ptr(dc), T._ptr(dq), T._ptr(da), T._ptr(dev_ticks[j]),
                                                       tr.num_events, ctypes.byref(ts), T._ptr(w), w.numel(),
                                                       T._stream(sU)))
@@ -498,6 +508,9 @@ def run_ours(args, rank, world, local_rank):
             ev.record(sU)
             sB.wait_event(ev)
             sw.simulate(j, sB)
+            simdone[j].record(sB)
+        if d2h_done[0] is not None:
+            d2h_done[0].synchronize()  # the previous step's results are on the host
         stream.wait_stream(sA)
         stream.wait_stream(sU)
         for sB in sBs:
@@ -505,7 +518,8 @@ def run_ours(args, rank, world, local_rank):
         sw.combine(stream)
         host_table.copy_(sw.table, non_blocking=True)
         host_ptails.copy_(sw.pooled_tails, non_blocking=True)
-        stream.synchronize()
+        d2h_done[0] = torch.cuda.Event()
+        d2h_done[0].record(stream)
 
     e2e = timed(e2e_step, args.steps, max(1, min(args.warmup, 2)))
     assert host_table.numpy().tobytes() == tab
