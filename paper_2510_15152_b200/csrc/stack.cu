@@ -64,6 +64,9 @@ constexpr uint32_t OUT_SMEM = 54u * 1024u;          // s2_out dynamic smem budge
 #endif
 constexpr uint32_t OUT_RANGE_MAX = TLRU_OUT_RANGE;  // events per s2_out CTA (<= 31744: 16-bit counters)
 static_assert(OUT_RANGE_MAX <= 31u * 1024u && OUT_RANGE_MAX % 1024u == 0, "s2_out range");
+#ifndef TLRU_B_EVICT_FIRST
+#define TLRU_B_EVICT_FIRST 1  // measured: s2_out 0.884 -> 0.875 ms per trace
+#endif
 constexpr uint32_t TAB_MAX = 8192;                  // s2_out count table covers capacities < TAB_MAX
 
 struct ChunkDev {
@@ -844,9 +847,17 @@ __global__ void __launch_bounds__(256, 4) s2_out_kernel(const ChunkDev* __restri
           uint16_t* dst = bout + off_s[t] + tlo;
           if (nv16) {
             const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(src + v0));
+#if TLRU_B_EVICT_FIRST
+            uint64_t pol;  // b is written once and never re-read here: evict it from L2 first
+            asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(dst),
+                         "r"(sa), "r"(nv16 * 16u), "l"(pol)
+                         : "memory");
+#else
             asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(sa),
                          "r"(nv16 * 16u)
                          : "memory");
+#endif
           }
           const uint16_t* s16 = reinterpret_cast<const uint16_t*>(src);
           for (uint32_t u = tlo + nv16 * EV; u < thi; ++u) bout[off_s[t] + u] = s16[u - base];  // trace end
