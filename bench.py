@@ -272,8 +272,9 @@ NEXT_FAMILIES = (  # (name, policies, xi values, what) -- DESIGN.md 6, bench --c
 )
 
 
-def measure_next_rows(T, trace, HB, stream):
-    """One batch per NEXT family on one resident config-5 trace: 25 capacities x its xi values x its
+def measure_next_rows(T, traces, HB, stream):
+    """One batch per NEXT family over the resident config-5 traces (at N = 1 all ten: the same
+    workloads as `bench.py --config <name>`): per trace 25 capacities x its xi values x its
     policies; one warm-up call, then one call timed with CUDA events on `stream`."""
     import torch
 
@@ -282,9 +283,9 @@ def measure_next_rows(T, trace, HB, stream):
     T.set_etlru_model(WILDCHAT["death_rate"] * 1e-6, prompt_law_ln_surv(WILDCHAT))
     out = {}
     for name, pols, xis, what in NEXT_FAMILIES:
-        rows = [(0, pol, C, xi, Q_HAT, SLO_BLOCKS) + ((THRESHOLD_BLOCKS,) if pol == 2 else ())
-                for pol in pols for C in CAPS_CONFIG5 for xi in (xis or XI_CONFIG5)]
-        bt = T.prepare_batch([trace], rows, hist_bins=HB)
+        rows = [(t, pol, C, xi, Q_HAT, SLO_BLOCKS) + ((THRESHOLD_BLOCKS,) if pol == 2 else ())
+                for t in range(len(traces)) for pol in pols for C in CAPS_CONFIG5 for xi in (xis or XI_CONFIG5)]
+        bt = T.prepare_batch(list(traces), rows, hist_bins=HB)
         bt.run()
         torch.cuda.synchronize()
         t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -295,14 +296,15 @@ def measure_next_rows(T, trace, HB, stream):
         st = T.last_sim_stats()
         assert st["failed_chains"] == 0
         ms = t0.elapsed_time(t1)
-        req = trace.num_events * len(rows)
+        req = sum(traces[r[0]].num_events for r in rows)
         out[name] = {"value": req / (ms / 1000.0), "unit": "requests/s", "ms": ms, "instances": len(rows),
                      "requests": req, "what": what,
                      "engine": {0: "replay", 1: "stack", 2: "mixed"}.get(st["engine"], str(st["engine"])),
                      "spilled_chains": st["spilled_chains"],
-                     "sample": "rank 0's first config-5 trace (10^6 conversations), resident in HBM; one call of "
-                               "tlru_simulate_batch incl. tail metrics (no generation)"}
+                     "sample": f"rank 0's {len(traces)} config-5 traces (10^6 conversations each), resident in "
+                               "HBM; one call of tlru_simulate_batch incl. tail metrics (no generation)"}
         del bt
+        torch.cuda.empty_cache()
     return out
 
 
@@ -434,12 +436,12 @@ def run_ours(args, rank, world, local_rank):
                    stats=rst)
         del rbatch
 
-    # ---- the paper's other policies on rank 0's first trace, one call each,
+    # ---- the paper's other policies on rank 0's traces, one call each,
     # timed on the device (the trace is already resident; generation is not in these figures).  Before the e2e
     # arm, whose upload without ticks rewrites the trace's time_ticks with event indices
     next_rows = None
     if args.config == "config5" and rank == 0 and not args.no_next and traces:
-        next_rows = measure_next_rows(T, traces[0], HB, stream)
+        next_rows = measure_next_rows(T, traces, HB, stream)
 
     # ---- e2e: the same step through the public API from pinned host buffers (H2D of each trace's
     # turns on stream A, upload + simulation + pooling on the simulation streams, the collectives),
