@@ -14,6 +14,7 @@
 //   * a chain whose live entries exceed W is re-run by the spill kernel with
 //     its state in global memory (never truncated).
 #include <algorithm>
+#include <type_traits>
 #include <mutex>
 #include <vector>
 
@@ -162,7 +163,14 @@ __device__ __forceinline__ void acc_commit(AccDev* acc, uint32_t inst, const Cha
 // One warp per (lane group, segment).  W = state entries per lane (compile-time).
 // AWARE: End-/Length-Aware groups: the segment is the whole trace (their cache is not the
 // top-C of the universe, so no exact warm start exists) and the state keeps per-entry surplus.
-template <int W, bool AWARE, bool NOS = false>
+template <class St>
+__device__ __forceinline__ St make_state(uint32_t* tau_s, uint16_t* X_s, uint16_t* S_s, int lane, uint16_t D,
+                                         uint32_t base) {
+  if constexpr (std::is_same_v<St, SmemStatePk>) return SmemStatePk{tau_s, lane, D, base};
+  else return St{tau_s, X_s, S_s, lane, D};
+}
+
+template <int W, bool AWARE, bool NOS = false, bool PK = false>
 __global__ void __launch_bounds__(32) sim_kernel(const ItemDev* __restrict__ items, const GroupDev* __restrict__ groups,
                                                  const LaneDev* __restrict__ lanes, const TraceDev* __restrict__ traces,
                                                  uint32_t seg_len, uint16_t* __restrict__ bout, AccDev* acc,
@@ -171,7 +179,7 @@ __global__ void __launch_bounds__(32) sim_kernel(const ItemDev* __restrict__ ite
   uint32_t* tau_s = reinterpret_cast<uint32_t*>(smem);
   uint16_t* X_s = reinterpret_cast<uint16_t*>(tau_s + W * 32);
   uint16_t* S_s = X_s + W * 32;
-  uint16_t* bst = (AWARE && !NOS) ? S_s + W * 32 : S_s;
+  uint16_t* bst = PK ? reinterpret_cast<uint16_t*>(tau_s + W * 32) : (AWARE && !NOS) ? S_s + W * 32 : S_s;
   const int lane = threadIdx.x;
   const ItemDev it = items[blockIdx.x];
   const GroupDev g = groups[it.group];
@@ -188,7 +196,8 @@ __global__ void __launch_bounds__(32) sim_kernel(const ItemDev* __restrict__ ite
   lp.policy = lp.xi = 0;
   if (lane < static_cast<int>(g.nlanes)) lp = lanes[g.lane0 + lane];
   bool active = lp.inst != 0xFFFFFFFFu;
-  SmemStateT<NOS> st{tau_s, X_s, S_s, lane, static_cast<uint16_t>(min(lp.D, 65535u))};
+  using St = std::conditional_t<PK, SmemStatePk, SmemStateT<NOS>>;
+  St st = make_state<St>(tau_s, X_s, S_s, lane, static_cast<uint16_t>(min(lp.D, 65535u)), s0);
   ChainRegs c;
   chain_init(c, lp.C, lp.D, lp.T, W, active && s > 0);
   const bool bel = AWARE && g.aware == kAwareBelady;  // warp-uniform
@@ -460,6 +469,9 @@ __global__ void sim_results_kernel(uint32_t ni, const AccDev* acc, tlru_result* 
 }
 
 // ----------------------------------------------------------------------------- planner
+#ifndef TLRU_NOS_PACKED
+#define TLRU_NOS_PACKED 1
+#endif
 #ifndef TLRU_FORCED_BURN
 #define TLRU_FORCED_BURN 8192u  // forced-caching lanes' burn-in (fragments kept only by Phase 2 can be old)
 #endif
@@ -502,6 +514,7 @@ struct Plan {
   std::vector<uint32_t> alane, atrace;       // aware lane -> global lane index, trace
   uint32_t aseg = 8192, aburn = 4096, aburn_long = TLRU_FORCED_BURN, anseg_max = 1, awsnap = 32;
   bool any_forced = false;
+  bool nos_packed = false;  // no-surplus lanes of the 256..1024-entry classes use SmemStatePk
   std::vector<EtItem> et_items;              // ET-LRU instances (etlru.cuh)
   std::vector<EtSeg> et_segs[kNumW];         // their (instance, segment) warps per state class
   uint32_t n_et = 0, et_seg_len = 8192, et_burn = 4096, et_nseg_max = 1, et_wsnap = 32;
@@ -686,6 +699,9 @@ static tlru_status make_plan(const tlru_trace* traces, uint32_t nt, const tlru_i
     uint64_t sa = P->any_forced ? P->aburn_long : 3ull * P->aburn;
     if (g_opt_seg) sa = std::max<uint32_t>(g_opt_seg, 64);  // tests: short segments exercise the fix-up
     P->aseg = static_cast<uint32_t>((sa + 31) & ~31ull);
+    // SmemStatePk's fields: X <= max_history <= 4095 and tau - (segment start - burn-in) < 2^20
+    P->nos_packed = TLRU_NOS_PACKED && maxhist <= 4095u &&
+                    uint64_t(P->aseg) + std::max(P->aburn, P->aburn_long) < (1ull << 20);
   }
   uint64_t nitems = 0;
   for (uint32_t gi = 0; gi < P->groups.size(); ++gi) {
@@ -804,17 +820,17 @@ static tlru_status record(int k, cudaStream_t st) {
   return TLRU_OK;
 }
 
-template <int W, bool AWARE, bool NOS = false>
+template <int W, bool AWARE, bool NOS = false, bool PK = false>
 static tlru_status launch_w(const std::vector<ItemDev>& items, const ItemDev* d_items, const SimWs& w,
                             uint32_t seg_len, uint16_t* bout, cudaStream_t st) {
   if (items.empty()) return TLRU_OK;
-  const size_t smem = size_t(W) * 32 * (sizeof(uint32_t) + ((AWARE && !NOS) ? 2 : 1) * sizeof(uint16_t)) +
-                      32 * BST_STRIDE * sizeof(uint16_t);
-  TLRU_CUDA(cudaFuncSetAttribute(sim_kernel<W, AWARE, NOS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  const size_t smem =
+      size_t(W) * 32 * (sizeof(uint32_t) + (PK ? 0 : ((AWARE && !NOS) ? 2 : 1)) * sizeof(uint16_t)) +
+      32 * BST_STRIDE * sizeof(uint16_t);
+  TLRU_CUDA(cudaFuncSetAttribute(sim_kernel<W, AWARE, NOS, PK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(smem)));
-  sim_kernel<W, AWARE, NOS><<<static_cast<unsigned>(items.size()), 32, smem, st>>>(d_items, w.groups, w.lanes, w.traces,
-                                                                              seg_len, bout, w.acc, w.spill,
-                                                                              w.counters, w.aw);
+  sim_kernel<W, AWARE, NOS, PK><<<static_cast<unsigned>(items.size()), 32, smem, st>>>(
+      d_items, w.groups, w.lanes, w.traces, seg_len, bout, w.acc, w.spill, w.counters, w.aw);
   TLRU_CHECK_LAUNCH();
   ++g_stats.kernels;
   return TLRU_OK;
@@ -1053,12 +1069,18 @@ static tlru_status run_engine(uint32_t engine, const tlru_trace* traces, uint32_
               TLRU_TRY((launch_w<128, true, true>(in_, dn, w, P.seg_len, uncached, st))); break;
       case 4: TLRU_TRY((launch_w<256, false>(P.items[k], d, w, P.seg_len, uncached, st)));
               TLRU_TRY((launch_w<256, true>(ia, da, w, P.seg_len, uncached, st)));
-              TLRU_TRY((launch_w<256, true, true>(in_, dn, w, P.seg_len, uncached, st))); break;
+              if (P.nos_packed) TLRU_TRY((launch_w<256, true, true, true>(in_, dn, w, P.seg_len, uncached, st)));
+              else TLRU_TRY((launch_w<256, true, true>(in_, dn, w, P.seg_len, uncached, st)));
+              break;
       case 5: TLRU_TRY((launch_w<512, false>(P.items[k], d, w, P.seg_len, uncached, st)));
               TLRU_TRY((launch_w<512, true>(ia, da, w, P.seg_len, uncached, st)));
-              TLRU_TRY((launch_w<512, true, true>(in_, dn, w, P.seg_len, uncached, st))); break;
+              if (P.nos_packed) TLRU_TRY((launch_w<512, true, true, true>(in_, dn, w, P.seg_len, uncached, st)));
+              else TLRU_TRY((launch_w<512, true, true>(in_, dn, w, P.seg_len, uncached, st)));
+              break;
       case 6: TLRU_TRY((launch_w<1024, false>(P.items[k], d, w, P.seg_len, uncached, st)));
-              TLRU_TRY((launch_w<1024, true, true>(in_, dn, w, P.seg_len, uncached, st))); break;
+              if (P.nos_packed) TLRU_TRY((launch_w<1024, true, true, true>(in_, dn, w, P.seg_len, uncached, st)));
+              else TLRU_TRY((launch_w<1024, true, true>(in_, dn, w, P.seg_len, uncached, st)));
+              break;
     }
   }
   if (P.n_et) {  // ET-LRU: one warp per (instance, segment), shared-memory state per class

@@ -61,6 +61,42 @@ struct SmemStateT {
 };
 using SmemState = SmemStateT<false>;
 
+// Packed lane-interleaved state for the no-surplus (NOS) lanes with many entries: one 32-bit word
+// per entry, (tau - base) << 12 | X, so a 512-entry lane array takes 64 KB per warp instead of 96
+// (three warps per SM instead of two).  Valid while X <= 4095 (X <= L_after <= the trace's
+// max_history) and tau - base < 2^20 (base = the chain's first event; the host checks both).
+// T(k) / Xr(k) return proxies that read and write their field of the word.
+struct PkT {
+  uint32_t* w;
+  uint32_t base;
+  __device__ __forceinline__ operator uint32_t() const { return (*w >> 12) + base; }
+  __device__ __forceinline__ const PkT& operator=(uint32_t v) const {
+    *w = ((v - base) << 12) | (*w & 0xFFFu);
+    return *this;
+  }
+  __device__ __forceinline__ const PkT& operator=(const PkT& o) const { return *this = static_cast<uint32_t>(o); }
+};
+struct PkX {
+  uint32_t* w;
+  __device__ __forceinline__ operator uint16_t() const { return static_cast<uint16_t>(*w & 0xFFFu); }
+  __device__ __forceinline__ const PkX& operator=(uint32_t v) const {
+    *w = (*w & ~0xFFFu) | (v & 0xFFFu);
+    return *this;
+  }
+  __device__ __forceinline__ const PkX& operator=(const PkX& o) const {
+    return *this = static_cast<uint32_t>(static_cast<uint16_t>(o));
+  }
+};
+struct SmemStatePk {
+  uint32_t* word;
+  int lane;
+  uint16_t D;     // the constant surplus bound (NOS)
+  uint32_t base;  // tau offset
+  __device__ __forceinline__ PkT T(uint32_t k) const { return PkT{word + k * 32u + lane, base}; }
+  __device__ __forceinline__ PkX Xr(uint32_t k) const { return PkX{word + k * 32u + lane}; }
+  __device__ __forceinline__ SConstD Sr(uint32_t) const { return SConstD{D}; }
+};
+
 // Chain-contiguous global-memory state (spill path).
 struct GlobalState {
   uint32_t* tau;
