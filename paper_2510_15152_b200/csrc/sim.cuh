@@ -117,6 +117,9 @@ struct ChainRegs {
   // Tail-Optimized Belady chains: blocks still cached by conversations that never return
   // (all free), and the sum of the entries' remaining surplus
   uint32_t dead, fsum;
+  // Belady chains: every entry at an index >= p1 has S == 0 (an upper bound on the highest entry
+  // with surplus; ~0u = none known), so Phase 1 starts its walk from min(tail, p1)
+  uint32_t p1;
 };
 
 __device__ __forceinline__ void chain_init(ChainRegs& c, uint32_t C, uint32_t D, uint32_t T, uint32_t W,
@@ -138,6 +141,7 @@ __device__ __forceinline__ void chain_init(ChainRegs& c, uint32_t C, uint32_t D,
   c.walking = has_prefix && C > 0;
   c.overflow = false;
   c.dead = c.fsum = 0;
+  c.p1 = 0xFFFFFFFFu;
 }
 
 // One step of the backward walk: e' is an event before the segment start with
@@ -422,6 +426,7 @@ __device__ __forceinline__ bool belady_insert(ChainRegs& c, const St& st, uint32
     if (j == c.W) return false;
     c.tail = j;
     lo = npos;
+    c.p1 = 0xFFFFFFFFu;  // indices remapped: no bound known
   }
   const bool down = c.head > 0 && (c.tail == c.W || lo - c.head <= c.tail - lo);
   if (down) {  // shift [head, lo) one slot towards the front
@@ -430,6 +435,7 @@ __device__ __forceinline__ bool belady_insert(ChainRegs& c, const St& st, uint32
       st.Xr(k - 1) = st.Xr(k);
       st.Sr(k - 1) = st.Sr(k);
     }
+    if (c.p1 <= lo) --c.p1;  // the zero-surplus run [p1, lo) moved down with them
     --c.head;
     --lo;
   } else {  // shift [lo, tail) one slot towards the back
@@ -438,8 +444,10 @@ __device__ __forceinline__ bool belady_insert(ChainRegs& c, const St& st, uint32
       st.Xr(k) = st.Xr(k - 1);
       st.Sr(k) = st.Sr(k - 1);
     }
+    if (c.p1 != 0xFFFFFFFFu && c.p1 >= lo) ++c.p1;
     ++c.tail;
   }
+  if (s > 0 && c.p1 != 0xFFFFFFFFu && c.p1 <= lo) c.p1 = lo + 1;  // the new entry has surplus
   st.T(lo) = key;
   st.Xr(lo) = static_cast<uint16_t>(x);
   st.Sr(lo) = static_cast<uint16_t>(s);
@@ -486,8 +494,11 @@ __device__ __forceinline__ uint32_t chain_request_belady(ChainRegs& c, const St&
     c.dead -= kd;
     over -= kd;
     c.ev_trim += kd;
-    for (uint32_t j = c.tail; over > 0 && c.fsum > 0 && j > c.head;) {
+    uint32_t j = min(c.tail, c.p1);
+    bool walked = false;
+    while (over > 0 && c.fsum > 0 && j > c.head) {
       --j;
+      walked = true;
       if (j == tpos) continue;
       const uint32_t s = st.Sr(j);
       if (s == 0) continue;
@@ -498,6 +509,8 @@ __device__ __forceinline__ uint32_t chain_request_belady(ChainRegs& c, const St&
       over -= take;
       c.ev_trim += take;
     }
+    // every entry above the last one visited has S == 0 now (theta's is counted as surplus)
+    if (walked) c.p1 = (j == tpos || st.Sr(j) > 0) ? j + 1 : j;
     // Phase 2: furthest-in-future, partial; every S is 0 here (theta's aside)
     if (tpos == 0xFFFFFFFFu) {
       while (over > 0 && c.tail > c.head) {
@@ -533,7 +546,10 @@ __device__ __forceinline__ uint32_t chain_request_belady(ChainRegs& c, const St&
     c.used = c.C;
   }
   if (forced) {  // theta rejoins the state
-    if (tpos != 0xFFFFFFFFu) c.fsum += st.Sr(tpos);
+    if (tpos != 0xFFFFFFFFu) {
+      c.fsum += st.Sr(tpos);
+      if (c.p1 != 0xFFFFFFFFu && c.p1 <= tpos) c.p1 = tpos + 1;
+    }
     c.dead += tdead;
   }
   c.max_occ = max(c.max_occ, c.used);
