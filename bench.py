@@ -456,6 +456,20 @@ def run_ours(args, rank, world, local_rank):
     dev_turns = [(torch.empty_like(c, device=dev), torch.empty_like(q, device=dev), torch.empty_like(a, device=dev))
                  for c, q, a in host_turns]
     dev_ticks = [torch.empty_like(h, device=dev) if h is not None else None for h in host_ticks]
+    # the upload's outputs a user of this workload asks for: the simulation view and next links (and
+    # the arrival times when ET-LRU rows read them; is_last when End-/Length-Aware rows do) -- not the
+    # conv / prompt / response copies
+    need_last = any(r[1] in (T.POLICY_END_AWARE, T.POLICY_LENGTH_AWARE) for r in rows_all)
+    up_structs = []
+    for ts in sw.sim_tstructs:
+        u = _abi.Trace()
+        ctypes.pointer(u)[0] = ts
+        u.conv = u.prompt = u.response = None
+        if not need_ticks:
+            u.time_ticks = None
+        if not need_last:
+            u.is_last = None
+        up_structs.append(u)
     up_ws = []
     for tr in traces:
         sz = ctypes.c_size_t()
@@ -499,7 +513,7 @@ def run_ours(args, rank, world, local_rank):
                     dev_ticks[j].copy_(host_ticks[j], non_blocking=True)
             evh.append(torch.cuda.Event())
             evh[-1].record(sA)
-        for j, ((dc, dq, da), tr, ts, w) in enumerate(zip(dev_turns, traces, sw.sim_tstructs, up_ws)):
+        for j, ((dc, dq, da), tr, ts, w) in enumerate(zip(dev_turns, traces, up_structs, up_ws)):
             sB = sBs[j % len(sBs)]
             sU.wait_event(evh[j])
             sU.wait_event(simdone[j])
