@@ -199,3 +199,30 @@ def test_long_prompt_law_table(T):
     rows = [(0, ET, C, xi, 0, 8) for C in (50, 300, 1500) for xi in (200, 450, 690)]
     bt = T.simulate_batch([tr], rows)
     check_et(bt, rows, [(conv, q, a, ticks)], 0.03, tab)
+
+
+@pytest.mark.parametrize("entries", [256, 512, 1024])
+def test_incremental_candidates_forced_class(T, entries):
+    """ET-LRU / forced ET-LRU in the slot classes that keep incremental eviction candidates
+    (et_rescan / et_offer), forced onto small random traces with short segments (the fix-up path
+    loads snapshots into them): element by element against the oracle."""
+    mu = 0.3
+    T.set_etlru_model(mu, TABLES[0])
+    rng = np.random.default_rng(entries)
+    conv, q, a = random_trace(4300 + entries, 4000, 60, q_max=5, a_max=7, locality=0.5)
+    ticks = np.cumsum(rng.integers(0, 3, size=conv.size)).astype(np.uint64)
+    tr = upload_ticks(T, conv, q, a, ticks)
+    rows = [(0, pol, C, xi, 0, 8) for pol in (ET, 9) for C in (0, 2, 15, 60, 250) for xi in (0, 3, 9)]
+    for seg in (0, 256):
+        T.set_sim_options(seg, entries)
+        try:
+            bt = T.simulate_batch([tr], rows)
+            assert T.last_sim_stats()["failed_chains"] == 0
+        finally:
+            T.set_sim_options(0, 0)
+        for i, (t, pol, C, xi, qh, slo) in enumerate(rows):
+            o = O.replay_etlru(conv, q, a, ticks, C, xi, mu, TABLES[0], forced=pol != ET)
+            assert np.array_equal(bt.b(i).astype(np.uint64), o.b), (seg, rows[i])
+            r = bt.results_numpy()[i]
+            assert (r["evicted_trim"], r["evicted_lru"], r["max_occupancy"]) == (o.evicted_trim, o.evicted_lru,
+                                                                               o.max_occupancy), (seg, rows[i])

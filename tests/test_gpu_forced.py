@@ -84,3 +84,21 @@ def test_full_size_sampled(T):
         assert np.array_equal(bt.b(i).astype(np.uint64), r.b), (C, xi)
         assert (res[i]["evicted_trim"], res[i]["evicted_lru"], res[i]["max_occupancy"]) == (
             r.evicted_trim, r.evicted_lru, r.max_occupancy)
+
+
+@pytest.mark.parametrize("entries", [256, 512, 1024])
+def test_packed_lanes_forced_class(T, entries):
+    """Forced-caching T-LRU and End-Aware lanes forced into the 256..1024-entry classes, whose
+    no-surplus state is packed ((tau - chain start) << 12 | X, SmemStatePk), with short segments
+    (snapshots of packed lanes go through the fix-up): against the oracle."""
+    conv, q, a = random_trace(5300 + entries, 5000, 90, q_max=6, a_max=9, locality=0.4)
+    tr = upload(T, conv, q, a)
+    rows = [(0, pol, C, xi, 2, 8) for pol in (FORCED, 3) for C in (0, 5, 40, 300) for xi in (0, 6, 20)]
+    for seg in (0, 512):
+        T.set_sim_options(seg, entries)
+        try:
+            bt = T.simulate_batch([tr], rows)
+            assert T.last_sim_stats()["failed_chains"] == 0
+        finally:
+            T.set_sim_options(0, 0)
+        check(T, bt, rows, [(conv, q, a)])
