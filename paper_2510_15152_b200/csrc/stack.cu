@@ -64,6 +64,10 @@ constexpr uint32_t OUT_SMEM = 54u * 1024u;          // s2_out dynamic smem budge
 #endif
 constexpr uint32_t OUT_RANGE_MAX = TLRU_OUT_RANGE;  // events per s2_out CTA (<= 31744: 16-bit counters)
 static_assert(OUT_RANGE_MAX <= 31u * 1024u && OUT_RANGE_MAX % 1024u == 0, "s2_out range");
+#ifndef TLRU_OUT_WRANGE
+#define TLRU_OUT_WRANGE 32768u  // measured: 2048 / 4096 / 8192 -> s2_out 1.21 / 1.02 / 0.92 ms vs 0.87 (no split)
+#endif
+constexpr uint32_t OUT_WRANGE = TLRU_OUT_WRANGE;  // s2_out writer groups: events per CTA (a multiple of 2048)
 #ifndef TLRU_WIN_EVICT_LAST
 #define TLRU_WIN_EVICT_LAST 1  // measured: s2_win 0.331 -> 0.308 ms per trace, step -0.2 ms
 #endif
@@ -711,7 +715,8 @@ __global__ void __launch_bounds__(256, 4) s2_out_kernel(const ChunkDev* __restri
                                                      const uint32_t* __restrict__ LbJ, uint32_t E, uint32_t range_len,
                                                      uint32_t bins, uint32_t rows, uint32_t tcap, bool aligned16,
                                                      uint16_t* __restrict__ bout, uint32_t* __restrict__ hist,
-                                                     const uint4* __restrict__ cnt_g, uint32_t range0,
+                                                     const uint4* __restrict__ cnt_g, uint32_t n_w, uint32_t n_h,
+                                                     uint32_t sub,
                                                      const CellDev* __restrict__ cells, uint32_t* __restrict__ gcell) {
   // [rows >= group size][hb2] difference rows, two 16-bit counters per word (bins 2v, 2v+1).  The
   // counters wrap into each other, but a word's final value is lo + 65536 * hi (mod 2^32) and
@@ -722,10 +727,27 @@ __global__ void __launch_bounds__(256, 4) s2_out_kernel(const ChunkDev* __restri
   __shared__ uint64_t off_s[GI_MAX];
   // cnt[v] = #{i : C_i <= v} for v < tcap, after the histogram rows (used when C_{n-1} < tcap)
   uint8_t* cnt = reinterpret_cast<uint8_t*>(hw + ((rows * hb2 + 3u) & ~3u));  // 16-byte aligned
-  // grid (groups, ranges): groups fastest, so the CTAs resident at one time share event ranges
-  // (the per-event inputs LbJ / A_nf are read once from DRAM and then hit in L2)
-  const GroupDev g = groups[blockIdx.x];
-  const uint32_t rid = range0 + blockIdx.y;
+  // 1-D grid, per event range of range_len events: its histogram groups (the chunk's groups
+  // [n_w, ng)), then its writer groups [0, n_w) over `sub` sub-ranges of range_len / sub events,
+  // groups fastest -- CTAs resident at one time share event ranges (the per-event inputs LbJ / A_nf
+  // are read once from DRAM and then hit in L2), and writers run short ranges (their bulk-store
+  // pattern is faster with fewer tiles per CTA) while the histogram groups keep long ones (their
+  // per-CTA flush of the difference rows).
+  const uint32_t per = n_h + n_w * sub;
+  const uint32_t kr = blockIdx.x / per, rr = blockIdx.x % per;
+  uint32_t gi, e_begin, e_end;
+  if (rr < n_h) {
+    gi = n_w + rr;
+    e_begin = kr * range_len;
+    e_end = min(E, e_begin + range_len);
+  } else {
+    const uint32_t wsub = range_len / sub, w = rr - n_h;
+    gi = w % n_w;
+    e_begin = kr * range_len + (w / n_w) * wsub;
+    e_end = min(E, e_begin + wsub);
+  }
+  if (e_begin >= E) return;
+  const GroupDev g = groups[gi];
   const uint32_t t = threadIdx.x, n = g.n;
   const bool hist_group = g.kind != 0;  // else a writer group: b rows only
   const uint32_t D = chunk->D[g.d], nsat = totals->nsat[g.d], inst0 = chunk->inst0;
@@ -766,7 +788,7 @@ __global__ void __launch_bounds__(256, 4) s2_out_kernel(const ChunkDev* __restri
     run_s[t] = j;
   }
   if (hist_group && use_cnt) {  // the group's table, built once by s2_cnt_kernel
-    const uint4* src = cnt_g + uint64_t(blockIdx.x) * ((tcap + 15u) >> 4);
+    const uint4* src = cnt_g + uint64_t(gi) * ((tcap + 15u) >> 4);
     for (uint32_t k = t; k < (tcap + 15u) >> 4; k += blockDim.x) reinterpret_cast<uint4*>(cnt)[k] = src[k];
   }
   __syncthreads();
@@ -777,7 +799,6 @@ __global__ void __launch_bounds__(256, 4) s2_out_kernel(const ChunkDev* __restri
     if (j < n) hadd(j, v, -1);
   };
   const AT* Ad = A + uint64_t(g.d) * Astride;
-  const uint32_t e_begin = rid * range_len, e_end = min(E, e_begin + range_len);
   constexpr uint32_t EV = 8;  // events per thread per tile: one 16-byte store per instance
   const uint32_t stride = EV * blockDim.x;
   const uint32_t D2 = min(D, 65535u) * 0x10001u;  // NF(L) = max(L, D) - D per 16-bit half (L <= 65535)
@@ -1257,6 +1278,12 @@ static tlru_status launch_s2(const tlru_trace& tr, const ChunkDev* ch, const Chu
   const uint32_t nr = std::max<uint32_t>(1u, (target + ng - 1) / std::max<uint32_t>(ng, 1u));
   uint32_t rl = (E + nr - 1) / nr;
   rl = std::min(OUT_RANGE_MAX, (rl + 1023u) & ~1023u);
+  // writer sub-ranges of OUT_WRANGE events inside the histogram groups' ranges
+  uint32_t sub = 1;
+  if (rl > OUT_WRANGE) {
+    sub = std::min(OUT_RANGE_MAX / OUT_WRANGE, (rl + OUT_WRANGE - 1) / OUT_WRANGE);
+    rl = sub * OUT_WRANGE;
+  }
   const uint32_t nranges = (E + rl - 1) / rl;
   // histogram groups: rows + count table; writer groups (TMA path): 3 stage slots x 4 runs x 4 KB
   const size_t out_smem = std::max<size_t>(((size_t(P.gi) * ((bins + 1) / 2) + 3) & ~size_t(3)) * sizeof(uint32_t) +
@@ -1276,11 +1303,15 @@ static tlru_status launch_s2(const tlru_trace& tr, const ChunkDev* ch, const Chu
       TLRU_CHECK_LAUNCH();
       TLRU_CUDA(cudaMemsetAsync(w.gcell, 0, size_t(ncell) * bins * sizeof(uint32_t), st));
     }
-    for (uint32_t r0 = 0; ng && r0 < nranges; r0 += 65535u) {  // grid.y <= 65535
+    uint32_t n_w = 0;  // the chunk's writer groups come first (make_stack_plan)
+    while (n_w < ng && P.groups[g0 + n_w].kind == 0) ++n_w;
+    const uint32_t n_h = ng - n_w;
+    if (ng) {
       if (ot && ot->first && ot->launches == 0) TLRU_CUDA(cudaEventRecord(ot->first, st));
-      s2_out_kernel<AT, HT><<<dim3(ng, std::min(65535u, nranges - r0)), 256, out_smem, st>>>(
+      const uint64_t nblk = uint64_t(nranges) * (n_h + uint64_t(n_w) * sub);
+      s2_out_kernel<AT, HT><<<static_cast<unsigned>(nblk), 256, out_smem, st>>>(
           ch, w.insts, w.groups + g0, tot, Aptr, w.Astride, w.LbJ, E, rl, bins, P.gi, P.tcap, aligned16, bout, hist,
-          reinterpret_cast<const uint4*>(cnt_g), r0, cells, w.gcell);
+          reinterpret_cast<const uint4*>(cnt_g), n_w, n_h, sub, cells, w.gcell);
       TLRU_CHECK_LAUNCH();
       if (ot && ot->last) {
         TLRU_CUDA(cudaEventRecord(ot->last, st));
