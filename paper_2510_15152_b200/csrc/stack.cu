@@ -57,7 +57,10 @@ constexpr uint32_t GI_MAX = 64;                     // instances per s2_out grou
 // one 16-byte store per instance row per 8 events, and the write stream loses DRAM efficiency
 // as the number of rows a CTA interleaves grows (tools/write_bw.cu: 7.4 TB/s with one row per
 // CTA, 5.9-6.9 with 8, 4.9 with 35); smaller groups re-read the per-event inputs more often.
-constexpr uint32_t GI_CAP = 16;
+#ifndef TLRU_GI_CAP
+#define TLRU_GI_CAP 16u
+#endif
+constexpr uint32_t GI_CAP = TLRU_GI_CAP;
 constexpr uint32_t OUT_SMEM = 54u * 1024u;          // s2_out dynamic smem budget: 4 CTAs per SM
 #ifndef TLRU_OUT_RANGE
 #define TLRU_OUT_RANGE (31u * 1024u)
