@@ -22,6 +22,10 @@
 #include "sim.cuh"
 #include "stack.cuh"
 
+#ifndef TLRU_XS_PAIRS
+#define TLRU_XS_PAIRS 1  // lanes with a surplus array keep (X, S) as interleaved halfword pairs
+#endif
+
 namespace tlru {
 
 struct LaneDev {
@@ -167,6 +171,7 @@ template <class St>
 __device__ __forceinline__ St make_state(uint32_t* tau_s, uint16_t* X_s, uint16_t* S_s, int lane, uint16_t D,
                                          uint32_t base) {
   if constexpr (std::is_same_v<St, SmemStatePk>) return SmemStatePk{tau_s, lane, D, base};
+  else if constexpr (std::is_same_v<St, SmemStateXS>) return SmemStateXS{tau_s, X_s, lane};
   else return St{tau_s, X_s, S_s, lane, D};
 }
 
@@ -196,7 +201,8 @@ __global__ void __launch_bounds__(32) sim_kernel(const ItemDev* __restrict__ ite
   lp.policy = lp.xi = 0;
   if (lane < static_cast<int>(g.nlanes)) lp = lanes[g.lane0 + lane];
   bool active = lp.inst != 0xFFFFFFFFu;
-  using St = std::conditional_t<PK, SmemStatePk, SmemStateT<NOS>>;
+  using St = std::conditional_t<PK, SmemStatePk,
+                                std::conditional_t<(AWARE && !NOS && TLRU_XS_PAIRS), SmemStateXS, SmemStateT<NOS>>>;
   St st = make_state<St>(tau_s, X_s, S_s, lane, static_cast<uint16_t>(min(lp.D, 65535u)), s0);
   ChainRegs c;
   chain_init(c, lp.C, lp.D, lp.T, W, active && s > 0);

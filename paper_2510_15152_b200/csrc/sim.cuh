@@ -58,8 +58,33 @@ struct SmemStateT {
     if constexpr (NOS) return SConstD{D};
     else return (S[k * 32u + lane]);
   }
+  template <bool WITH_S>
+  __device__ __forceinline__ void move(uint32_t d, uint32_t s) const {  // entry s -> entry d
+    T(d) = T(s);
+    Xr(d) = Xr(s);
+    if constexpr (WITH_S && !NOS) Sr(d) = Sr(s);
+  }
 };
 using SmemState = SmemStateT<false>;
+
+// Lanes with a surplus array (End-/Length-Aware, Belady): tau array + interleaved (X, S) halfword
+// pairs, entry k of lane l at tau[k * 32 + l] and xs[2 (k * 32 + l)] (X), [... + 1] (S), so moving an
+// entry (compaction, Belady's sorted-insert shifts) is two 4-byte copies instead of three.
+struct SmemStateXS {
+  uint32_t* tau;
+  uint16_t* xs;
+  int lane;
+  __device__ __forceinline__ uint32_t& T(uint32_t k) const { return tau[k * 32u + lane]; }
+  __device__ __forceinline__ uint16_t& Xr(uint32_t k) const { return xs[2u * (k * 32u + lane)]; }
+  __device__ __forceinline__ uint16_t& Sr(uint32_t k) const { return xs[2u * (k * 32u + lane) + 1u]; }
+  template <bool WITH_S>
+  __device__ __forceinline__ void move(uint32_t d, uint32_t s) const {
+    T(d) = T(s);
+    uint32_t* w = reinterpret_cast<uint32_t*>(xs);
+    if constexpr (WITH_S) w[d * 32u + lane] = w[s * 32u + lane];
+    else Xr(d) = Xr(s);
+  }
+};
 
 // Packed lane-interleaved state for the no-surplus (NOS) lanes with many entries: one 32-bit word
 // per entry, (tau - base) << 12 | X, so a 512-entry lane array takes 64 KB per warp instead of 96
@@ -95,6 +120,10 @@ struct SmemStatePk {
   __device__ __forceinline__ PkT T(uint32_t k) const { return PkT{word + k * 32u + lane, base}; }
   __device__ __forceinline__ PkX Xr(uint32_t k) const { return PkX{word + k * 32u + lane}; }
   __device__ __forceinline__ SConstD Sr(uint32_t) const { return SConstD{D}; }
+  template <bool WITH_S>
+  __device__ __forceinline__ void move(uint32_t d, uint32_t s) const {  // tau and X share the word; same base
+    word[d * 32u + lane] = word[s * 32u + lane];
+  }
 };
 
 // Chain-contiguous global-memory state (spill path).
@@ -105,6 +134,12 @@ struct GlobalState {
   __device__ __forceinline__ uint32_t& T(uint32_t k) const { return tau[k]; }
   __device__ __forceinline__ uint16_t& Xr(uint32_t k) const { return X[k]; }
   __device__ __forceinline__ uint16_t& Sr(uint32_t k) const { return S[k]; }
+  template <bool WITH_S>
+  __device__ __forceinline__ void move(uint32_t d, uint32_t s) const {
+    tau[d] = tau[s];
+    X[d] = X[s];
+    if constexpr (WITH_S) S[d] = S[s];
+  }
 };
 
 struct ChainRegs {
@@ -210,12 +245,8 @@ __device__ __forceinline__ bool chain_compact(ChainRegs& c, const St& st) {
   const bool fh_dead = (c.fh < c.tail) && st.Xr(c.fh) == 0;
   for (uint32_t k = c.head; k < c.tail; ++k) {
     if (k == c.fh) new_fh = j;
-    uint16_t x = st.Xr(k);
-    if (x != 0) {
-      uint32_t t = st.T(k);
-      st.T(j) = t;
-      st.Xr(j) = x;
-      if (AWARE) st.Sr(j) = st.Sr(k);
+    if (st.Xr(k) != 0) {
+      if (j != k) st.template move<AWARE>(j, k);
       ++j;
     }
   }
@@ -414,11 +445,8 @@ __device__ __forceinline__ bool belady_insert(ChainRegs& c, const St& st, uint32
     uint32_t j = 0, npos = 0;
     for (uint32_t k = 0; k < c.tail; ++k) {
       if (k == lo) npos = j;
-      const uint16_t xk = st.Xr(k);
-      if (xk != 0) {
-        st.T(j) = st.T(k);
-        st.Xr(j) = xk;
-        st.Sr(j) = st.Sr(k);
+      if (st.Xr(k) != 0) {
+        if (j != k) st.template move<true>(j, k);
         ++j;
       }
     }
@@ -430,20 +458,12 @@ __device__ __forceinline__ bool belady_insert(ChainRegs& c, const St& st, uint32
   }
   const bool down = c.head > 0 && (c.tail == c.W || lo - c.head <= c.tail - lo);
   if (down) {  // shift [head, lo) one slot towards the front
-    for (uint32_t k = c.head; k < lo; ++k) {
-      st.T(k - 1) = st.T(k);
-      st.Xr(k - 1) = st.Xr(k);
-      st.Sr(k - 1) = st.Sr(k);
-    }
+    for (uint32_t k = c.head; k < lo; ++k) st.template move<true>(k - 1, k);
     if (c.p1 <= lo) --c.p1;  // the zero-surplus run [p1, lo) moved down with them
     --c.head;
     --lo;
   } else {  // shift [lo, tail) one slot towards the back
-    for (uint32_t k = c.tail; k > lo; --k) {
-      st.T(k) = st.T(k - 1);
-      st.Xr(k) = st.Xr(k - 1);
-      st.Sr(k) = st.Sr(k - 1);
-    }
+    for (uint32_t k = c.tail; k > lo; --k) st.template move<true>(k, k - 1);
     if (c.p1 != 0xFFFFFFFFu && c.p1 >= lo) ++c.p1;
     ++c.tail;
   }
