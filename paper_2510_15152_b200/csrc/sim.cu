@@ -826,6 +826,36 @@ static tlru_status record(int k, cudaStream_t st) {
   return TLRU_OK;
 }
 
+#ifndef TLRU_CLASS_STREAMS
+#define TLRU_CLASS_STREAMS 4
+#endif
+// The per-state-class kernels of one batch are independent (disjoint instances); each class's
+// last wave leaves SMs idle, so they are forked over a small per-(host thread, device) pool of
+// streams and joined back onto the caller's stream before the fix-up kernels.
+struct ClassStreams {
+  cudaStream_t s[TLRU_CLASS_STREAMS];
+  cudaEvent_t fork, join[TLRU_CLASS_STREAMS];
+  bool init = false;
+};
+static thread_local ClassStreams g_class_streams[16];  // per host thread: distinct callers never share
+
+static tlru_status class_streams(ClassStreams** out) {
+  int dev = 0;
+  TLRU_CUDA(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 16) TLRU_FAIL(TLRU_EUNSUPPORTED, "device %d", dev);
+  ClassStreams& c = g_class_streams[dev];
+  if (!c.init) {
+    for (int i = 0; i < TLRU_CLASS_STREAMS; ++i) {
+      TLRU_CUDA(cudaStreamCreateWithFlags(&c.s[i], cudaStreamNonBlocking));
+      TLRU_CUDA(cudaEventCreateWithFlags(&c.join[i], cudaEventDisableTiming));
+    }
+    TLRU_CUDA(cudaEventCreateWithFlags(&c.fork, cudaEventDisableTiming));
+    c.init = true;
+  }
+  *out = &c;
+  return TLRU_OK;
+}
+
 template <int W, bool AWARE, bool NOS = false, bool PK = false>
 static tlru_status launch_w(const std::vector<ItemDev>& items, const ItemDev* d_items, const SimWs& w,
                             uint32_t seg_len, uint16_t* bout, cudaStream_t st) {
@@ -1052,9 +1082,20 @@ static tlru_status run_engine(uint32_t engine, const tlru_trace* traces, uint32_
   }
   TLRU_CUDA(cudaMemsetAsync(w.hist, 0, uint64_t(ni) * P.bins * sizeof(uint32_t), st));
   TLRU_CUDA(cudaMemsetAsync(w.clamped, 0, ni * sizeof(unsigned long long), st));
-  // K2: largest state class first (longest per-event latency)
+  // K2: largest state class first (longest per-event latency); classes forked over the pool
   if (timing) TLRU_TRY(record(0, st));
+  ClassStreams* cs = nullptr;
+  const bool fork = TLRU_CLASS_STREAMS > 1;
+  if (fork) {
+    TLRU_TRY(class_streams(&cs));
+    TLRU_CUDA(cudaEventRecord(cs->fork, st));
+    for (int i = 0; i < TLRU_CLASS_STREAMS; ++i) TLRU_CUDA(cudaStreamWaitEvent(cs->s[i], cs->fork, 0));
+  }
+  const cudaStream_t st_caller = st;
+  int rr = 0;
+  auto next_stream = [&]() { return fork ? cs->s[(rr++) % TLRU_CLASS_STREAMS] : st_caller; };
   for (int k = kNumW - 1; k >= 0; --k) {
+    const cudaStream_t st = next_stream();
     const ItemDev* d = w.items + item_off[k];
     const ItemDev* da = w.items + aware_off[k];
     const std::vector<ItemDev>& ia = P.items_aware[k];
@@ -1094,6 +1135,7 @@ static tlru_status run_engine(uint32_t engine, const tlru_trace* traces, uint32_
     for (int k = kNumW - 1; k >= 0; --k) {
       const std::vector<EtSeg>& v = P.et_segs[k];
       const EtSeg* d = w.et_segs + et_off[k];
+      const cudaStream_t st = v.empty() ? st_caller : next_stream();
       switch (k) {
         case 0: TLRU_TRY((launch_et<32>(v, d, w, m, uncached, st))); break;
         case 1: TLRU_TRY((launch_et<64>(v, d, w, m, uncached, st))); break;
@@ -1104,6 +1146,15 @@ static tlru_status run_engine(uint32_t engine, const tlru_trace* traces, uint32_
         case 6: TLRU_TRY((launch_et<1024>(v, d, w, m, uncached, st))); break;
       }
     }
+  }
+  if (fork) {  // join every class kernel back onto the caller's stream before the fix-up kernels
+    for (int i = 0; i < TLRU_CLASS_STREAMS; ++i) {
+      TLRU_CUDA(cudaEventRecord(cs->join[i], cs->s[i]));
+      TLRU_CUDA(cudaStreamWaitEvent(st_caller, cs->join[i], 0));
+    }
+  }
+  if (P.n_et) {
+    const EtModel m{w.et_table, static_cast<uint32_t>(g_et_table.size() - 1), g_et_mu};
     // fix-up: re-run every segment whose start state was not exact (or that outgrew its slots)
     etlru_fix_kernel<<<P.n_et, 32, 0, st>>>(w.et_items, P.n_et, w.traces, m, w.et_sg, uncached, w.acc, w.et_gpool,
                                             P.W_big, w.counters + 3, w.counters + 1);
