@@ -837,13 +837,19 @@ struct ClassStreams {
   cudaEvent_t fork, join[TLRU_CLASS_STREAMS];
   bool init = false;
 };
-static thread_local ClassStreams g_class_streams[16];  // per host thread: distinct callers never share
+// per (host thread, device, caller stream): callers on distinct streams never share a pool, so their
+// batches still overlap each other
+static thread_local std::vector<std::pair<cudaStream_t, ClassStreams>> g_class_streams[16];
 
-static tlru_status class_streams(ClassStreams** out) {
+static tlru_status class_streams(cudaStream_t caller, ClassStreams** out) {
   int dev = 0;
   TLRU_CUDA(cudaGetDevice(&dev));
   if (dev < 0 || dev >= 16) TLRU_FAIL(TLRU_EUNSUPPORTED, "device %d", dev);
-  ClassStreams& c = g_class_streams[dev];
+  auto& pools = g_class_streams[dev];
+  size_t idx = 0;
+  while (idx < pools.size() && pools[idx].first != caller) ++idx;
+  if (idx == pools.size()) pools.emplace_back(caller, ClassStreams{});
+  ClassStreams& c = pools[idx].second;
   if (!c.init) {
     for (int i = 0; i < TLRU_CLASS_STREAMS; ++i) {
       TLRU_CUDA(cudaStreamCreateWithFlags(&c.s[i], cudaStreamNonBlocking));
@@ -1087,7 +1093,7 @@ static tlru_status run_engine(uint32_t engine, const tlru_trace* traces, uint32_
   ClassStreams* cs = nullptr;
   const bool fork = TLRU_CLASS_STREAMS > 1;
   if (fork) {
-    TLRU_TRY(class_streams(&cs));
+    TLRU_TRY(class_streams(st, &cs));
     TLRU_CUDA(cudaEventRecord(cs->fork, st));
     for (int i = 0; i < TLRU_CLASS_STREAMS; ++i) TLRU_CUDA(cudaStreamWaitEvent(cs->s[i], cs->fork, 0));
   }
@@ -1135,7 +1141,9 @@ static tlru_status run_engine(uint32_t engine, const tlru_trace* traces, uint32_
     for (int k = kNumW - 1; k >= 0; --k) {
       const std::vector<EtSeg>& v = P.et_segs[k];
       const EtSeg* d = w.et_segs + et_off[k];
-      const cudaStream_t st = v.empty() ? st_caller : next_stream();
+      // ET-LRU classes stay on the caller's stream, largest first: forked, the small classes' warps
+      // took SM slots from the largest class (the critical path) -- 10-trace workload 6.3e8 -> 5.6e8
+      const cudaStream_t st = st_caller;
       switch (k) {
         case 0: TLRU_TRY((launch_et<32>(v, d, w, m, uncached, st))); break;
         case 1: TLRU_TRY((launch_et<64>(v, d, w, m, uncached, st))); break;
