@@ -50,8 +50,9 @@ def peaks():
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def _clock_sampler_proc(index, go, stop, out):
-    """Child process (no CUDA): polls NVML every 5 ms between `go` and `stop`."""
+def _clock_sampler_proc(index, go, stop, out, count):
+    """Child process (no CUDA): polls NVML every 5 ms between `go` and `stop` (at least once);
+    `count` tells the parent how many samples it has taken."""
     res = {"sm": [], "mx": 0, "reasons": 0, "error": None}
     try:
         import pynvml as nv
@@ -59,12 +60,16 @@ def _clock_sampler_proc(index, go, stop, out):
         h = nv.nvmlDeviceGetHandleByIndex(index)
         res["mx"] = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
         go.wait()
-        while not stop.is_set():
+        while True:
             res["sm"].append(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
             res["reasons"] |= int(nv.nvmlDeviceGetCurrentClocksEventReasons(h))
+            count.value += 1
+            if stop.is_set():
+                break
             time.sleep(0.005)
     except Exception as ex:  # noqa: BLE001 -- report, never fail the bench
         res["error"] = repr(ex)
+        count.value += 1
     out.put(res)
 
 
@@ -79,12 +84,17 @@ class ClockSampler:
         import multiprocessing as mp
         ctx = mp.get_context("fork")
         self.go, self.stop, self.q = ctx.Event(), ctx.Event(), ctx.Queue()
-        self.p = ctx.Process(target=_clock_sampler_proc, args=(index, self.go, self.stop, self.q), daemon=True)
+        self.count = ctx.Value("i", 0)
+        self.p = ctx.Process(target=_clock_sampler_proc, args=(index, self.go, self.stop, self.q, self.count),
+                             daemon=True)
         self.p.start()  # NVML init happens before the timed region
         self.res = None
 
     def __enter__(self):
         self.go.set()
+        t_end = time.time() + 10.0  # the sampler is polling before the timed region starts
+        while self.count.value == 0 and time.time() < t_end and self.p.is_alive():
+            time.sleep(0.001)
         return self
 
     def __exit__(self, *a):
